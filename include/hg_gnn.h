@@ -1,0 +1,177 @@
+/*
+ * hg_gnn — C ABI of the B200-native sample-based GNN training hot path
+ * (NeutronOrch, arXiv 2311.13225; reference package `hetgnn` v0.1.0).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every pointer argument is DEVICE memory
+ *    unless the parameter name says `host_`; the caller allocates every buffer
+ *    including workspaces (sizes from the *_ws_size functions, in elements of
+ *    the pointer's type).  The library keeps no allocations and no global
+ *    mutable state; all entry points are reentrant.
+ *  - `stream` is a cudaStream_t (CUstream) passed as void*; work is enqueued
+ *    asynchronously on it.  Nothing synchronises the host.
+ *  - Counts that are produced by a previous step (frontier sizes, edge counts)
+ *    are passed as `const int32_t* d_n` device pointers together with a host
+ *    upper bound `cap`; a NULL d_n means "exactly cap".  This lets a whole
+ *    training step be captured into one CUDA graph.
+ *  - Vertex ids are int32 on device (V < 2^31); CSR offsets are int64.
+ *  - Return value: 0 on success, < 0 on error (-1 invalid argument, -2 CUDA
+ *    launch error, -3 unsupported shape); hg_last_error() has the message
+ *    (thread-local).  The Python layer maps these onto the reference's
+ *    exception classes (SamplerError, ShapeError, ...).
+ *
+ * Each entry point names the reference interface it replaces (file:line in
+ * /root/reference/pkg/src/hetgnn).
+ */
+#ifndef HG_GNN_H
+#define HG_GNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_GNN_ABI_VERSION 1
+
+int hg_abi_version(void);
+int hg_last_error(char* buf, int len);
+
+/* ---- splitmix64 streams: kernels.py:51-70 (_mix64, derive_seed) -------- */
+uint64_t hg_mix64_host(uint64_t x);
+uint64_t hg_derive_seed(uint64_t seed, const uint64_t* host_parts, int n_parts);
+
+/* ---- K1 neighbour draw: kernels.py:77-118,147-158 (_sample_layer /
+ *      sample_layer).  layer >= 0: *d_seed is the batch rng seed and the
+ *      stream is derive_seed(seed, 0x5A, layer) (sampler.py:143); layer < 0:
+ *      *d_seed is the stream seed itself.  Writes counts[i] = min(deg, f) and
+ *      the drawn global ids into slots[i*f + j] (emission order), and
+ *      atomicMin's first-occurrence positions into minpos[V] (all INT32_MAX at
+ *      rest).  scratch: cap_dst*2*fanout ints, used only when fanout > 32. */
+int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                    const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                    int32_t layer, int32_t* counts, int32_t* slots, int32_t* minpos, int32_t* scratch,
+                    void* stream);
+
+/* ---- K2/K3 dedup + relabel + (dst, src) order: kernels.py:166-180
+ *      (stable_unique) and sampler.py:104-118 (_expand_frontier lexsort).
+ *      Produces src_vertices (first-occurrence order, dst prefix first),
+ *      *d_n_src, slots re-ordered by local src id with slot_local, per-dst
+ *      non-self counts `nself` (gnnmath.py:145-154; nullable) and block
+ *      out-degrees `outdeg` (gnnmath.py:96; nullable, zeroed by caller), and
+ *      restores minpos. */
+int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout);
+int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                     const int32_t* counts, int32_t* slots, int32_t* slot_local, int32_t* minpos,
+                     int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
+                     int32_t* outdeg, int32_t* ws, void* stream);
+
+/* Block.edge_src / edge_dst (sampler.py:45-78) from the slot form. */
+int64_t hg_block_edges_ws_size(int32_t cap_dst);
+int hg_block_to_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                      const int32_t* slot_local, int32_t* edge_src, int32_t* edge_dst, int32_t* d_n_edges,
+                      int32_t* ws, void* stream);
+/* Raw emission (edge_dst_local, edge_src_global) of kernels.sample_layer. */
+int hg_raw_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                 const int32_t* slots, int32_t* edge_dst, int32_t* edge_src, int32_t* d_n_edges, int32_t* ws,
+                 void* stream);
+
+/* Stable src-major view for the transposed aggregation (gnnmath.py:140,199). */
+int64_t hg_csc_ws_size(int32_t cap_dst, int32_t fanout);
+int hg_build_csc(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                 const int32_t* slot_local, int32_t cap_src, int32_t* csc_slot, int32_t* seg_beg,
+                 int32_t* seg_end, int32_t* ws, void* stream);
+
+/* ---- generic plug-in kernels (numpy-shaped API) ------------------------- */
+/* kernels.stable_unique (kernels.py:166-180) for arbitrary int64 values. */
+int64_t hg_unique_ws_size(int64_t n);
+int hg_unique_first_i64(const int64_t* vals, int64_t n, int64_t* uniq, int64_t* inverse, int32_t* d_n_uniq,
+                        int32_t* ws, void* stream);
+/* kernels.count_into (kernels.py:161-163). */
+int hg_count_into(int64_t* counter, const int32_t* ids, const int32_t* d_n, int32_t cap, void* stream);
+int hg_count_into_i64(int64_t* counter, const int64_t* ids, int64_t n, void* stream);
+/* kernels.segment_weighted_rows (kernels.py:121-144), fp64, bit-exact. */
+int64_t hg_swr_ws_size(int64_t n_edges, int32_t n_out);
+int hg_segment_weighted_rows_f64(const int64_t* edge_src, const int64_t* edge_dst, const double* w,
+                                 int64_t n_edges, const double* rows, int32_t d, int32_t n_out, double* out,
+                                 int32_t* ws, void* stream);
+
+/* ---- K4-K7 gather + aggregation (orchestrator.py:239; gnnmath.py:89-200) --
+ *  model 0 = SAGE mean of non-self neighbours, 1 = GCN block sym-norm.
+ *  global_src 1: rows addressed by global id (bottom layer: reads the feature
+ *  table and also writes the gathered self rows to self_out); 0: by local id. */
+int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* hin, int32_t ld_in, int32_t F,
+                     const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                     const int32_t* counts, const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself,
+                     const int32_t* outdeg, const uint8_t* inj_mask, float* self_out, int32_t ld_self,
+                     float* agg_out, int32_t ld_agg, void* stream);
+int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself, int32_t ld_dself,
+                     int32_t F, const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                     const int32_t* counts, const int32_t* slot_g, const int32_t* nself, const int32_t* outdeg,
+                     const int32_t* csc_slot, const int32_t* seg_beg, const int32_t* seg_end,
+                     const int32_t* d_n_src, int32_t cap_src, const float* hmask, int32_t ld_hmask,
+                     const uint8_t* inj_mask, float* dx, int32_t ld_dx, void* stream);
+
+/* ---- K8 dense transforms (gnnmath.py:121,135,139,173,190-198) ---------- */
+int hg_gemm_f32(const float* A1, int32_t lda1, int32_t K1, const float* B1, int32_t ldb1, const float* A2,
+                int32_t lda2, int32_t K2, const float* B2, int32_t ldb2, int32_t trans_b, float* C, int32_t ldc,
+                int32_t N, const int32_t* d_M, int32_t M_cap, int32_t act, void* stream);
+int64_t hg_wgrad_ws_size(int32_t K, int32_t N, int32_t M_cap);
+int hg_wgrad_f32(const float* A, int32_t lda, int32_t K, const float* G, int32_t ldg, int32_t N,
+                 const int32_t* d_M, int32_t M_cap, float* out, float scale, float* ws, void* stream);
+
+/* ---- K9/K10 loss and updates (gnnmath.py:263-312; orchestrator.py:246-255) */
+/* dlogits = (softmax - onehot) / *d_div (d_div NULL: / n); *d_loss = mean CE over
+ * the n = min(*d_n, cap) rows; labels indexed by seeds[r] (seeds NULL: by r). */
+int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const int32_t* d_n, int32_t cap,
+                    const int32_t* labels, const int32_t* seeds, const int32_t* d_div, float* dlogits,
+                    int32_t ldd, float* d_loss, void* stream);
+/* per-batch row record: loss_arr[bp[3]] = *d_loss, md_arr[bp[3]] = max|dw|; resets *d_maxdelta */
+int hg_record_batch(const int64_t* bp, const float* d_loss, uint32_t* d_maxdelta, float* loss_arr,
+                    float* md_arr, void* stream);
+int hg_sgd(float* w, const float* g, int64_t n, float lr, uint32_t* d_maxdelta, void* stream);
+int hg_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+            int32_t* d_t, uint32_t* d_maxdelta, void* stream);
+
+/* ---- K11 historical-embedding store (store.py:24-146; orchestrator.py:259-271,
+ *      381-395 producer, 480-504 consumer, gnnmath.py:240-245 injection).
+ *  bp: per-batch int64 parameter block (see hg_train.cu BP_* indices). */
+int hg_store_put(const int32_t* ids, const int32_t* d_n, int32_t cap, const float* emb, int32_t ld_emb, int32_t H,
+                 const int32_t* slot_of, float* tab, int32_t* ver, int32_t* stamp, int32_t version,
+                 int32_t stamp_val, int32_t* d_puts, void* stream);
+int hg_store_lookup(const int32_t* dst, const int32_t* d_n, int32_t cap, const int64_t* bp,
+                    const int32_t* cpu_tag_of, const int32_t* slot_of, const int32_t* ver0, const int32_t* ver1,
+                    const int32_t* stamp0, const int32_t* stamp1, int32_t gap_bound, uint8_t* inj_mask,
+                    int32_t* inj_slot, int32_t* batch_hits, int32_t* batch_miss, int32_t* batch_warm,
+                    uint64_t* stats, void* stream);
+int hg_inject_rows(const uint8_t* inj_mask, const int32_t* inj_slot, const int32_t* d_n, int32_t cap,
+                   const int64_t* bp, const float* tab0, const float* tab1, int32_t H, float* h, int32_t ldh,
+                   void* stream);
+
+/* ---- epoch planning helpers (orchestrator.py:200-229 queue replay) ------ */
+int hg_tag_vertices(const int32_t* ids, const int32_t* d_n, int32_t cap, int32_t* tag_of, int32_t tag,
+                    void* stream);
+int64_t hg_filter_ws_size(int32_t n);
+int hg_filter_tagged(const int32_t* list, int32_t n, const int32_t* tag_of, int32_t tag, int32_t* out,
+                     int32_t* d_n_out, int32_t* ws, void* stream);
+
+/* ---- evaluation (orchestrator.py:662-680) -------------------------------- */
+int hg_full_aggregate(int32_t model, const float* hin, int32_t ld_in, int32_t F, const int64_t* offsets,
+                      const int32_t* targets, int32_t V, const int32_t* outdeg, float* out, int32_t ld_out,
+                      void* stream);
+int hg_target_histogram(const int32_t* targets, int64_t E, int32_t* cnt, void* stream);
+int hg_argmax_correct(const float* logits, int32_t ld, int32_t C, int32_t V, const int32_t* labels,
+                      const uint8_t* mask, uint64_t* d_correct, void* stream);
+
+/* ---- primitives ---------------------------------------------------------- */
+int64_t hg_scan_ws_size(int64_t cap);
+int hg_scan_exclusive(const int32_t* in, int32_t* out, const int32_t* d_n, int64_t cap, int32_t* d_total,
+                      int32_t* ws, void* stream);
+int64_t hg_radix_ws_size(int64_t n);
+int hg_radix_sort_pairs(uint32_t* keys, int32_t* vals, uint32_t* k_alt, int32_t* v_alt, int64_t n,
+                        int32_t key_bits, int32_t* ws, int32_t* host_out_in_alt, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HG_GNN_H */

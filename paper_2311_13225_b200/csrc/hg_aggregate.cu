@@ -1,0 +1,385 @@
+// K4-K7: gather + mean/GCN aggregation forward, transposed aggregation backward.
+//
+// Forward replaces, for one sampled block,
+//   feature gather  data.features[stack.bottom_src()]        (orchestrator.py:239)
+//   SAGE            _sage_neighbor_edges + segment_weighted_rows (gnnmath.py:145-154,171)
+//   GCN             gcn_norm_weights   + segment_weighted_rows (gnnmath.py:89-97,120)
+// in ONE pass: the bottom layer reads feature rows straight from the
+// HBM-resident table by global id (no materialised [n_src x F] gather buffer)
+// and writes [self rows | aggregate] for the dense transform; rows of
+// destinations whose output will be replaced by a historical embedding
+// (gnnmath.py:240-245) are skipped (zero-filled) — the reduced gather of
+// transfer.needed_bottom_rows (transfer.py:59-73).
+//
+// Each destination is served by a group of LPR lanes; lane l of the group owns
+// float4 columns l, l+LPR, ...  Edges are consumed in slot order (ascending
+// local src = the reference's (dst, src) order) with four rows in flight per
+// step, so accumulation order per column is fixed: deterministic, no atomics.
+//
+// Backward (layers >= 1 only, need_dx = l > 0, gnnmath.py:256) replaces the
+// transposed scatter segment_weighted_rows(ed, es, ...) (gnnmath.py:140,199):
+// each src row gathers its edges from the stable src-major (CSC) view, in
+// ascending dst order like the reference's edge loop, adds the SAGE self-term
+// gradient, and applies the lower layer's ReLU' and injected-row masks
+// (gnnmath.py:130-134,183-188) before writing dZ of the layer below.
+#include "hg_common.cuh"
+#include "hg_gnn_internal.h"
+
+namespace {
+
+enum { M_SAGE_LOCAL = 0, M_SAGE_GLOBAL = 1, M_GCN_LOCAL = 2, M_GCN_GLOBAL = 3 };
+
+__device__ __forceinline__ float4 f4_fma(float w, float4 r, float4 a) {
+    a.x = fmaf(w, r.x, a.x);
+    a.y = fmaf(w, r.y, a.y);
+    a.z = fmaf(w, r.z, a.z);
+    a.w = fmaf(w, r.w, a.w);
+    return a;
+}
+
+__device__ __forceinline__ float gcn_w(int outdeg_s, int indeg_d) {
+    return (float)(1.0 / sqrt((double)outdeg_s * (double)indeg_d));
+}
+
+template <int LPR, int NV, int MODE>
+__global__ void __launch_bounds__(256) k_agg_fwd(
+    const float* __restrict__ hin, int ld_in, int F4, const int* __restrict__ frontier, const int* d_n, int cap,
+    int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
+    const int* __restrict__ nself, const int* __restrict__ outdeg, const uint8_t* __restrict__ inj,
+    float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out, int ld_agg) {
+    constexpr bool GLOBAL = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL);
+    constexpr bool GCN = (MODE == M_GCN_LOCAL || MODE == M_GCN_GLOBAL);
+    const int n = hg_load_count(d_n, cap);
+    const int lane = threadIdx.x & 31;
+    const int lr = lane & (LPR - 1);
+    const int g0 = lane & ~(LPR - 1);
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << g0);
+    const int groups_per_block = blockDim.x / LPR;
+    for (int i0 = blockIdx.x * groups_per_block; i0 < n; i0 += gridDim.x * groups_per_block) {
+        const int i = i0 + threadIdx.x / LPR;
+        if (i >= n) continue;
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool skip = inj && inj[i];
+        const int v = frontier[i];
+        if (!skip) {
+            if (GLOBAL && self_out) {  // self row gather (the SAGE/GCN-free "gather" part)
+                const float4* src = reinterpret_cast<const float4*>(hin + (int64_t)v * ld_in);
+                float4* dst = reinterpret_cast<float4*>(self_out + (int64_t)i * ld_self);
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int c = lr + k * LPR;
+                    if (c < F4) dst[c] = __ldg(src + c);
+                }
+            }
+            const int cnt = counts[i];
+            const int64_t sbase = (int64_t)i * f;
+            float wd = 0.f;
+            if (!GCN) { const int ns = nself[i]; wd = ns > 0 ? 1.0f / (float)ns : 0.f; }
+            for (int j0 = 0; j0 < cnt; j0 += LPR) {
+                // lanes fetch up to LPR edge descriptors, then broadcast
+                int my_row = -1;
+                float my_w = 0.f;
+                if (j0 + lr < cnt) {
+                    const int sg = slot_g[sbase + j0 + lr];
+                    const int sl = slot_local[sbase + j0 + lr];
+                    if (GCN) { my_row = GLOBAL ? sg : sl; my_w = gcn_w(outdeg[sl], cnt); }
+                    else if (sg != v) { my_row = GLOBAL ? sg : sl; my_w = wd; }  // non-self edge
+                }
+                const int m = min(LPR, cnt - j0);
+                int j = 0;
+                for (; j + 4 <= m; j += 4) {
+                    int r[4]; float w[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        r[t] = __shfl_sync(gmask, my_row, j + t, LPR);
+                        w[t] = __shfl_sync(gmask, my_w, j + t, LPR);
+                    }
+                    float4 x[4][NV];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const float4* rp = reinterpret_cast<const float4*>(hin + (int64_t)(r[t] < 0 ? 0 : r[t]) * ld_in);
+#pragma unroll
+                        for (int k = 0; k < NV; ++k) {
+                            const int c = lr + k * LPR;
+                            x[t][k] = (r[t] >= 0 && c < F4) ? __ldg(rp + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (r[t] >= 0) {
+#pragma unroll
+                            for (int k = 0; k < NV; ++k) acc[k] = f4_fma(w[t], x[t][k], acc[k]);
+                        }
+                }
+                for (; j < m; ++j) {
+                    const int r = __shfl_sync(gmask, my_row, j, LPR);
+                    const float w = __shfl_sync(gmask, my_w, j, LPR);
+                    if (r >= 0) {
+                        const float4* rp = reinterpret_cast<const float4*>(hin + (int64_t)r * ld_in);
+#pragma unroll
+                        for (int k = 0; k < NV; ++k) {
+                            const int c = lr + k * LPR;
+                            if (c < F4) acc[k] = f4_fma(w, __ldg(rp + c), acc[k]);
+                        }
+                    }
+                }
+            }
+        } else if (GLOBAL && self_out) {
+            float4* dst = reinterpret_cast<float4*>(self_out + (int64_t)i * ld_self);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int c = lr + k * LPR;
+                if (c < F4) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        float4* out = reinterpret_cast<float4*>(agg_out + (int64_t)i * ld_agg);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lr + k * LPR;
+            if (c < F4) out[c] = acc[k];
+        }
+    }
+}
+
+template <int LPR, int NV, bool GCN>
+__global__ void __launch_bounds__(256) k_agg_bwd(
+    const float* __restrict__ dagg, int ld_dagg, const float* __restrict__ dself, int ld_dself, int F4,
+    const int* __restrict__ frontier, const int* d_n_dst, int cap_dst, int f, const int* __restrict__ counts,
+    const int* __restrict__ slot_g, const int* __restrict__ nself, const int* __restrict__ outdeg,
+    const int* __restrict__ csc_slot, const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
+    const int* d_n_src, int cap_src, const float* __restrict__ hmask, int ld_hmask,
+    const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx) {
+    const int n_src = hg_load_count(d_n_src, cap_src);
+    const int n_dst = hg_load_count(d_n_dst, cap_dst);
+    const int lane = threadIdx.x & 31;
+    const int lr = lane & (LPR - 1);
+    const int g0 = lane & ~(LPR - 1);
+    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << g0);
+    const int groups_per_block = blockDim.x / LPR;
+    for (int s0 = blockIdx.x * groups_per_block; s0 < n_src; s0 += gridDim.x * groups_per_block) {
+        const int s = s0 + threadIdx.x / LPR;
+        if (s >= n_src) continue;
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int beg = seg_beg[s], end = seg_end[s];
+        for (int j0 = beg; j0 < end; j0 += LPR) {
+            int my_row = -1;
+            float my_w = 0.f;
+            if (j0 + lr < end) {
+                const int e = csc_slot[j0 + lr];
+                const int d = e / f;
+                if (GCN) { my_row = d; my_w = gcn_w(outdeg[s], counts[d]); }
+                else if (slot_g[e] != frontier[d]) { my_row = d; my_w = 1.0f / (float)nself[d]; }
+            }
+            const int m = min(LPR, end - j0);
+            for (int j = 0; j < m; ++j) {
+                const int r = __shfl_sync(gmask, my_row, j, LPR);
+                const float w = __shfl_sync(gmask, my_w, j, LPR);
+                if (r >= 0) {
+                    const float4* rp = reinterpret_cast<const float4*>(dagg + (int64_t)r * ld_dagg);
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) {
+                        const int c = lr + k * LPR;
+                        if (c < F4) acc[k] = f4_fma(w, __ldg(rp + c), acc[k]);
+                    }
+                }
+            }
+        }
+        const bool zero_row = inj && inj[s];
+        float4* out = reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lr + k * LPR;
+            if (c >= F4) continue;
+            float4 a = acc[k];
+            if (dself && s < n_dst) {  // dx[:n_dst] = dz W_self^T, then += scatter (gnnmath.py:195-199)
+                const float4 ds = __ldg(reinterpret_cast<const float4*>(dself + (int64_t)s * ld_dself) + c);
+                a.x = ds.x + a.x; a.y = ds.y + a.y; a.z = ds.z + a.z; a.w = ds.w + a.w;
+            }
+            if (hmask) {  // ReLU' of the layer below: z > 0  <=>  relu(z) > 0
+                const float4 h = __ldg(reinterpret_cast<const float4*>(hmask + (int64_t)s * ld_hmask) + c);
+                a.x = h.x > 0.f ? a.x : 0.f; a.y = h.y > 0.f ? a.y : 0.f;
+                a.z = h.z > 0.f ? a.z : 0.f; a.w = h.w > 0.f ? a.w : 0.f;
+            }
+            if (zero_row) a = make_float4(0.f, 0.f, 0.f, 0.f);
+            out[c] = a;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fp64, bit-exact segment_weighted_rows for arbitrary edge lists (plug-in API,
+// kernels.py:121-144): out[d] += w*rows[s] in edge order, no FMA contraction.
+// Edges are grouped by destination with a stable radix sort first.
+// ---------------------------------------------------------------------------
+__global__ void k_swr_keys(const int64_t* __restrict__ edge_dst, long long n, uint32_t* __restrict__ keys,
+                           int* __restrict__ vals) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        keys[e] = (uint32_t)edge_dst[e];
+        vals[e] = (int)e;
+    }
+}
+
+__global__ void k_swr_bounds(const uint32_t* __restrict__ keys, long long n, int* __restrict__ beg,
+                             int* __restrict__ end) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const uint32_t key = keys[k];
+        if (k == 0 || keys[k - 1] != key) beg[key] = (int)k;
+        if (k == n - 1 || keys[k + 1] != key) end[key] = (int)(k + 1);
+    }
+}
+
+__global__ void k_swr_rows(const int64_t* __restrict__ edge_src, const double* __restrict__ w,
+                           const double* __restrict__ rows, int d, const int* __restrict__ order,
+                           const int* __restrict__ beg, const int* __restrict__ end, int n_out,
+                           double* __restrict__ out) {
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < n_out; o += warps) {
+        const int b = beg[o], e = end[o];
+        for (int c = lane; c < d; c += 32) {
+            double acc = 0.0;
+            for (int k = b; k < e; ++k) {
+                const int ed = order[k];
+                acc = __dadd_rn(acc, __dmul_rn(w[ed], rows[edge_src[ed] * (int64_t)d + c]));
+            }
+            out[(int64_t)o * d + c] = acc;
+        }
+    }
+}
+
+template <int MODE>
+int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld_in, int F4, const int* frontier,
+               const int* d_n, int cap, int f, const int* counts, const int* slot_g, const int* slot_local,
+               const int* nself, const int* outdeg, const uint8_t* inj, float* self_out, int ld_self,
+               float* agg_out, int ld_agg) {
+#define HG_FWD(L, V)                                                                                       \
+    if (LPR == L && NV == V) {                                                                             \
+        k_agg_fwd<L, V, MODE><<<g, 256, 0, s>>>(hin, ld_in, F4, frontier, d_n, cap, f, counts, slot_g,     \
+                                                slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, \
+                                                ld_agg);                                                   \
+        return HG_OK;                                                                                      \
+    }
+    HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 8)
+#undef HG_FWD
+    return HG_EUNSUPPORTED;
+}
+
+template <bool GCN>
+int launch_bwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* dagg, int ld_dagg, const float* dself,
+               int ld_dself, int F4, const int* frontier, const int* d_n_dst, int cap_dst, int f, const int* counts,
+               const int* slot_g, const int* nself, const int* outdeg, const int* csc_slot, const int* seg_beg,
+               const int* seg_end, const int* d_n_src, int cap_src, const float* hmask, int ld_hmask,
+               const uint8_t* inj, float* dx, int ld_dx) {
+#define HG_BWD(L, V)                                                                                            \
+    if (LPR == L && NV == V) {                                                                                  \
+        k_agg_bwd<L, V, GCN><<<g, 256, 0, s>>>(dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, \
+                                               f, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end,    \
+                                               d_n_src, cap_src, hmask, ld_hmask, inj, dx, ld_dx);              \
+        return HG_OK;                                                                                           \
+    }
+    HG_BWD(8, 1) HG_BWD(16, 1) HG_BWD(32, 1) HG_BWD(32, 2) HG_BWD(32, 4) HG_BWD(32, 8)
+#undef HG_BWD
+    return HG_EUNSUPPORTED;
+}
+
+void pick_lanes(int F4, int& LPR, int& NV) {
+    if (F4 <= 8) { LPR = 8; NV = 1; }
+    else if (F4 <= 16) { LPR = 16; NV = 1; }
+    else if (F4 <= 32) { LPR = 32; NV = 1; }
+    else if (F4 <= 64) { LPR = 32; NV = 2; }
+    else if (F4 <= 128) { LPR = 32; NV = 4; }
+    else { LPR = 32; NV = 8; }
+}
+
+}  // namespace
+
+// model: 0 = SAGE (mean over non-self sampled neighbours), 1 = GCN (block sym-norm).
+// global_src: 1 = rows addressed by global id (bottom layer, reads the feature
+// table), 0 = by local src id (upper layers, reads the previous activation).
+// F: columns (multiple of 4; pad the row stride ld_* to a multiple of 4).
+extern "C" int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* hin, int32_t ld_in, int32_t F,
+                                const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                                const int32_t* counts, const int32_t* slot_g, const int32_t* slot_local,
+                                const int32_t* nself, const int32_t* outdeg, const uint8_t* inj_mask,
+                                float* self_out, int32_t ld_self, float* agg_out, int32_t ld_agg, void* stream) {
+    if (F % 4 || ld_in % 4 || ld_agg % 4 || (self_out && ld_self % 4)) {
+        hg_set_error("aggregate_fwd: F and row strides must be multiples of 4");
+        return HG_EINVAL;
+    }
+    if (F > 1024) { hg_set_error("aggregate_fwd: F > 1024 unsupported"); return HG_EUNSUPPORTED; }
+    if (cap_dst == 0) return HG_OK;
+    const int F4 = F / 4;
+    int LPR, NV;
+    pick_lanes(F4, LPR, NV);
+    dim3 g(hg_grid((long long)cap_dst * LPR, 256, 8));
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc;
+    const int mode = (model ? 2 : 0) + (global_src ? 1 : 0);
+    switch (mode) {
+        case M_SAGE_LOCAL: rc = launch_fwd<M_SAGE_LOCAL>(LPR, NV, g, s, hin, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+        case M_SAGE_GLOBAL: rc = launch_fwd<M_SAGE_GLOBAL>(LPR, NV, g, s, hin, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+        case M_GCN_LOCAL: rc = launch_fwd<M_GCN_LOCAL>(LPR, NV, g, s, hin, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+        default: rc = launch_fwd<M_GCN_GLOBAL>(LPR, NV, g, s, hin, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+    }
+    if (rc) { hg_set_error("aggregate_fwd: unsupported width"); return rc; }
+    return hg_check_launch("aggregate_fwd");
+}
+
+extern "C" int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself,
+                                int32_t ld_dself, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
+                                int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                                const int32_t* nself, const int32_t* outdeg, const int32_t* csc_slot,
+                                const int32_t* seg_beg, const int32_t* seg_end, const int32_t* d_n_src,
+                                int32_t cap_src, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
+                                float* dx, int32_t ld_dx, void* stream) {
+    if (F % 4 || ld_dagg % 4 || ld_dx % 4) { hg_set_error("aggregate_bwd: widths must be multiples of 4"); return HG_EINVAL; }
+    if (F > 1024) { hg_set_error("aggregate_bwd: F > 1024 unsupported"); return HG_EUNSUPPORTED; }
+    if (cap_src == 0) return HG_OK;
+    const int F4 = F / 4;
+    int LPR, NV;
+    pick_lanes(F4, LPR, NV);
+    dim3 g(hg_grid((long long)cap_src * LPR, 256, 8));
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = model ? launch_bwd<true>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx)
+                   : launch_bwd<false>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx);
+    if (rc) { hg_set_error("aggregate_bwd: unsupported width"); return rc; }
+    return hg_check_launch("aggregate_bwd");
+}
+
+extern "C" int64_t hg_swr_ws_size(int64_t n_edges, int32_t n_out) {
+    return (int64_t)(4 * n_edges + 2 * (long long)n_out + (long long)hg_radix_ws_ints(n_edges) + 16);
+}
+
+// fp64 segment_weighted_rows (kernels.py:121-144), bit-identical to the
+// reference's numba loop / np.add.at for any edge order.
+extern "C" int hg_segment_weighted_rows_f64(const int64_t* edge_src, const int64_t* edge_dst, const double* w,
+                                            int64_t n_edges, const double* rows, int32_t d, int32_t n_out,
+                                            double* out, int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(out, 0, sizeof(double) * (size_t)n_out * d, s);
+    if (n_edges == 0 || n_out == 0 || d == 0) return hg_check_launch("swr(empty)");
+    const long long n = n_edges;
+    uint32_t* keys = (uint32_t*)ws;
+    int* vals = ws + n;
+    uint32_t* k_alt = (uint32_t*)(ws + 2 * n);
+    int* beg = ws + 3 * n;
+    int* end = beg + n_out;
+    int* rws = end + n_out;
+    int* v_alt = rws + hg_radix_ws_ints(n);
+    cudaMemsetAsync(beg, 0, sizeof(int) * 2 * (size_t)n_out, s);
+    int bits = 1;
+    while ((1u << bits) < (uint32_t)n_out && bits < 32) ++bits;
+    k_swr_keys<<<hg_grid(n, 256, 8), 256, 0, s>>>(edge_dst, n, keys, vals);
+    int in_alt = 0;
+    int rc = hg_radix_sort_launch(keys, vals, k_alt, v_alt, n, bits, rws, &in_alt, s);
+    if (rc) return rc;
+    const uint32_t* sk = in_alt ? k_alt : keys;
+    const int* sv = in_alt ? v_alt : vals;
+    k_swr_bounds<<<hg_grid(n, 256, 8), 256, 0, s>>>(sk, n, beg, end);
+    k_swr_rows<<<hg_grid((long long)n_out * 32, 256, 8), 256, 0, s>>>(edge_src, w, rows, d, sv, beg, end, n_out, out);
+    return hg_check_launch("segment_weighted_rows_f64");
+}

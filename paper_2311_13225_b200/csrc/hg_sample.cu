@@ -1,0 +1,568 @@
+// K1-K3: bit-exact k-hop block sampling on an HBM-resident CSR.
+//
+// Replaces the reference's per-layer block construction
+//   sampler._expand_frontier (sampler.py:104-118)
+//     = kernels._sample_layer (kernels.py:77-118)      -> k_sample_seg / k_sample_seq
+//     + kernels.stable_unique (kernels.py:166-180)     -> k_mark + scan + k_emit_src
+//     + np.lexsort((src_local, dst_local))             -> k_relabel_sort_seg
+//
+// Layout ("slot" form, what the training step consumes): destination i owns
+// the fixed-stride slot range [i*f, i*f + counts[i]); slots hold the sampled
+// global ids and, after relabel, the local src ids sorted ascending — exactly
+// the reference's (dst, src) edge order.  No prefix sum is needed to address a
+// segment, so the aggregation kernels index segments directly.  A compacted
+// CSR (the reference's Block.edge_src/edge_dst) is produced only on request
+// (hg_block_to_edges).
+//
+// RNG: the reference's splitmix64 per-(stream, vertex) partial Fisher–Yates.
+// Draw j of vertex v uses r_j = mix64(s_v + (j+1)*GOLDEN), which is counter
+// based, so the lanes of a segment compute all r_j and picks in parallel; the
+// swap chain of the partial Fisher–Yates is then resolved with a shared-memory
+// "last writer" table, pointer jumping and __match_any_sync (see k_sample_seg).
+//
+// Dedup: positions follow the reference's emission order (frontier first,
+// then draws in (dst, draw) order).  A dense int32 minpos[V] table (all
+// INT_MAX at rest) receives atomicMin(position) for every emitted id; an id's
+// first occurrence is the position that won.  The table is restored by
+// k_reset_minpos, touching only the ids of this block.
+#include "hg_common.cuh"
+#include "hg_gnn_internal.h"
+
+namespace {
+
+// --------------------------------------------------------------------------
+// draw kernel, fanout <= 32: one W-lane segment per destination
+// --------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ offsets,
+                                                    const int* __restrict__ targets,
+                                                    const int* __restrict__ frontier, const int* d_n,
+                                                    int cap, int f, const uint64_t* __restrict__ d_seed,
+                                                    int layer, int* __restrict__ counts,
+                                                    int* __restrict__ slots, int* __restrict__ minpos) {
+    __shared__ int s_last[256];
+    const int n = hg_load_count(d_n, cap);
+    const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
+    const uint64_t base = hg_mix64(stream + HG_GOLDEN);  // kernels.py:153
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & (W - 1);
+    const int seg0 = lane & ~(W - 1);  // first lane of my segment
+    const unsigned segmask = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << seg0);
+    const int segs_per_block = blockDim.x / W;
+    int* last = s_last + (threadIdx.x & ~(W - 1));
+    for (int i0 = blockIdx.x * segs_per_block; i0 < n; i0 += gridDim.x * segs_per_block) {
+        const int i = i0 + threadIdx.x / W;
+        if (i >= n) continue;  // segment-uniform
+        const int v = frontier[i];
+        if (sub == 0) atomicMin(&minpos[v], i);  // frontier position i
+        const int64_t off = offsets[v];
+        const int64_t deg = offsets[v + 1] - off;
+        const int cnt = deg < f ? (int)deg : f;
+        if (sub == 0) counts[i] = cnt;
+        int u = -1;
+        if (deg <= f) {  // kernels.py:100-103: every neighbour, CSR order
+            if (sub < deg) u = targets[off + sub];
+        } else {  // kernels.py:104-117
+            int pick = -1 - sub;  // distinct sentinels for idle lanes
+            if (sub < f) {
+                const uint64_t st = hg_mix64(base ^ ((uint64_t)(int64_t)v * HG_PHI)) +
+                                    (uint64_t)(sub + 1) * HG_GOLDEN;
+                const uint64_t r = hg_mix64(st);
+                pick = sub + (int)(r % (uint64_t)(deg - sub));
+            }
+            // last[p] = latest earlier draw m (< p) whose pick was position p
+            last[sub] = -1;
+            __syncwarp(segmask);
+            if (sub < f && pick < f && pick != sub) atomicMax(&last[pick], sub);
+            __syncwarp(segmask);
+            // before(p) = value held at position p right before draw p:
+            // follow last[] down to a position never overwritten (pointer jumping)
+            int root = (sub < f && last[sub] >= 0) ? last[sub] : sub;
+#pragma unroll
+            for (int k = 1; k < W; k <<= 1) root = __shfl_sync(segmask, root, root, W);
+            // draw j emits the current content of position pick_j: the value the
+            // latest earlier draw k with the same pick moved there (before(k)),
+            // or pick_j itself if untouched
+            const unsigned peers = __match_any_sync(segmask, pick) & hg_lanemask_lt();
+            const int k = peers ? (31 - __clz(peers)) - seg0 : sub;
+            const int moved = __shfl_sync(segmask, root, k, W);
+            if (sub < f) u = targets[off + (peers ? moved : pick)];
+        }
+        if (sub < cnt) {
+            slots[(int64_t)i * f + sub] = u;
+            atomicMin(&minpos[u], n + i * f + sub);
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// draw kernel, fanout > 32: one thread per destination, sequential partial
+// Fisher–Yates with a small swap map in scratch (pos, val pairs; O(f^2))
+// --------------------------------------------------------------------------
+__global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __restrict__ targets,
+                             const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                             const uint64_t* __restrict__ d_seed, int layer, int* __restrict__ counts,
+                             int* __restrict__ slots, int* __restrict__ minpos, int* __restrict__ scratch) {
+    const int n = hg_load_count(d_n, cap);
+    const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
+    const uint64_t base = hg_mix64(stream + HG_GOLDEN);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int v = frontier[i];
+        atomicMin(&minpos[v], i);
+        const int64_t off = offsets[v];
+        const int64_t deg = offsets[v + 1] - off;
+        const int cnt = deg < f ? (int)deg : f;
+        counts[i] = cnt;
+        int* sp = slots + (int64_t)i * f;
+        if (deg <= f) {
+            for (int j = 0; j < cnt; ++j) sp[j] = targets[off + j];
+        } else {
+            int* mp = scratch + (int64_t)i * 2 * f;  // map entries: position, value
+            int m = 0;
+            uint64_t st = hg_mix64(base ^ ((uint64_t)(int64_t)v * HG_PHI));
+            for (int j = 0; j < f; ++j) {
+                st += HG_GOLDEN;
+                const uint64_t r = hg_mix64(st);
+                const int pick = j + (int)(r % (uint64_t)(deg - j));
+                int vj = j, vp = pick, ip = -1;
+                for (int t = 0; t < m; ++t) {
+                    if (mp[2 * t] == j) vj = mp[2 * t + 1];
+                    if (mp[2 * t] == pick) { vp = mp[2 * t + 1]; ip = t; }
+                }
+                // swap(idx[j], idx[pick]); emit idx[j].  Position j is never read
+                // again (later picks are > j), so only position pick is recorded.
+                if (pick != j) {
+                    if (ip >= 0) mp[2 * ip + 1] = vj;
+                    else { mp[2 * m] = pick; mp[2 * m + 1] = vj; ++m; }
+                }
+                sp[j] = targets[off + vp];
+            }
+        }
+        for (int j = 0; j < cnt; ++j) atomicMin(&minpos[sp[j]], n + i * f + j);
+    }
+}
+
+__device__ __forceinline__ bool pos_item(long long p, int n, int f, const int* frontier, const int* counts,
+                                         const int* slots, int& u) {
+    if (p < n) { u = frontier[p]; return true; }
+    const long long q = p - n;
+    const int i = (int)(q / f);
+    const int j = (int)(q - (long long)i * f);
+    if (j >= counts[i]) return false;
+    u = slots[q];
+    return true;
+}
+
+// flag[p] = (position p holds the first occurrence of its id)
+__global__ void k_mark(const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                       const int* __restrict__ counts, const int* __restrict__ slots,
+                       const int* __restrict__ minpos, int* __restrict__ flags) {
+    const int n = hg_load_count(d_n, cap);
+    const long long P = (long long)n * (f + 1);
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+         p += (long long)gridDim.x * blockDim.x) {
+        int u;
+        flags[p] = (pos_item(p, n, f, frontier, counts, slots, u) && minpos[u] == (int)p) ? 1 : 0;
+    }
+}
+
+// src_vertices[rank[p]] = id, for first occurrences (rank = exclusive scan of flags)
+__global__ void k_emit_src(const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                           const int* __restrict__ counts, const int* __restrict__ slots,
+                           const int* __restrict__ minpos, const int* __restrict__ rank,
+                           int* __restrict__ src_vertices) {
+    const int n = hg_load_count(d_n, cap);
+    const long long P = (long long)n * (f + 1);
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
+         p += (long long)gridDim.x * blockDim.x) {
+        int u;
+        if (pos_item(p, n, f, frontier, counts, slots, u) && minpos[u] == (int)p) src_vertices[rank[p]] = u;
+    }
+}
+
+// per destination: local id = rank[minpos[id]]; sort the segment by local id
+// (stable on draw order, = np.lexsort((src_local, dst_local))); write sorted
+// global ids back into slots and local ids into slot_local; per-dst non-self
+// count (SAGE, gnnmath.py:145-154) and block out-degree (GCN, gnnmath.py:96).
+template <int W>
+__global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict__ frontier, const int* d_n,
+                                                          int cap, int f, const int* __restrict__ counts,
+                                                          int* __restrict__ slots, int* __restrict__ slot_local,
+                                                          const int* __restrict__ minpos,
+                                                          const int* __restrict__ rank,
+                                                          int* __restrict__ nself, int* __restrict__ outdeg) {
+    const int n = hg_load_count(d_n, cap);
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & (W - 1);
+    const int seg0 = lane & ~(W - 1);
+    const unsigned segmask = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << seg0);
+    const int segs_per_block = blockDim.x / W;
+    for (int i0 = blockIdx.x * segs_per_block; i0 < n; i0 += gridDim.x * segs_per_block) {
+        const int i = i0 + threadIdx.x / W;
+        if (i >= n) continue;
+        const int cnt = counts[i];
+        const int v = frontier[i];
+        int u = -1, loc = HG_INT_MAX;
+        if (sub < cnt) {
+            u = slots[(int64_t)i * f + sub];
+            loc = rank[minpos[u]];
+        }
+        int r = 0;
+        for (int k = 0; k < cnt; ++k) {
+            const int lk = __shfl_sync(segmask, loc, k, W);
+            r += (lk < loc) || (lk == loc && k < sub);
+        }
+        const unsigned nonself = __ballot_sync(segmask, sub < cnt && u != v);
+        __syncwarp(segmask);
+        if (sub < cnt) {
+            slots[(int64_t)i * f + r] = u;
+            slot_local[(int64_t)i * f + r] = loc;
+            if (outdeg) atomicAdd(&outdeg[loc], 1);
+        }
+        if (sub == 0 && nself) nself[i] = __popc(nonself);
+    }
+}
+
+__global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                                   const int* __restrict__ counts, int* __restrict__ slots,
+                                   int* __restrict__ slot_local, const int* __restrict__ minpos,
+                                   const int* __restrict__ rank, int* __restrict__ nself,
+                                   int* __restrict__ outdeg) {
+    const int n = hg_load_count(d_n, cap);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int cnt = counts[i];
+        const int v = frontier[i];
+        int* sp = slots + (int64_t)i * f;
+        int* lp = slot_local + (int64_t)i * f;
+        int ns = 0;
+        for (int j = 0; j < cnt; ++j) {
+            lp[j] = rank[minpos[sp[j]]];
+            ns += sp[j] != v;
+        }
+        for (int j = 1; j < cnt; ++j) {  // stable insertion sort by local id
+            int l = lp[j], u = sp[j], k = j - 1;
+            while (k >= 0 && lp[k] > l) { lp[k + 1] = lp[k]; sp[k + 1] = sp[k]; --k; }
+            lp[k + 1] = l;
+            sp[k + 1] = u;
+        }
+        if (outdeg) for (int j = 0; j < cnt; ++j) atomicAdd(&outdeg[lp[j]], 1);
+        if (nself) nself[i] = ns;
+    }
+}
+
+__global__ void k_reset_minpos(const int* __restrict__ src_vertices, const int* d_n_src, int cap,
+                               int* __restrict__ minpos) {
+    const int n = hg_load_count(d_n_src, cap);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        minpos[src_vertices[k]] = HG_INT_MAX;
+}
+
+// compacted edges (Block.edge_src / edge_dst) from the slot form; starts =
+// exclusive scan of counts
+__global__ void k_block_edges(const int* d_n, int cap, int f, const int* __restrict__ counts,
+                              const int* __restrict__ starts, const int* __restrict__ slot_local,
+                              int* __restrict__ edge_src, int* __restrict__ edge_dst) {
+    const int n = hg_load_count(d_n, cap);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)n * f;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / f), j = (int)(q - (long long)i * f);
+        if (j < counts[i]) {
+            edge_src[starts[i] + j] = slot_local[q];
+            edge_dst[starts[i] + j] = i;
+        }
+    }
+}
+
+// raw-sample emission (kernels.sample_layer): edges in (dst, draw) order
+__global__ void k_emit_raw(const int* d_n, int cap, int f, const int* __restrict__ counts,
+                           const int* __restrict__ starts, const int* __restrict__ slots,
+                           int* __restrict__ edge_dst, int* __restrict__ edge_src) {
+    const int n = hg_load_count(d_n, cap);
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < (long long)n * f;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / f), j = (int)(q - (long long)i * f);
+        if (j < counts[i]) {
+            edge_dst[starts[i] + j] = i;
+            edge_src[starts[i] + j] = slots[q];
+        }
+    }
+}
+
+// CSC keys for the transposed (backward) aggregation: key = src local id of a
+// valid slot, or `big` for empty slots (sorted to the end); value = slot index
+__global__ void k_csc_keys(const int* d_n, int cap, int f, const int* __restrict__ counts,
+                           const int* __restrict__ slot_local, uint32_t big, uint32_t* __restrict__ keys,
+                           int* __restrict__ vals) {
+    const int n = hg_load_count(d_n, cap);
+    const long long Q = (long long)cap * f;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Q;
+         q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / f), j = (int)(q - (long long)i * f);
+        const bool ok = i < n && j < counts[i];
+        keys[q] = ok ? (uint32_t)slot_local[q] : big;
+        vals[q] = (int)q;
+    }
+}
+
+// per-src segment [seg_beg[s], seg_end[s]) in the sorted key array (zeroed before)
+__global__ void k_csc_bounds(const uint32_t* __restrict__ keys, long long Q, uint32_t big,
+                             int* __restrict__ seg_beg, int* __restrict__ seg_end) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < Q;
+         k += (long long)gridDim.x * blockDim.x) {
+        const uint32_t key = keys[k];
+        if (key == big) continue;
+        if (k == 0 || keys[k - 1] != key) seg_beg[key] = (int)k;
+        if (k == Q - 1 || keys[k + 1] != key) seg_end[key] = (int)(k + 1);
+    }
+}
+
+int seg_width(int f) { return f <= 4 ? 4 : f <= 8 ? 8 : f <= 16 ? 16 : 32; }
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+
+// Draw step of one layer (kernels.py:77-118).  d_seed: the batch rng seed when
+// layer >= 0 (stream = derive_seed(seed, 0x5A, layer), sampler.py:143), else the
+// stream seed itself (kernels.sample_layer).  scratch: cap*2*fanout ints, only
+// touched when fanout > 32.
+extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                               const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                               const uint64_t* d_seed, int32_t layer, int32_t* counts, int32_t* slots,
+                               int32_t* minpos, int32_t* scratch, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fanout < 1 || cap_dst < 0) { hg_set_error("sample_layer: bad fanout/cap"); return HG_EINVAL; }
+    if ((long long)cap_dst * (fanout + 1) >= 0x7fffffffLL) { hg_set_error("sample_layer: cap too large"); return HG_EINVAL; }
+    if (cap_dst == 0) return HG_OK;
+    if (fanout <= 32) {
+        const int W = seg_width(fanout);
+        const int grid = hg_grid((long long)cap_dst * W, 256, 8);
+        switch (W) {
+            case 4: k_sample_seg<4><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
+            case 8: k_sample_seg<8><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
+            case 16: k_sample_seg<16><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
+            default: k_sample_seg<32><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
+        }
+    } else {
+        if (!scratch) { hg_set_error("sample_layer: fanout > 32 needs scratch"); return HG_EINVAL; }
+        k_sample_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout,
+                                                              d_seed, layer, counts, slots, minpos, scratch);
+    }
+    return hg_check_launch("sample_layer");
+}
+
+// Dedup + relabel + per-dst sort (kernels.py:166-180, sampler.py:106-118).
+// ws: >= hg_dedup_ws_size(cap_dst, fanout) ints.  Produces src_vertices[0..n_src),
+// *d_n_src, sorted slots / slot_local, nself (nullable), outdeg (nullable; must be
+// zeroed over cap_src by the caller), and restores minpos.
+extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
+    long long P = (long long)cap_dst * (fanout + 1);
+    return (int64_t)(P + (long long)hg_scan_ws_ints(P) + 16);
+}
+
+extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                                const int32_t* counts, int32_t* slots, int32_t* slot_local, int32_t* minpos,
+                                int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
+                                int32_t* outdeg, int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("dedup(empty)"); }
+    const long long P = (long long)cap_dst * (fanout + 1);
+    int* flags = ws;
+    int* scan_ws = ws + P;
+    const int g = hg_grid(P, 256, 8);
+    k_mark<<<g, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos, flags);
+    int rc = hg_scan_launch(flags, flags, d_n_dst, fanout + 1, P, d_n_src, scan_ws, s);
+    if (rc) return rc;
+    k_emit_src<<<g, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos, flags, src_vertices);
+    if (fanout <= 32) {
+        const int W = seg_width(fanout);
+        const int grid = hg_grid((long long)cap_dst * W, 256, 8);
+        switch (W) {
+            case 4: k_relabel_sort_seg<4><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
+            case 8: k_relabel_sort_seg<8><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
+            case 16: k_relabel_sort_seg<16><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
+            default: k_relabel_sort_seg<32><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
+        }
+    } else {
+        k_relabel_sort_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
+                                                                    slot_local, minpos, flags, nself, outdeg);
+    }
+    k_reset_minpos<<<hg_grid(cap_src, 256, 8), 256, 0, s>>>(src_vertices, d_n_src, cap_src, minpos);
+    return hg_check_launch("dedup_relabel");
+}
+
+// Compacted Block edges; starts: cap_dst ints workspace (+ scan ws after it).
+extern "C" int64_t hg_block_edges_ws_size(int32_t cap_dst) {
+    return (int64_t)(cap_dst + (long long)hg_scan_ws_ints(cap_dst) + 16);
+}
+
+extern "C" int hg_block_to_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                                 const int32_t* slot_local, int32_t* edge_src, int32_t* edge_dst,
+                                 int32_t* d_n_edges, int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cap_dst == 0) { cudaMemsetAsync(d_n_edges, 0, sizeof(int), s); return HG_OK; }
+    int rc = hg_scan_launch(counts, ws, d_n_dst, 1, cap_dst, d_n_edges, ws + cap_dst, s);
+    if (rc) return rc;
+    k_block_edges<<<hg_grid((long long)cap_dst * fanout, 256, 8), 256, 0, s>>>(d_n_dst, cap_dst, fanout, counts,
+                                                                               ws, slot_local, edge_src, edge_dst);
+    return hg_check_launch("block_to_edges");
+}
+
+extern "C" int hg_raw_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                            const int32_t* slots, int32_t* edge_dst, int32_t* edge_src, int32_t* d_n_edges,
+                            int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cap_dst == 0) { cudaMemsetAsync(d_n_edges, 0, sizeof(int), s); return HG_OK; }
+    int rc = hg_scan_launch(counts, ws, d_n_dst, 1, cap_dst, d_n_edges, ws + cap_dst, s);
+    if (rc) return rc;
+    k_emit_raw<<<hg_grid((long long)cap_dst * fanout, 256, 8), 256, 0, s>>>(d_n_dst, cap_dst, fanout, counts, ws,
+                                                                            slots, edge_dst, edge_src);
+    return hg_check_launch("raw_edges");
+}
+
+// Transposed (src-major) view of a block's slots for the backward scatter
+// (gnnmath.py:140,199), stable so each src's edges stay in ascending dst order.
+// csc_slot: cap_dst*fanout ints (sorted slot indices); seg_beg/seg_end: cap_src
+// ints each.  ws >= hg_csc_ws_size(cap_dst, fanout) ints.
+extern "C" int64_t hg_csc_ws_size(int32_t cap_dst, int32_t fanout) {
+    long long Q = (long long)cap_dst * fanout;
+    return (int64_t)(3 * Q + (long long)hg_radix_ws_ints(Q) + 16);
+}
+
+extern "C" int hg_build_csc(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                            const int32_t* slot_local, int32_t cap_src, int32_t* csc_slot, int32_t* seg_beg,
+                            int32_t* seg_end, int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long Q = (long long)cap_dst * fanout;
+    cudaMemsetAsync(seg_beg, 0, sizeof(int) * (size_t)cap_src, s);
+    cudaMemsetAsync(seg_end, 0, sizeof(int) * (size_t)cap_src, s);
+    if (Q == 0) return hg_check_launch("build_csc(empty)");
+    uint32_t* keys = (uint32_t*)ws;
+    uint32_t* k_alt = (uint32_t*)(ws + Q);
+    int* v_alt = ws + 2 * Q;
+    int* rws = ws + 3 * Q;
+    const uint32_t big = (uint32_t)cap_src;
+    int bits = 1;
+    while ((1u << bits) <= big && bits < 32) ++bits;
+    k_csc_keys<<<hg_grid(Q, 256, 8), 256, 0, s>>>(d_n_dst, cap_dst, fanout, counts, slot_local, big, keys, csc_slot);
+    int in_alt = 0;
+    int rc = hg_radix_sort_launch(keys, csc_slot, k_alt, v_alt, Q, bits, rws, &in_alt, s);
+    if (rc) return rc;
+    if (in_alt) {
+        cudaMemcpyAsync(csc_slot, v_alt, sizeof(int) * Q, cudaMemcpyDeviceToDevice, s);
+        keys = k_alt;
+    }
+    k_csc_bounds<<<hg_grid(Q, 256, 8), 256, 0, s>>>(keys, Q, big, seg_beg, seg_end);
+    return hg_check_launch("build_csc");
+}
+
+// ---------------------------------------------------------------------------
+// generic first-occurrence dedup of int64 values (kernels.stable_unique):
+// open-addressing hash (key, min position) + flags/scan/emit
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ uint32_t hash_slot(unsigned long long key, uint32_t mask) {
+    return (uint32_t)hg_mix64(key) & mask;
+}
+constexpr unsigned long long EMPTY_KEY = 0xffffffffffffffffULL;
+
+__global__ void k_uq_insert(const long long* __restrict__ vals, long long n, unsigned long long* __restrict__ hkeys,
+                            int* __restrict__ hpos, uint32_t mask) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long key = (unsigned long long)vals[p];
+        if (key == EMPTY_KEY) { atomicMin(&hpos[mask + 1], (int)p); continue; }  // sentinel-valued id
+        uint32_t h = hash_slot(key, mask);
+        while (true) {
+            unsigned long long prev = atomicCAS(&hkeys[h], EMPTY_KEY, key);
+            if (prev == EMPTY_KEY || prev == key) { atomicMin(&hpos[h], (int)p); break; }
+            h = (h + 1) & mask;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t uq_find(unsigned long long key, const unsigned long long* hkeys, uint32_t mask) {
+    if (key == EMPTY_KEY) return mask + 1;
+    uint32_t h = hash_slot(key, mask);
+    while (hkeys[h] != key) h = (h + 1) & mask;
+    return h;
+}
+
+__global__ void k_uq_flags(const long long* __restrict__ vals, long long n, const unsigned long long* __restrict__ hkeys,
+                           const int* __restrict__ hpos, uint32_t mask, int* __restrict__ flags,
+                           int* __restrict__ slot_of) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+        const uint32_t h = uq_find((unsigned long long)vals[p], hkeys, mask);
+        slot_of[p] = (int)h;
+        flags[p] = hpos[h] == (int)p;
+    }
+}
+
+__global__ void k_uq_emit(const long long* __restrict__ vals, long long n, const int* __restrict__ hpos,
+                          const int* __restrict__ slot_of, const int* __restrict__ rank,
+                          long long* __restrict__ uniq, long long* __restrict__ inverse) {
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+        const int first = hpos[slot_of[p]];
+        if (first == (int)p) uniq[rank[p]] = vals[p];
+        inverse[p] = rank[first];
+    }
+}
+}  // namespace
+
+extern "C" int64_t hg_unique_ws_size(int64_t n) {
+    long long cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    return (int64_t)(2 * cap + cap + 1 + 2 * n + (long long)hg_scan_ws_ints(n) + 16);
+}
+
+// uniq (n) / inverse (n) int64; *d_n_uniq = unique count.
+extern "C" int hg_unique_first_i64(const int64_t* vals, int64_t n, int64_t* uniq, int64_t* inverse,
+                                   int32_t* d_n_uniq, int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n <= 0) { cudaMemsetAsync(d_n_uniq, 0, sizeof(int), s); return HG_OK; }
+    if (n >= 0x7fffffffLL) { hg_set_error("unique_first: n too large"); return HG_EINVAL; }
+    long long cap = 16;
+    while (cap < 2 * n) cap <<= 1;
+    unsigned long long* hkeys = (unsigned long long*)ws;
+    int* hpos = ws + 2 * cap;
+    int* flags = hpos + cap + 1;
+    int* slot_of = flags + n;
+    int* scan_ws = slot_of + n;
+    cudaMemsetAsync(hkeys, 0xff, sizeof(unsigned long long) * cap, s);
+    cudaMemsetAsync(hpos, 0x7f, sizeof(int) * (cap + 1), s);
+    const int g = hg_grid(n, 256, 8);
+    const uint32_t mask = (uint32_t)(cap - 1);
+    k_uq_insert<<<g, 256, 0, s>>>((const long long*)vals, n, hkeys, hpos, mask);
+    k_uq_flags<<<g, 256, 0, s>>>((const long long*)vals, n, hkeys, hpos, mask, flags, slot_of);
+    int rc = hg_scan_launch(flags, flags, nullptr, 1, n, d_n_uniq, scan_ws, s);
+    if (rc) return rc;
+    k_uq_emit<<<g, 256, 0, s>>>((const long long*)vals, n, hpos, slot_of, flags, (long long*)uniq,
+                                (long long*)inverse);
+    return hg_check_launch("unique_first_i64");
+}
+
+// counter[v] += 1 for every v in ids (kernels.py:161-163), int64 counters
+namespace {
+__global__ void k_count_into(long long* __restrict__ counter, const int* __restrict__ ids, const int* d_n, int cap) {
+    const int n = hg_load_count(d_n, cap);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long*)&counter[ids[k]], 1ULL);
+}
+__global__ void k_count_into64(long long* __restrict__ counter, const long long* __restrict__ ids, long long n) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long*)&counter[ids[k]], 1ULL);
+}
+}  // namespace
+
+extern "C" int hg_count_into(int64_t* counter, const int32_t* ids, const int32_t* d_n, int32_t cap, void* stream) {
+    if (cap <= 0) return HG_OK;
+    k_count_into<<<hg_grid(cap, 256, 8), 256, 0, (cudaStream_t)stream>>>((long long*)counter, ids, d_n, cap);
+    return hg_check_launch("count_into");
+}
+
+extern "C" int hg_count_into_i64(int64_t* counter, const int64_t* ids, int64_t n, void* stream) {
+    if (n <= 0) return HG_OK;
+    k_count_into64<<<hg_grid(n, 256, 8), 256, 0, (cudaStream_t)stream>>>((long long*)counter, (const long long*)ids, n);
+    return hg_check_launch("count_into_i64");
+}

@@ -1,0 +1,92 @@
+"""Device plumbing: CUDA availability, raw pointers, HBM-resident graph.
+
+torch is used only to own device memory and streams; every computation on
+these buffers is one of the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from ._lib import BackendUnavailable, load
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("a CUDA device (B200, sm_100a) is required; there is no CPU fallback")
+    load()
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def ptr(t):
+    """Raw device pointer of a tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def pad4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+def i32(x, device):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int32), device=device)
+
+
+def i64(x, device):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int64), device=device)
+
+
+def u64_tensor(values, device):
+    """uint64 scalars stored bit-exactly in an int64 tensor (kernels read uint64_t*)."""
+    arr = np.asarray([int(v) & 0xFFFFFFFFFFFFFFFF for v in np.atleast_1d(values)], dtype=np.uint64)
+    return torch.as_tensor(arr.view(np.int64), device=device)
+
+
+class DeviceGraph:
+    """HBM layout of one dataset (see graph.py docstring):
+    offsets int64[V+1], targets int32[E], features fp32[V, F_pad], labels int32[V]."""
+
+    def __init__(self, offsets, targets, features=None, labels=None, device=None):
+        self.device = require_cuda(device)
+        offsets = np.asarray(offsets)
+        targets = np.asarray(targets)
+        self.num_vertices = int(offsets.shape[0] - 1)
+        self.num_edges = int(targets.shape[0])
+        if self.num_vertices >= 2**31 - 1:
+            raise ValueError("vertex ids must fit int32")
+        self.offsets = i64(offsets, self.device)
+        self.targets = i32(targets, self.device)
+        self.feat_dim = 0
+        self.feat_ld = 0
+        self.features = None
+        if features is not None:
+            feats = np.asarray(features)
+            V, F = feats.shape
+            self.feat_dim = F
+            self.feat_ld = pad4(F)
+            x = torch.zeros((V, self.feat_ld), dtype=torch.float32, device=self.device)
+            x[:, :F] = torch.as_tensor(np.ascontiguousarray(feats, dtype=np.float32), device=self.device)
+            self.features = x
+        self.labels = None if labels is None else i32(labels, self.device)
+        # first-occurrence table for the dedup kernel: INT32_MAX at rest
+        self.minpos = torch.full((self.num_vertices,), 2**31 - 1, dtype=torch.int32, device=self.device)
+
+    @classmethod
+    def from_dataset(cls, ds, device=None):
+        return cls(ds.offsets, ds.targets, ds.features, ds.labels, device=device)
+
+    def nbytes(self) -> int:
+        n = self.offsets.numel() * 8 + self.targets.numel() * 4 + self.minpos.numel() * 4
+        if self.features is not None:
+            n += self.features.numel() * 4
+        if self.labels is not None:
+            n += self.labels.numel() * 4
+        return n

@@ -1,0 +1,133 @@
+"""GPU parity of the plug-in kernels and the sampler against the golden vectors
+(produced by the reference) and the CPU oracle.  Integer outputs: bit-exact.
+segment_weighted_rows (fp64): bit-exact."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_stack, has_cuda
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_cuda(), reason="needs CUDA")]
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2311_13225_b200 import kernels
+    return kernels
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2311_13225_b200 import sampler
+    return sampler
+
+
+def test_sample_layer_golden(K, golden, golden_meta, ggraphs):
+    for k, (gname, f, s) in enumerate(golden_meta["sample_layer"]):
+        g = ggraphs[gname].graph
+        ed, es = K.sample_layer(g.offsets, g.targets, golden[f"sl{k}_dst"], f, s)
+        assert np.array_equal(ed, golden[f"sl{k}_ed"]), (k, gname, f)
+        assert np.array_equal(es, golden[f"sl{k}_es"]), (k, gname, f)
+
+
+def test_sample_layer_appendix_a(K, ggraphs):
+    star = ggraphs["star"].graph
+    ed, es = K.sample_layer(star.offsets, star.targets, np.arange(6), 3, 777)
+    assert ed.tolist() == [0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5]
+    assert es.tolist() == [5, 3, 1, 0, 1, 0, 2, 0, 3, 0, 4, 0, 5]
+
+
+def test_stable_unique_golden(K, golden):
+    for k in range(5):
+        u, inv = K.stable_unique(golden[f"su{k}_in"])
+        assert np.array_equal(u, golden[f"su{k}_u"])
+        assert np.array_equal(inv, golden[f"su{k}_inv"])
+
+
+def test_stable_unique_sentinel_and_negative(K):
+    from oracle import oracle as O
+    v = np.array([-1, 5, -1, 2**63 - 1, -(2**63), 5, 0, -1], dtype=np.int64)
+    u, inv = K.stable_unique(v)
+    ru, rinv = O.stable_unique(v)
+    assert np.array_equal(u, ru) and np.array_equal(inv, rinv)
+
+
+def _cmp(st, ref):
+    assert len(st.blocks) == len(ref)
+    for b, r in zip(st.blocks, ref):
+        assert np.array_equal(b.dst_vertices, r["dst"])
+        assert np.array_equal(b.src_vertices, r["src"])
+        assert np.array_equal(b.edge_src, r["es"])
+        assert np.array_equal(b.edge_dst, r["ed"])
+
+
+def test_sample_khop_golden(S, golden, golden_meta, ggraphs):
+    for k, (gname, fan, s) in enumerate(golden_meta["khop"]):
+        st = S.sample_khop(ggraphs[gname].graph, golden[f"kh{k}_seeds"], S.Fanouts(tuple(fan)), s)
+        _cmp(st, golden_stack(golden, f"kh{k}"))
+    blk = S.sample_one_hop_hot(ggraphs["pl"].graph, np.array([0, 10, 3, 999, 500]), 6, 31337)
+    _cmp(S.SampledBlockStack(blocks=[blk], seeds=None), golden_stack(golden, "oh0"))
+
+
+def test_sample_khop_c1(S, golden):
+    from paper_2311_13225_b200.datagen import make_dataset
+    ds = make_dataset("c1")
+    st = S.sample_khop(ds, golden["c1kh_seeds"], (10, 25), 4242)
+    _cmp(st, golden_stack(golden, "c1kh"))
+
+
+@pytest.mark.parametrize("fan", [(15, 10, 5), (10, 25), (4, 4), (40, 3)])
+def test_sample_khop_vs_oracle_c2_shape(S, fan):
+    """Full-size products-shaped batch, oracle on the same graph bytes."""
+    from oracle import oracle as O
+    from paper_2311_13225_b200.datagen import make_dataset
+    ds = make_dataset("c2", scale=0.1)
+    seeds = ds.train_ids()[:1024]
+    st = S.sample_khop(ds, seeds, fan, 0x1234567)
+    ref = O.sample_khop(O.Graph(ds.offsets, ds.targets.astype(np.int64)), seeds, fan, 0x1234567)
+    _cmp(st, [dict(dst=b.dst_vertices, src=b.src_vertices, es=b.edge_src, ed=b.edge_dst) for b in ref.blocks])
+
+
+def test_sampling_uniformity_five_sigma(K, ggraphs):
+    """test_kernels.py:92-107 on the GPU draw kernel."""
+    star = ggraphs["star"].graph
+    hits = np.zeros(6, np.int64)
+    reps = 3000
+    for seed in range(reps):
+        _, srcs = K.sample_layer(star.offsets, star.targets, np.array([0]), 3, seed)
+        assert len(set(srcs.tolist())) == 3
+        hits[srcs] += 1
+    assert np.all(np.abs(hits - reps * 0.5) <= 5 * np.sqrt(reps * 0.25)), hits
+
+
+def test_segment_weighted_rows_bitexact(K):
+    from oracle import oracle as O
+    rng = np.random.default_rng(3)
+    for n_e, n_src, n_out, d in [(400, 50, 30, 6), (5000, 300, 200, 37), (1, 1, 1, 1), (0, 5, 4, 3)]:
+        es = rng.integers(0, n_src, n_e)
+        ed = rng.integers(0, n_out, n_e)
+        w = rng.standard_normal(n_e)
+        rows = rng.standard_normal((n_src, d))
+        got = K.segment_weighted_rows(es, ed, w, rows, n_out)
+        want = np.zeros((n_out, d))
+        np.add.at(want, ed, w[:, None] * rows[es])
+        assert np.array_equal(got, want)
+        assert np.array_equal(got, O.segment_weighted_rows(es, ed, w, rows, n_out))
+
+
+def test_count_into(K):
+    c = np.zeros(10, np.int64)
+    K.count_into(c, np.array([1, 1, 3, 9, 1]))
+    assert c.tolist() == [0, 3, 0, 1, 0, 0, 0, 0, 0, 1]
+
+
+def test_sampler_errors(S, ggraphs):
+    g = ggraphs["pl"].graph
+    with pytest.raises(S.SamplerError):
+        S.sample_khop(g, np.array([], np.int64), (2,), 1)
+    with pytest.raises(S.SamplerError):
+        S.sample_khop(g, np.array([5000]), (2,), 1)
+    with pytest.raises(S.SamplerError):
+        S.sample_one_hop_hot(g, np.array([1, 1]), 2, 1)
+    with pytest.raises(S.SamplerError):
+        S.Fanouts(())
