@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(NT) k_gemm(const float* __restrict__ A1, int l
     __shared__ float As[BK][BM + 4];
     __shared__ float Bs[BK][BN + 4];
     const int M = hg_load_count(d_M, M_cap);
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
     if (m0 >= M) return;
     float acc[4][4] = {};
     gemm_accumulate<TRANS_B>(A1, lda1, K1, B1, ldb1, N, m0, n0, M, acc, As, Bs);
@@ -147,7 +147,7 @@ extern "C" int hg_gemm_f32(const float* A1, int32_t lda1, int32_t K1, const floa
                            int32_t trans_b, float* C, int32_t ldc, int32_t N, const int32_t* d_M, int32_t M_cap,
                            int32_t act, void* stream) {
     if (M_cap <= 0 || N <= 0) return HG_OK;
-    dim3 grid(hg_ceil_div(N, BN), hg_ceil_div(M_cap, BM));
+    dim3 grid(hg_ceil_div(M_cap, BM), hg_ceil_div(N, BN));
     cudaStream_t s = (cudaStream_t)stream;
     if (trans_b)
         k_gemm<true><<<grid, NT, 0, s>>>(A1, lda1, K1, B1, ldb1, A2, lda2, K2, B2, ldb2, C, ldc, N, d_M, M_cap, act);

@@ -1,0 +1,384 @@
+"""The device-resident training step (the hot loop of orchestrator._run_epoch,
+orchestrator.py:456-545, restated for one B200).
+
+One step = one batch:
+
+    sample L blocks top-down (K1-K3, sampler.py:130-147)
+    -> historical-embedding lookup for the bottom destinations (store.py:67-98,
+       orchestrator.py:486-500)
+    -> bottom layer: fused feature gather + aggregation (K4/K5, orchestrator.py:239,
+       gnnmath.py:157-179 / 105-126), dense transform (K8) + ReLU, injection of
+       reused embeddings (gnnmath.py:240-245)
+    -> upper layers, logits, softmax-CE (gnnmath.py:263-274)
+    -> backward (gnnmath.py:250-260; dx only above the bottom layer)
+    -> SGD / Adam over one flat parameter buffer + max |dw| (orchestrator.py:246-255)
+    -> per-batch record (loss, max |dw|).
+
+Every size that depends on sampling lives in device memory; buffers are sized
+by static upper bounds (n_src <= n_dst*(f+1), <= V), so the whole step is
+enqueued with zero host synchronisation and can be captured into a single
+CUDA graph and replayed per batch.  Per-batch inputs (seed ids, the batch
+rng seed and the store window parameters) are copied from pinned host memory
+into fixed device buffers before each replay.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceGraph, pad4, ptr, stream_ptr
+from .sampler import LayerSampler
+
+# per-batch parameter block layout (see csrc/hg_train.cu BP_*)
+BP_RNG_SEED, BP_N_SEEDS, BP_READING_BATCH, BP_BATCH_IN_EPOCH = 0, 1, 2, 3
+BP_CPU_TAG, BP_TABLE_SEL, BP_CUR_STAMP, BP_WARMUP = 4, 5, 6, 7
+BP_SIZE = 8
+
+
+class DenseParams:
+    """All layer weights in one flat fp32 device buffer (gnnmath.ModelParams,
+    gnnmath.py:24-52).  GCN: [W] per layer; SAGE: [W_self, W_neigh] per layer,
+    each row-major [d_in, d_out]."""
+
+    def __init__(self, model: str, dims, weights, device):
+        self.model = model
+        self.dims = [int(d) for d in dims]
+        self.L = len(self.dims) - 1
+        self.n_mats = 1 if model == "gcn" else 2
+        self.offs = []
+        off = 0
+        for l in range(self.L):
+            row = []
+            for _ in range(self.n_mats):
+                row.append(off)
+                off += self.dims[l] * self.dims[l + 1]
+            self.offs.append(row)
+        self.numel = off
+        self.flat = torch.zeros(off, dtype=torch.float32, device=device)
+        self.grad = torch.zeros_like(self.flat)
+        if weights is not None:
+            self.load(weights)
+
+    def view(self, l: int, m: int, buf=None) -> torch.Tensor:
+        buf = self.flat if buf is None else buf
+        n = self.dims[l] * self.dims[l + 1]
+        return buf[self.offs[l][m]:self.offs[l][m] + n].view(self.dims[l], self.dims[l + 1])
+
+    def load(self, weights):
+        for l, lw in enumerate(weights):
+            for m, w in enumerate(lw):
+                self.view(l, m).copy_(torch.as_tensor(np.asarray(w, dtype=np.float32)))
+
+    def to_numpy(self, buf=None):
+        return [[self.view(l, m, buf).cpu().numpy().astype(np.float64) for m in range(self.n_mats)]
+                for l in range(self.L)]
+
+    @property
+    def bottom_numel(self) -> int:
+        return self.n_mats * self.dims[0] * self.dims[1]
+
+
+@dataclass
+class HotBuffers:
+    """Device embedding store (store.py:24-146): two physical tables that swap
+    the roles "current" / "staging" per super-batch via BP_TABLE_SEL; entries are
+    valid for reading iff their stamp equals BP_CUR_STAMP, which makes both
+    advance_super_batch and reset_epoch O(1) (no clearing)."""
+
+    slot_of: torch.Tensor      # int32 [V]: hot-list position or -1
+    cpu_tag_of: torch.Tensor   # int32 [V]: membership tag of the current cpu_set
+    tab: list                  # 2 x fp32 [n_hot, H]
+    ver: list                  # 2 x int32 [n_hot]
+    stamp: list                # 2 x int32 [n_hot]
+    inj_mask: torch.Tensor     # uint8 [cap_dst0]
+    inj_slot: torch.Tensor     # int32 [cap_dst0]
+    batch_hits: torch.Tensor   # int32 [max_batches]
+    batch_miss: torch.Tensor
+    batch_warm: torch.Tensor
+    stats: torch.Tensor        # uint64 as int64 [2]: packed (max gap, batch), violations
+    puts: torch.Tensor         # int32 [1]
+    gap_bound: int
+    H: int
+
+    @classmethod
+    def create(cls, V, hot_list, H, n, cap_dst0, max_batches, device):
+        n_hot = max(int(hot_list.shape[0]), 1)
+        slot_of = torch.full((V,), -1, dtype=torch.int32, device=device)
+        if hot_list.shape[0]:
+            slot_of[torch.as_tensor(hot_list.astype(np.int64), device=device)] = torch.arange(
+                hot_list.shape[0], dtype=torch.int32, device=device)
+        z = lambda *s, dt=torch.int32: torch.zeros(*s, dtype=dt, device=device)  # noqa: E731
+        return cls(slot_of=slot_of, cpu_tag_of=torch.full((V,), -1, dtype=torch.int32, device=device),
+                   tab=[z(n_hot, H, dt=torch.float32), z(n_hot, H, dt=torch.float32)],
+                   ver=[z(n_hot), z(n_hot)],
+                   stamp=[torch.full((n_hot,), -1, dtype=torch.int32, device=device) for _ in range(2)],
+                   inj_mask=z(max(cap_dst0, 1), dt=torch.uint8), inj_slot=z(max(cap_dst0, 1)),
+                   batch_hits=z(max_batches), batch_miss=z(max_batches), batch_warm=z(max_batches),
+                   stats=z(2, dt=torch.int64), puts=z(1), gap_bound=2 * n - 1, H=H)
+
+    def reset_counters(self):
+        for t in (self.batch_hits, self.batch_miss, self.batch_warm, self.puts):
+            t.zero_()
+
+
+class TrainEngine:
+    """Buffers + kernel sequence of one training step for a fixed model/fanout."""
+
+    def __init__(self, dg: DeviceGraph, model: str, dims, fanouts, batch_cap: int, lr: float,
+                 optimizer: str = "sgd", weights=None, hot: HotBuffers | None = None, max_batches: int = 1,
+                 allreduce=None):
+        _lib.load()
+        if model not in ("gcn", "sage"):
+            raise ValueError(f"unknown model {model!r}")
+        self.dg, self.model = dg, model
+        self.sage = model == "sage"
+        self.dims = [int(d) for d in dims]
+        self.fan = [int(f) for f in fanouts]
+        self.L = len(self.fan)
+        assert len(self.dims) == self.L + 1
+        self.batch_cap = int(batch_cap)
+        self.lr = float(lr)
+        self.optimizer = optimizer
+        self.hot = hot
+        self.allreduce = allreduce  # callable(grad_tensor) for multi-GPU data parallel
+        dev = self.device = dg.device
+        V = dg.num_vertices
+        if self.dims[0] != dg.feat_dim:
+            raise ValueError("feature width mismatch")
+        self.ld = [pad4(d) for d in self.dims]
+        self.ld[0] = dg.feat_ld
+        # ---- capacities, top-down (sampler.py:142-146) ----
+        self.cap_dst = [0] * self.L
+        self.cap_src = [0] * self.L
+        self.cap_dst[self.L - 1] = self.batch_cap
+        for l in range(self.L - 1, -1, -1):
+            self.cap_src[l] = int(min(V, self.cap_dst[l] * (self.fan[l] + 1)))
+            if l > 0:
+                self.cap_dst[l - 1] = self.cap_src[l]
+        self.samplers = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage,
+                                      need_outdeg=not self.sage, need_csc=l > 0) for l in range(self.L)]
+        # ---- per-batch inputs ----
+        z32 = lambda *s: torch.zeros(*s, dtype=torch.int32, device=dev)  # noqa: E731
+        zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        self.seeds = z32(self.batch_cap)
+        self.counts_in = z32(2)  # [n_seeds, n_div]
+        self.bp = torch.zeros(BP_SIZE, dtype=torch.int64, device=dev)
+        # ---- parameters ----
+        self.params = DenseParams(model, self.dims, weights, dev)
+        if optimizer == "adam":
+            self.adam_m = torch.zeros_like(self.params.flat)
+            self.adam_v = torch.zeros_like(self.params.flat)
+            self.adam_t = z32(1)
+        # ---- activations / gradients ----
+        self.self_buf = zf(self.cap_dst[0], self.ld[0]) if self.sage else None
+        self.agg = [zf(self.cap_dst[l], self.ld[l]) for l in range(self.L)]
+        self.out = [zf(self.cap_dst[l], self.ld[l + 1]) for l in range(self.L)]  # out[l] = H_{l+1}
+        self.dz = [zf(self.cap_dst[l], self.ld[l + 1]) for l in range(self.L)]
+        self.dagg = [zf(self.cap_dst[l], self.ld[l]) if l > 0 else None for l in range(self.L)]
+        self.dself = [zf(self.cap_dst[l], self.ld[l]) if (l > 0 and self.sage) else None for l in range(self.L)]
+        lib = _lib.load()
+        ws = max(int(lib.hg_wgrad_ws_size(self.dims[l], self.dims[l + 1], self.cap_dst[l])) for l in range(self.L))
+        self.wgrad_ws = zf(max(ws, 1))
+        self.d_loss = zf(1)
+        self.d_maxdelta = z32(1)
+        self.loss_arr = zf(max(max_batches, 1))
+        self.md_arr = zf(max(max_batches, 1))
+        self.graph = None
+
+    # ------------------------------------------------------------------
+    def frontier(self, l):
+        """(frontier ids, device count) of layer l's destinations."""
+        if l == self.L - 1:
+            return self.seeds, self.counts_in[0:1]
+        s = self.samplers[l + 1]
+        return s.src, s.n_src
+
+    def enqueue_sample(self, stream=None, seed_ptr=None, layers=None):
+        """Blocks L-1 .. 0 (sampler.py:142-146); layer l's stream is
+        derive_seed(*seed, 0x5A, l), computed on device."""
+        sp = self.bp if seed_ptr is None else seed_ptr
+        for l in (range(self.L - 1, -1, -1) if layers is None else layers):
+            fr, n = self.frontier(l)
+            self.samplers[l].run(fr, n, sp, l, stream)
+
+    def enqueue_step(self, stream=None):
+        s = stream_ptr(stream)
+        L, P = self.L, self.params
+        g = self.dg
+        self.enqueue_sample(stream)
+        hot = self.hot
+        inj = None
+        if hot is not None and L > 1:
+            fr0, n0 = self.frontier(0)
+            _lib.call("hg_store_lookup", ptr(fr0), ptr(n0), self.cap_dst[0], ptr(self.bp), ptr(hot.cpu_tag_of),
+                      ptr(hot.slot_of), ptr(hot.ver[0]), ptr(hot.ver[1]), ptr(hot.stamp[0]), ptr(hot.stamp[1]),
+                      hot.gap_bound, ptr(hot.inj_mask), ptr(hot.inj_slot), ptr(hot.batch_hits),
+                      ptr(hot.batch_miss), ptr(hot.batch_warm), ptr(hot.stats), s)
+            inj = hot.inj_mask
+        model = 0 if self.sage else 1
+        # ---------------- forward ----------------
+        for l in range(L):
+            smp = self.samplers[l]
+            fr, n = self.frontier(l)
+            d_in, d_out = self.dims[l], self.dims[l + 1]
+            if l == 0:
+                hin, ld_in, glob = g.features, g.feat_ld, 1
+            else:
+                hin, ld_in, glob = self.out[l - 1], self.ld[l], 0
+            self_out = self.self_buf if (l == 0 and self.sage) else None
+            _lib.call("hg_aggregate_fwd", model, glob, ptr(hin), ld_in, self.ld[l], ptr(fr), ptr(n),
+                      self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
+                      ptr(smp.nself), ptr(smp.outdeg), ptr(inj if l == 0 else None), ptr(self_out),
+                      self.ld[0], ptr(self.agg[l]), self.ld[l], s)
+            act = 1 if l < L - 1 else 0
+            if self.sage:
+                a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
+                _lib.call("hg_gemm_f32", ptr(a1), lda1, d_in, ptr(P.view(l, 0)), d_out, ptr(self.agg[l]),
+                          self.ld[l], d_in, ptr(P.view(l, 1)), d_out, 0, ptr(self.out[l]), self.ld[l + 1], d_out,
+                          ptr(n), self.cap_dst[l], act, s)
+            else:
+                _lib.call("hg_gemm_f32", ptr(self.agg[l]), self.ld[l], d_in, ptr(P.view(l, 0)), d_out, None, 0, 0,
+                          None, 0, 0, ptr(self.out[l]), self.ld[l + 1], d_out, ptr(n), self.cap_dst[l], act, s)
+            if l == 0 and inj is not None:
+                _lib.call("hg_inject_rows", ptr(hot.inj_mask), ptr(hot.inj_slot), ptr(n), self.cap_dst[0],
+                          ptr(self.bp), ptr(hot.tab[0]), ptr(hot.tab[1]), hot.H, ptr(self.out[0]), self.ld[1], s)
+        # ---------------- loss ----------------
+        C = self.dims[L]
+        _lib.call("hg_softmax_xent", ptr(self.out[L - 1]), self.ld[L], C, ptr(self.counts_in[0:1]), self.batch_cap,
+                  ptr(g.labels), ptr(self.seeds), ptr(self.counts_in[1:2]), ptr(self.dz[L - 1]), self.ld[L],
+                  ptr(self.d_loss), s)
+        # ---------------- backward ----------------
+        for l in range(L - 1, -1, -1):
+            smp = self.samplers[l]
+            fr, n = self.frontier(l)
+            d_in, d_out = self.dims[l], self.dims[l + 1]
+            if self.sage:
+                a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
+                _lib.call("hg_wgrad_f32", ptr(a1), lda1, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(n),
+                          self.cap_dst[l], ptr(P.view(l, 0, P.grad)), 1.0, ptr(self.wgrad_ws), s)
+                _lib.call("hg_wgrad_f32", ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
+                          ptr(n), self.cap_dst[l], ptr(P.view(l, 1, P.grad)), 1.0, ptr(self.wgrad_ws), s)
+            else:
+                _lib.call("hg_wgrad_f32", ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
+                          ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), 1.0, ptr(self.wgrad_ws), s)
+            if l == 0:
+                continue
+            if self.sage:  # dself = dz W_self^T, dmean = dz W_neigh^T
+                _lib.call("hg_gemm_f32", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_out, None, 0,
+                          0, None, 0, 1, ptr(self.dself[l]), self.ld[l], d_in, ptr(n), self.cap_dst[l], 0, s)
+                _lib.call("hg_gemm_f32", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 1)), d_out, None, 0,
+                          0, None, 0, 1, ptr(self.dagg[l]), self.ld[l], d_in, ptr(n), self.cap_dst[l], 0, s)
+            else:
+                _lib.call("hg_gemm_f32", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_out, None, 0,
+                          0, None, 0, 1, ptr(self.dagg[l]), self.ld[l], d_in, ptr(n), self.cap_dst[l], 0, s)
+            _lib.call("hg_aggregate_bwd", model, ptr(self.dagg[l]), self.ld[l], ptr(self.dself[l]), self.ld[l],
+                      self.ld[l], ptr(fr), ptr(n), self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots),
+                      ptr(smp.nself), ptr(smp.outdeg), ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end),
+                      ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]), self.ld[l],
+                      ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]), self.ld[l], s)
+        # ---------------- update ----------------
+        if self.allreduce is not None:
+            self.allreduce(P.grad)
+        if self.optimizer == "sgd":
+            _lib.call("hg_sgd", ptr(P.flat), ptr(P.grad), P.numel, self.lr, ptr(self.d_maxdelta), s)
+        else:
+            _lib.call("hg_adam", ptr(P.flat), ptr(P.grad), ptr(self.adam_m), ptr(self.adam_v), P.numel, self.lr,
+                      0.9, 0.999, 1e-8, ptr(self.adam_t), ptr(self.d_maxdelta), s)
+        _lib.call("hg_record_batch", ptr(self.bp), ptr(self.d_loss), ptr(self.d_maxdelta), ptr(self.loss_arr),
+                  ptr(self.md_arr), s)
+
+    # ------------------------------------------------------------------
+    def capture(self, stream: torch.cuda.Stream | None = None):
+        """Capture enqueue_step into a CUDA graph (one launch per batch)."""
+        stream = stream or torch.cuda.Stream(device=self.device)
+        saved = self._save_state()
+        stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(stream):  # warm-up outside capture (lazy module loads)
+            self.enqueue_step()
+        torch.cuda.current_stream(self.device).wait_stream(stream)
+        torch.cuda.synchronize(self.device)
+        self._restore_state(saved)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            self.enqueue_step()
+        torch.cuda.synchronize(self.device)
+        self.graph = g
+        return g
+
+    def _save_state(self):
+        st = {"flat": self.params.flat.clone(), "md": self.d_maxdelta.clone(),
+              "loss": self.loss_arr.clone(), "mdarr": self.md_arr.clone()}
+        if self.optimizer == "adam":
+            st.update(m=self.adam_m.clone(), v=self.adam_v.clone(), t=self.adam_t.clone())
+        if self.hot is not None:
+            h = self.hot
+            st.update(hits=h.batch_hits.clone(), miss=h.batch_miss.clone(), warm=h.batch_warm.clone(),
+                      stats=h.stats.clone())
+        return st
+
+    def _restore_state(self, st):
+        """The warm-up pass ran one real update; undo it so capture is side-effect free."""
+        self.params.flat.copy_(st["flat"])
+        self.d_maxdelta.copy_(st["md"])
+        self.loss_arr.copy_(st["loss"])
+        self.md_arr.copy_(st["mdarr"])
+        if self.optimizer == "adam":
+            self.adam_m.copy_(st["m"])
+            self.adam_v.copy_(st["v"])
+            self.adam_t.copy_(st["t"])
+        if self.hot is not None:
+            h = self.hot
+            h.batch_hits.copy_(st["hits"])
+            h.batch_miss.copy_(st["miss"])
+            h.batch_warm.copy_(st["warm"])
+            h.stats.copy_(st["stats"])
+        torch.cuda.synchronize(self.device)
+
+    def run_step(self, stream=None):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.enqueue_step(stream)
+
+
+class BatchFeeder:
+    """Pinned-host -> device staging of per-batch inputs (seed ids, counts and the
+    parameter block), ring-buffered so the host never overwrites a slot whose
+    copy has not completed."""
+
+    def __init__(self, engine: TrainEngine, slots: int = 4):
+        self.e = engine
+        cap = engine.batch_cap
+        self.seeds = [torch.zeros(cap, dtype=torch.int32).pin_memory() for _ in range(slots)]
+        self.counts = [torch.zeros(2, dtype=torch.int32).pin_memory() for _ in range(slots)]
+        self.bp = [torch.zeros(BP_SIZE, dtype=torch.int64).pin_memory() for _ in range(slots)]
+        self.events = [None] * slots
+        self.k = 0
+        self.h2d_bytes = 0
+
+    def feed(self, seeds: np.ndarray, rng_seed: int, reading_batch: int, batch_in_epoch: int, cpu_tag: int = -1,
+             table_sel: int = 0, cur_stamp: int = -1, warm: int = 0, n_div: int | None = None):
+        k = self.k
+        self.k = (k + 1) % len(self.seeds)
+        if self.events[k] is not None:
+            self.events[k].synchronize()
+        n = int(seeds.shape[0])
+        if n > self.e.batch_cap:
+            raise ValueError("batch larger than the engine's capacity")
+        self.seeds[k].numpy()[:n] = seeds
+        self.counts[k].numpy()[:] = (n, n if n_div is None else n_div)
+        rs = int(rng_seed) & 0xFFFFFFFFFFFFFFFF
+        self.bp[k].numpy()[:] = np.array([rs], dtype=np.uint64).view(np.int64)[0], n, reading_batch, \
+            batch_in_epoch, cpu_tag, table_sel, cur_stamp, warm
+        e = self.e
+        e.seeds[:n].copy_(self.seeds[k][:n], non_blocking=True)
+        e.counts_in.copy_(self.counts[k], non_blocking=True)
+        e.bp.copy_(self.bp[k], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[k] = ev
+        self.h2d_bytes = n * 4 + 8 + BP_SIZE * 8

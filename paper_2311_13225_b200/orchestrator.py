@@ -1,0 +1,470 @@
+"""End-to-end training driver (reference orchestrator.py:1-739) on one B200.
+
+Keeps the reference's public surface — ``TrainConfig``, ``EpochReport``,
+``run_training``, ``evaluate``, ``build_epoch_plan``, ``epsilon_monitor`` — and
+its numerics contract: the same epoch shuffles, batches, batch/hot/queue
+stream seeds, hot list, queues, producer versions (chunk j of super-batch g+1
+pinned to version first+group[j]), double-buffered store with the 2n-1 gap
+bound, injection of reused bottom-layer embeddings and epsilon trace.
+
+What changes is where it runs: every batch is one replay of a captured CUDA
+graph (engine.TrainEngine) and the hot-embedding producer runs on its own CUDA
+stream gated by per-version events ("pipelined"), or inline on the training
+stream ("serial"); both give bit-identical results.  The reference's
+discrete-event device simulator (devsim/skeletons/presets) and its idle-time
+feedback are out of scope: with no modelled CPU/GPU split the hot-set partition
+keeps every queued vertex in the reuse set (hotness.partition_hot with zero
+idle time, hotness.py:129), i.e. the reference with simulate_costs=False.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib, runplan
+from .device import DeviceGraph, pad4, ptr, stream_ptr, u64_tensor
+from .engine import BatchFeeder, HotBuffers, TrainEngine
+from .gnnmath import init_params
+from .hotness import estimate_hotness, select_hot
+from .sampler import Fanouts, LayerSampler
+from .store import FallbackBudgetExceeded, StalenessViolation
+
+EXECUTIONS = ("serial", "pipelined")
+STRATEGIES = ("case1", "case2", "case3", "case4", "layer-based")  # skeletons.STRATEGIES
+
+
+class ConfigError(ValueError):
+    """orchestrator.py:66-67."""
+
+
+@dataclass
+class TrainConfig:
+    """orchestrator.py:74-146 (same fields and defaults)."""
+
+    model: str = "gcn"
+    layers: int = 3
+    fanouts: tuple = (25, 10, 5)
+    hidden_dim: int = 64
+    batch_size: int = 1024
+    super_batch_n: int = 4
+    hot_ratio: float = 0.2
+    strategy: str = "layer-based"
+    lr: float = 0.1
+    epochs: int = 1
+    seed: int = 0
+    optimizer: str = "sgd"
+    presample_rounds: int = 20
+    execution: str = "serial"
+    stage_budget_frac: float = 1.0
+    max_fallback_frac: float = 0.5
+    simulate_costs: bool = False  # accepted for compatibility; the simulator is out of scope
+    preset: object = None
+    use_graph: bool = True  # replay each step as one captured CUDA graph
+
+    def validate(self) -> None:
+        if self.model not in ("gcn", "sage"):
+            raise ConfigError(f"model must be gcn or sage, got {self.model!r}")
+        if self.layers != len(self.fanouts):
+            raise ConfigError(f"layers ({self.layers}) must equal len(fanouts) ({len(self.fanouts)})")
+        try:
+            Fanouts(tuple(self.fanouts))
+        except ValueError as exc:
+            raise ConfigError(str(exc)) from exc
+        if self.super_batch_n < 1:
+            raise ConfigError(f"super-batch size must be >= 1, got {self.super_batch_n}")
+        if self.batch_size < 1:
+            raise ConfigError(f"batch size must be >= 1, got {self.batch_size}")
+        if not (0.0 <= self.hot_ratio <= 1.0):
+            raise ConfigError(f"hot ratio must be in [0, 1], got {self.hot_ratio}")
+        if self.strategy not in STRATEGIES:
+            raise ConfigError(f"strategy must be one of {STRATEGIES}, got {self.strategy!r}")
+        if self.execution not in EXECUTIONS:
+            raise ConfigError(f"execution must be one of {EXECUTIONS}, got {self.execution!r}")
+        if self.optimizer not in ("sgd", "adam"):
+            raise ConfigError(f"optimizer must be sgd or adam, got {self.optimizer!r}")
+        if self.epochs < 1:
+            raise ConfigError(f"epochs must be >= 1, got {self.epochs}")
+        if not (0.0 < self.stage_budget_frac <= 1.0):
+            raise ConfigError("stage budget fraction must be in (0, 1]")
+
+    def dims(self, feat_dim: int, num_classes: int) -> list:
+        return [feat_dim] + [self.hidden_dim] * (self.layers - 1) + [num_classes]
+
+    def to_dict(self) -> dict:
+        return {"model": self.model, "layers": self.layers, "fanouts": list(self.fanouts),
+                "hidden_dim": self.hidden_dim, "batch_size": self.batch_size,
+                "super_batch_n": self.super_batch_n, "hot_ratio": self.hot_ratio, "strategy": self.strategy,
+                "lr": self.lr, "epochs": self.epochs, "seed": self.seed, "optimizer": self.optimizer,
+                "presample_rounds": self.presample_rounds, "execution": self.execution,
+                "stage_budget_frac": self.stage_budget_frac, "max_fallback_frac": self.max_fallback_frac}
+
+
+@dataclass
+class EpochReport:
+    """orchestrator.py:149-169 (simulator fields dropped)."""
+
+    epoch: int
+    losses: list = field(default_factory=list)
+    batch_rows: list = field(default_factory=list)
+    val_accuracy: float = 0.0
+    test_accuracy: float = 0.0
+    epsilon_trace: list = field(default_factory=list)
+    max_weight_deltas: list = field(default_factory=list)
+    max_gap: int = 0
+    max_gap_batch: int = -1
+    max_gap_super_batch: int = -1
+    stage_seconds_measured: dict = field(default_factory=dict)
+    stage_events: list = field(default_factory=list)  # (target_sb, version, count)
+    warmup_computed: int = 0
+    reuse_hits: int = 0
+    fallbacks: int = 0
+
+
+@dataclass
+class EpochPlan:
+    """orchestrator.py:172-181; queues live on the device, sizes on the host."""
+
+    epoch: int
+    batches: list
+    groups: list
+    batch_seeds: list
+    first_global_batch: int
+    queues: dict = field(default_factory=dict)       # g -> device int32 tensor
+    queue_sizes: dict = field(default_factory=dict)  # g -> int
+    hot_seeds: dict = field(default_factory=dict)    # g -> int
+
+
+class HotProducer:
+    """Bottom-layer embeddings for queued hot vertices (orchestrator.py:259-271,
+    381-395): one-hop sample of the chunk with the super-batch's hot stream
+    (sampler.sample_one_hop_hot), fused gather+aggregate, dense transform with
+    the bottom weights of the pinned version, ReLU iff L > 1, then put into the
+    staging table."""
+
+    def __init__(self, engine: TrainEngine, cap_chunk: int, n_snaps: int):
+        e = self.e = engine
+        dev = e.device
+        self.cap = max(int(cap_chunk), 1)
+        # own first-occurrence table: the producer runs concurrently with the
+        # training stream's samplers
+        self.smp = LayerSampler(e.dg, self.cap, e.fan[0], need_nself=e.sage, need_outdeg=not e.sage,
+                                minpos=torch.full_like(e.dg.minpos, 2**31 - 1))
+        zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        self.self_buf = zf(self.cap, e.ld[0]) if e.sage else None
+        self.agg = zf(self.cap, e.ld[0])
+        self.emb = zf(self.cap, e.ld[1])
+        self.snaps = zf(max(n_snaps, 1), e.params.bottom_numel)
+        self.d_n = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def snapshot(self, j: int):
+        """_ParamCell.publish (orchestrator.py:281-284): copy W0 at this version."""
+        self.snaps[j].copy_(self.e.params.flat[:self.e.params.bottom_numel])
+
+    def run_chunk(self, ids: torch.Tensor, c: int, seed_dev: torch.Tensor, snap: int, version: int, stamp: int,
+                  table: int, stream=None):
+        e, hot = self.e, self.e.hot
+        s = stream_ptr(stream)
+        d0, d1 = e.dims[0], e.dims[1]
+        self.smp.run(ids, None, seed_dev, 0, stream, cap_dst=c)
+        model = 0 if e.sage else 1
+        _lib.call("hg_aggregate_fwd", model, 1, ptr(e.dg.features), e.dg.feat_ld, e.ld[0], ptr(ids), None, c,
+                  e.fan[0], ptr(self.smp.counts), ptr(self.smp.slots), ptr(self.smp.slot_local), ptr(self.smp.nself),
+                  ptr(self.smp.outdeg), None, ptr(self.self_buf), e.ld[0], ptr(self.agg), e.ld[0], s)
+        w = self.snaps[snap]
+        act = 1 if e.L > 1 else 0
+        if e.sage:
+            _lib.call("hg_gemm_f32", ptr(self.self_buf), e.ld[0], d0, ptr(w[:d0 * d1]), d1, ptr(self.agg), e.ld[0], d0,
+                      ptr(w[d0 * d1:2 * d0 * d1]), d1, 0, ptr(self.emb), e.ld[1], d1, None, c, act, s)
+        else:
+            _lib.call("hg_gemm_f32", ptr(self.agg), e.ld[0], d0, ptr(w[:d0 * d1]), d1, None, 0, 0, None, 0, 0,
+                      ptr(self.emb), e.ld[1], d1, None, c, act, s)
+        _lib.call("hg_store_put", ptr(ids), None, c, ptr(self.emb), e.ld[1], hot.H, ptr(hot.slot_of),
+                  ptr(hot.tab[table]), ptr(hot.ver[table]), ptr(hot.stamp[table]), int(version), int(stamp),
+                  ptr(hot.puts), s)
+
+
+class Trainer:
+    """State of one run_training call (orchestrator.py:183-196 _RunState)."""
+
+    def __init__(self, ds, config: TrainConfig, device=None, hot_list=None, weights=None, dist=None):
+        config.validate()
+        self.cfg = config
+        self.ds = ds
+        self.dg = ds if isinstance(ds, DeviceGraph) else DeviceGraph.from_dataset(ds, device=device)
+        self.train_ids = np.nonzero(np.asarray(ds.train_mask))[0].astype(np.int64)
+        self.fan = tuple(int(f) for f in config.fanouts)
+        C = int(np.asarray(ds.labels).max()) + 1
+        self.dims = config.dims(self.dg.feat_dim, C)
+        self.dist = dist
+        if weights is None:
+            weights = init_params(config.model, self.dims, config.seed).weights
+        self.layer_based = config.strategy == "layer-based"
+        n_batches = (self.train_ids.shape[0] + config.batch_size - 1) // config.batch_size
+        self.engine = TrainEngine(self.dg, config.model, self.dims, self.fan, config.batch_size, config.lr,
+                                  optimizer=config.optimizer, weights=weights, max_batches=n_batches,
+                                  allreduce=dist.allreduce if dist is not None else None)
+        self.version = 0
+        # ---- hot list (hotness.py:70-108 via orchestrator.py:692-702) ----
+        if hot_list is None:
+            hot_list = np.empty(0, np.int64)
+            if self.layer_based and config.hot_ratio > 0 and config.layers > 1:
+                table = estimate_hotness(self.dg, self.train_ids, Fanouts(self.fan), config.presample_rounds,
+                                         config.seed, batch_size=config.batch_size, engine=self.engine)
+                hot_list = select_hot(table, config.hot_ratio)
+        self.hot_list = np.asarray(hot_list, np.int64)
+        self.use_hot = self.layer_based and self.hot_list.size > 0 and config.layers > 1
+        self.emb_dim = config.hidden_dim if config.layers > 1 else C
+        dev = self.dg.device
+        if self.layer_based:
+            self.engine.hot = HotBuffers.create(self.dg.num_vertices, self.hot_list, self.emb_dim,
+                                                config.super_batch_n, self.engine.cap_dst[0], max(n_batches, 1), dev)
+        self.hot_dev = torch.as_tensor(self.hot_list.astype(np.int32), device=dev) if self.hot_list.size else None
+        self.reach_tag = torch.full((self.dg.num_vertices,), -1, dtype=torch.int32, device=dev) \
+            if self.use_hot else None
+        self.producer = None
+        self.tag_serial = 0
+        self.stamp_serial = 0
+        self.feeder = BatchFeeder(self.engine)
+        self.prod_stream = torch.cuda.Stream(device=dev) if config.execution == "pipelined" else None
+        self.batch_to_group = {}
+        if config.use_graph:
+            self.engine.capture()
+
+    # ------------------------------------------------------------------
+    def _new_tag(self):
+        self.tag_serial += 1
+        return self.tag_serial
+
+    def build_epoch_plan(self, epoch: int, first_global_batch: int) -> EpochPlan:
+        """orchestrator.py:200-229; the replay sampling and the hot-list filter run
+        on the device; only the queue sizes come back to the host."""
+        cfg, e = self.cfg, self.engine
+        order = runplan.shuffle_epoch(self.train_ids, cfg.seed, epoch)
+        batches = runplan.split_batches(order, cfg.batch_size)
+        groups = runplan.super_batch_groups(len(batches), cfg.super_batch_n)
+        seeds = [runplan.batch_sample_seed(cfg.seed, epoch, b) for b in range(len(batches))]
+        plan = EpochPlan(epoch=epoch, batches=batches, groups=groups, batch_seeds=seeds,
+                         first_global_batch=first_global_batch)
+        if not self.use_hot:
+            return plan
+        dev = self.dg.device
+        lib = _lib.load()
+        n_hot = int(self.hot_list.shape[0])
+        ws = torch.zeros(int(lib.hg_filter_ws_size(n_hot)), dtype=torch.int32, device=dev)
+        counts = torch.zeros(len(groups), dtype=torch.int32, device=dev)
+        for g in range(1, len(groups)):
+            tag = self._new_tag()
+            rs = runplan.queue_replay_seed(cfg.seed, epoch, g)
+            for b in groups[g]:
+                self.feeder.feed(batches[b], rs, 0, 0)
+                # blocks L-1 .. 1 fix the bottom destinations (= layer-1 sources)
+                e.enqueue_sample(layers=range(e.L - 1, 0, -1))
+                fr0, n0 = e.frontier(0)
+                _lib.call("hg_tag_vertices", ptr(fr0), ptr(n0), e.cap_dst[0], ptr(self.reach_tag), tag,
+                          stream_ptr())
+            q = torch.zeros(max(n_hot, 1), dtype=torch.int32, device=dev)
+            _lib.call("hg_filter_tagged", ptr(self.hot_dev), n_hot, ptr(self.reach_tag), tag, ptr(q),
+                      ptr(counts[g:g + 1]), ptr(ws), stream_ptr())
+            plan.queues[g] = q
+            plan.hot_seeds[g] = runplan.hot_sample_seed(cfg.seed, epoch, g)
+        sizes = counts.cpu().numpy()
+        for g in range(1, len(groups)):
+            k = int(sizes[g])
+            if cfg.stage_budget_frac < 1.0 and k:
+                k = int(np.ceil(k * cfg.stage_budget_frac))
+            plan.queue_sizes[g] = k
+        return plan
+
+    # ------------------------------------------------------------------
+    def run_epoch(self, plan: EpochPlan) -> EpochReport:
+        """orchestrator.py:330-618 (batch loop :456-545)."""
+        cfg, e = self.cfg, self.engine
+        hot = e.hot
+        rep = EpochReport(epoch=plan.epoch)
+        dev = self.dg.device
+        t0 = time.perf_counter()
+        nb = len(plan.batches)
+        if hot is not None:
+            hot.reset_counters()
+        if self.use_hot and self.producer is None:
+            cap = max([plan.queue_sizes.get(g, 0) for g in plan.queue_sizes] + [1])
+            cap = (cap + cfg.super_batch_n - 1) // cfg.super_batch_n
+            self.producer = HotProducer(e, max(cap, 1), cfg.super_batch_n)
+        elif self.producer is not None:
+            need = max([(plan.queue_sizes.get(g, 0) + cfg.super_batch_n - 1) // cfg.super_batch_n
+                        for g in plan.queue_sizes] + [1])
+            if need > self.producer.cap:
+                self.producer = HotProducer(e, need, cfg.super_batch_n)
+        hot_seed_dev = {g: u64_tensor(s, dev) for g, s in plan.hot_seeds.items()}
+        main = torch.cuda.current_stream(dev)
+        # store epoch reset (store.py:120-130): fresh stamps make old entries unreadable
+        stamps = {}
+        for g in range(len(plan.groups)):
+            self.stamp_serial += 1
+            stamps[g] = self.stamp_serial
+        prod_done = None
+        for g, group in enumerate(plan.groups):
+            q_next_n = plan.queue_sizes.get(g + 1, 0) if self.use_hot else 0
+            bounds = runplan.chunk_bounds(q_next_n, len(group)) if q_next_n else []
+            cpu_tag = -1
+            if self.use_hot and g > 0 and plan.queue_sizes.get(g, 0) > 0:
+                cpu_tag = self._new_tag()
+                _lib.call("hg_tag_vertices", ptr(plan.queues[g]), None, plan.queue_sizes[g], ptr(hot.cpu_tag_of),
+                          cpu_tag, stream_ptr())
+            if prod_done is not None:  # staging for this super-batch must be complete (:555-559)
+                main.wait_event(prod_done)
+                prod_done = None
+            for j, b in enumerate(group):
+                gb = plan.first_global_batch + b
+                self.batch_to_group[gb] = g
+                warm = 1 if (self.layer_based and g == 0 and self.hot_list.size) else 0
+                self.feeder.feed(plan.batches[b], plan.batch_seeds[b], gb, b, cpu_tag=cpu_tag, table_sel=g % 2,
+                                 cur_stamp=stamps[g], warm=warm,
+                                 n_div=self.dist.global_batch(plan.batches[b]) if self.dist else None)
+                if bounds and bounds[j][1] > bounds[j][0]:
+                    lo, hi = bounds[j]
+                    c = hi - lo
+                    self.producer.snapshot(j)
+                    args = (plan.queues[g + 1][lo:hi], c, hot_seed_dev[g + 1], j, gb, stamps[g + 1], (g + 1) % 2)
+                    if self.prod_stream is not None:
+                        ev = torch.cuda.Event()
+                        ev.record(main)
+                        self.prod_stream.wait_event(ev)
+                        with torch.cuda.stream(self.prod_stream):
+                            self.producer.run_chunk(*args, stream=self.prod_stream)
+                    else:
+                        self.producer.run_chunk(*args)
+                    rep.stage_events.append((g + 1, gb, c))
+                e.run_step()
+                self.version += 1
+            if self.prod_stream is not None and bounds:
+                prod_done = torch.cuda.Event()
+                prod_done.record(self.prod_stream)
+        if prod_done is not None:
+            main.wait_event(prod_done)
+        torch.cuda.synchronize(dev)
+        rep.losses = e.loss_arr[:nb].double().cpu().tolist()
+        rep.max_weight_deltas = e.md_arr[:nb].double().cpu().tolist()
+        hits = hot.batch_hits[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)
+        miss = hot.batch_miss[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)
+        for g, group in enumerate(plan.groups):
+            rep.epsilon_trace.append(max(rep.max_weight_deltas[b] for b in group) * 2 * cfg.super_batch_n)
+            for b in group:
+                rep.batch_rows.append({"epoch": plan.epoch, "batch": plan.first_global_batch + b, "super_batch": g,
+                                       "loss": rep.losses[b], "reuse_hits": int(hits[b]), "fallbacks": int(miss[b]),
+                                       "max_weight_delta": rep.max_weight_deltas[b]})
+        rep.reuse_hits, rep.fallbacks = int(hits.sum()), int(miss.sum())
+        if hot is not None:
+            rep.warmup_computed = int(hot.batch_warm[:nb].sum().item())
+            stats = hot.stats.cpu().numpy().view(np.uint64)
+            if int(stats[1]):
+                raise StalenessViolation(f"{int(stats[1])} reuse events exceeded the 2n-1 gap bound")
+            packed = int(stats[0])
+            if packed:
+                rep.max_gap = packed >> 32
+                rep.max_gap_batch = 0xFFFFFFFF - (packed & 0xFFFFFFFF)
+                rep.max_gap_super_batch = self.batch_to_group.get(rep.max_gap_batch, -1)
+        tot = rep.reuse_hits + rep.fallbacks
+        if tot > 0 and rep.fallbacks / tot > cfg.max_fallback_frac:
+            raise FallbackBudgetExceeded(f"fallback fraction {rep.fallbacks / tot:.2f} exceeds configured "
+                                         f"{cfg.max_fallback_frac:.2f}")
+        rep.stage_seconds_measured = {"epoch": time.perf_counter() - t0}
+        return rep
+
+    def weights(self):
+        return self.engine.params.to_numpy()
+
+
+def evaluate(trainer_or_graph, weights=None, model=None) -> dict:
+    """orchestrator.py:669-680: full-graph, full-neighbour inference accuracy."""
+    if isinstance(trainer_or_graph, Trainer):
+        t = trainer_or_graph
+        dg, params, ds = t.dg, t.engine.params, t.ds
+    else:
+        raise TypeError("evaluate() takes a Trainer")
+    acc, _ = full_graph_forward(dg, params, ds.val_mask, ds.test_mask)
+    return acc
+
+
+def full_graph_forward(dg: DeviceGraph, params, val_mask, test_mask, return_logits=False):
+    dev = dg.device
+    s = stream_ptr()
+    V = dg.num_vertices
+    sage = params.model == "sage"
+    code = 0 if sage else 1
+    outdeg = None
+    if not sage:
+        outdeg = torch.zeros(V, dtype=torch.int32, device=dev)
+        _lib.call("hg_target_histogram", ptr(dg.targets), dg.num_edges, ptr(outdeg), s)
+    h, ld = dg.features, dg.feat_ld
+    nV = torch.tensor([V], dtype=torch.int32, device=dev)
+    for l in range(params.L):
+        d_in, d_out = params.dims[l], params.dims[l + 1]
+        agg = torch.zeros((V, ld), dtype=torch.float32, device=dev)
+        _lib.call("hg_full_aggregate", code, ptr(h), ld, ld, ptr(dg.offsets), ptr(dg.targets), V, ptr(outdeg),
+                  ptr(agg), ld, s)
+        ld_out = pad4(d_out)
+        out = torch.zeros((V, ld_out), dtype=torch.float32, device=dev)
+        act = 1 if l < params.L - 1 else 0
+        if sage:
+            _lib.call("hg_gemm_f32", ptr(h), ld, d_in, ptr(params.view(l, 0)), d_out, ptr(agg), ld, d_in,
+                      ptr(params.view(l, 1)), d_out, 0, ptr(out), ld_out, d_out, ptr(nV), V, act, s)
+        else:
+            _lib.call("hg_gemm_f32", ptr(agg), ld, d_in, ptr(params.view(l, 0)), d_out, None, 0, 0, None, 0, 0,
+                      ptr(out), ld_out, d_out, ptr(nV), V, act, s)
+        h, ld = out, ld_out
+        del agg
+    C = params.dims[-1]
+    res = {}
+    for name, m in (("val", val_mask), ("test", test_mask)):
+        m = np.asarray(m, bool)
+        if not m.any():
+            res[name] = 0.0
+            continue
+        md = torch.as_tensor(m.astype(np.uint8), device=dev)
+        corr = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.call("hg_argmax_correct", ptr(h), ld, C, V, ptr(dg.labels), ptr(md), ptr(corr), s)
+        res[name] = float(int(corr.item()) / int(m.sum()))
+    return res, (h[:, :C] if return_logits else None)
+
+
+def run_training(graph, data=None, config: TrainConfig | None = None, device=None, hot_list=None,
+                 dist=None, return_trainer=False):
+    """orchestrator.py:683-725.  ``graph`` may be a datagen.Dataset (with
+    ``data`` None) or a (Graph, VertexData) pair like the reference."""
+    config = config or TrainConfig()
+    ds = graph if data is None else _Merged(graph, data)
+    tr = Trainer(ds, config, device=device, hot_list=hot_list, dist=dist)
+    reports = []
+    first = 0
+    for epoch in range(config.epochs):
+        plan = tr.build_epoch_plan(epoch, first)
+        rep = tr.run_epoch(plan)
+        acc = evaluate(tr)
+        rep.val_accuracy, rep.test_accuracy = acc["val"], acc["test"]
+        reports.append(rep)
+        first += len(plan.batches)
+    return (reports, tr) if return_trainer else reports
+
+
+class _Merged:
+    """(Graph, VertexData) viewed as one dataset object."""
+
+    def __init__(self, graph, data):
+        self.offsets, self.targets = graph.offsets, graph.targets
+        self.features, self.labels = data.features, data.labels
+        self.train_mask, self.val_mask, self.test_mask = data.train_mask, data.val_mask, data.test_mask
+
+
+def epsilon_monitor(max_weight_deltas, n: int, batches_per_super_batch: int | None = None):
+    """orchestrator.py:728-739."""
+    size = batches_per_super_batch or n
+    out = []
+    for i in range(0, len(max_weight_deltas), size):
+        w = max_weight_deltas[i:i + size]
+        out.append(max(w) * 2 * n if w else 0.0)
+    return out
