@@ -1,0 +1,402 @@
+#!/usr/bin/env python3
+"""Throughput benchmark: train seeds/s of the GraphSAGE products-shaped config.
+
+Workload (BASELINE.json configs[1], "C2"): synthetic ogbn-products-shaped graph
+(2.4M vertices, ~64.6M CSR entries incl. self-loops, 100-dim fp32 features,
+47 classes), 3-layer mean-GraphSAGE, fanouts [15, 10, 5] (bottom first),
+hidden 64, batch 1024, SGD.  A step is one training batch: k-hop sampling ->
+fused gather/aggregate -> dense transforms -> softmax-CE -> backward -> SGD.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Our arm (default): ``value`` is measured with every step's inputs already in
+HBM (device-to-device staging + one CUDA-graph replay per step); ``e2e`` is the
+same metric through the public per-step API (Trainer.train_step) from HOST
+seed ids: pinned H2D of the step's inputs and a D2H read of the step's loss
+inside the timed region.  Multi-GPU (torchrun): weak scaling, 1024 seeds per
+rank per step, one NCCL gradient all-reduce per step inside the graph.
+
+``--impl reference`` times the reference's CPU implementation of the same
+path: the oracle port (oracle/, a restatement of the reference's numba/numpy
+code pinned to its golden vectors) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train seeds/sec (GraphSAGE products-shape)"
+UNIT = "seeds/s"
+WORKLOAD = dict(workload="c2-products-shape", graph="synthetic Chung-Lu zipf2.5 (datagen.make_dataset('c2'))",
+                vertices=2_400_000, feat_dim=100, classes=47, model="sage", layers=3, fanouts=[15, 10, 5],
+                hidden=64, batch_size=1024, optimizer="sgd", hot_ratio=0.0)
+CACHE = os.environ.get("HG_BENCH_CACHE", "/tmp/hg_bench_cache")
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# the CPU reference path (oracle port of the reference's per-batch pipeline)
+# ---------------------------------------------------------------------------
+def cpu_reference_steps(ds, batches, seeds_rng, budget_s, max_steps, warmup=1):
+    """Time the reference's per-batch path on the host (orchestrator.py:236-256 +
+    sampler.sample_khop): oracle sample_khop (C restatement of the numba draw
+    + numpy dedup/lexsort) -> float64 gather -> forward/backward (numpy/OpenBLAS)
+    -> SGD.  Returns (seeds_per_s, steps_timed, seconds)."""
+    from oracle import oracle as O
+    g = O.Graph(offsets=ds.offsets, targets=ds.targets.astype(np.int64))
+    feats64 = ds.features.astype(np.float64)
+    data = O.VertexData(features=feats64, labels=ds.labels, train_mask=ds.train_mask, val_mask=ds.val_mask,
+                        test_mask=ds.test_mask)
+    cfg = dict(O.DEFAULT_CFG, model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024,
+               lr=0.01, strategy="case1", hot_ratio=0.0)
+    dims = [ds.feat_dim, 64, 64, int(ds.labels.max()) + 1]
+    W = O.init_params("sage", dims, 0)
+    adam = O.Adam()
+    n_seeds = 0
+    t_total = 0.0
+    steps = 0
+    for i, seeds in enumerate(batches):
+        t0 = time.perf_counter()
+        st = O.sample_khop(g, seeds, cfg["fanouts"], seeds_rng[i])
+        O.train_batch(cfg, data, W, st, ds.labels[seeds], None, adam)
+        dt = time.perf_counter() - t0
+        if i < warmup:
+            continue
+        t_total += dt
+        n_seeds += seeds.shape[0]
+        steps += 1
+        if t_total >= budget_s or steps >= max_steps:
+            break
+    return n_seeds / t_total, steps, t_total
+
+
+def host_cores():
+    return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def epoch_batches(ds, n_needed, bs=1024, seed=0, rank=0, world=1):
+    """Full batches from successive epoch shuffles (runplan semantics); in weak
+    scaling each rank takes its own disjoint batches."""
+    from paper_2311_13225_b200 import runplan
+    train = ds.train_ids()
+    out, seeds = [], []
+    epoch = 0
+    while len(out) < n_needed:
+        order = runplan.shuffle_epoch(train, seed, epoch)
+        batches = runplan.split_batches(order, bs)
+        for b, x in enumerate(batches):
+            if x.shape[0] != bs:
+                continue
+            if (b % world) != rank:
+                continue
+            out.append(x)
+            seeds.append(runplan.batch_sample_seed(seed, epoch, b // world))
+            if len(out) >= n_needed:
+                break
+        epoch += 1
+    return out, seeds
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2311_13225_b200.datagen import make_dataset
+    ds = make_dataset("c2", cache_dir=CACHE)
+    batches, rs = epoch_batches(ds, args.warmup + args.steps)
+    budget = float(os.environ.get("HG_REF_BUDGET_S", "120"))
+    v, steps, secs = cpu_reference_steps(ds, batches, rs, budget, args.steps, warmup=args.warmup)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * secs / max(steps, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": dict(WORKLOAD, parallelism="host-cpu", l2_flush="inputs>L2 (2.4M x 100 feature table)"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port",
+                             "sample": f"{steps} batches of 1024 seeds (requested {args.steps}, capped at "
+                                       f"{budget:.0f}s of CPU work) after {args.warmup} warm-up; {cpu_model()}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="also report a per-phase time breakdown")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    from paper_2311_13225_b200 import _lib
+    from paper_2311_13225_b200.datagen import make_dataset
+    from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer
+
+    dist_ctx = None
+    if world > 1:
+        torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
+        from paper_2311_13225_b200.parallel import DistContext
+        dist_ctx = DistContext("nccl")
+        import torch.distributed as dist
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)  # NCCL warm-up outside capture
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ds = make_dataset("c2", cache_dir=CACHE)
+    cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
+                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0)
+    tr = Trainer(ds, cfg, dist=dist_ctx)
+    e = tr.engine
+    # segments split around the dominant kernel (bottom fused gather+aggregate)
+    segs = e.capture_segments(split_at=("fwd0_agg", "fwd0_gemm"))
+    names = [n for n, _ in segs]
+    assert names == ["start", "fwd0_agg", "fwd0_gemm"], names
+    K, W = args.steps, args.warmup
+    batches, rseeds = epoch_batches(ds, W + K, rank=rank, world=world)
+    # stage every step's inputs in HBM (value = device-resident inputs)
+    d_seeds = torch.as_tensor(np.stack(batches).astype(np.int32), device=dev)
+    bp = np.zeros((W + K, 8), dtype=np.int64)
+    for i in range(W + K):
+        bp[i, 0] = np.array([rseeds[i] & 0xFFFFFFFFFFFFFFFF], np.uint64).view(np.int64)[0]
+        bp[i, 1], bp[i, 2], bp[i, 3], bp[i, 4] = 1024, i, 0, -1
+    d_bp = torch.as_tensor(bp, device=dev)
+    n_div = 1024 * world
+    d_counts = torch.tensor([1024, n_div], dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+
+    def step(i, timed_idx=None):
+        e.seeds.copy_(d_seeds[i], non_blocking=True)
+        e.bp.copy_(d_bp[i], non_blocking=True)
+        e.counts_in.copy_(d_counts, non_blocking=True)
+        segs[0][1].replay()
+        if timed_idx is not None:
+            ev_a[timed_idx].record(stream)
+        segs[1][1].replay()
+        if timed_idx is not None:
+            ev_b[timed_idx].record(stream)
+        segs[2][1].replay()
+
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    if dist_ctx:
+        dist_ctx.barrier()
+    clocks = ClockSampler(_env_int("LOCAL_RANK", 0))
+    clocks.start()
+    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t_start.record(stream)
+    for k in range(K):
+        step(W + k, k)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist_ctx:
+        dist_ctx.barrier()
+    ms = t_start.elapsed_time(t_end)
+    if dist_ctx:
+        ms = dist_ctx.max_over_ranks(ms)
+    value = world * 1024 * K / (ms / 1000.0)
+    agg_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]))
+    # algorithmic bytes of the dominant kernel per launch:
+    # unique src rows read + edge ids + per-dst metadata + [self | mean] rows written
+    F = ds.feat_dim
+    sizes = []
+    for i in range(min(K, 16)):
+        e.seeds.copy_(d_seeds[W + i])
+        e.bp.copy_(d_bp[W + i])
+        e.counts_in.copy_(d_counts)
+        segs[0][1].replay()
+        torch.cuda.synchronize()
+        n_dst0 = int(e.samplers[1].n_src.item())
+        n_src0 = int(e.samplers[0].n_src.item())
+        E0 = int(e.samplers[0].counts[:n_dst0].sum().item())
+        sizes.append((n_dst0, n_src0, E0))
+    n_dst0, n_src0, E0 = (float(np.mean([s[j] for s in sizes])) for j in range(3))
+    alg_bytes = n_src0 * F * 4 + E0 * 8 + n_dst0 * 12 + 2 * n_dst0 * F * 4
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg_bytes / (agg_ms / 1000.0) / 1e9
+    # kernels per step (graph kernel nodes) -> launches in the timed region
+    lib = _lib.load()
+    per_step = 0
+    for _, g in segs:
+        try:
+            per_step += int(lib.hg_graph_kernel_count(g.raw_cuda_graph()))
+        except Exception:
+            per_step = -1
+            break
+    # ---- e2e through the public API from host seed ids ----
+    e2e_K = K
+    handles = []
+    torch.cuda.synchronize()
+    e2e_start = torch.cuda.Event(enable_timing=True)
+    e2e_end = torch.cuda.Event(enable_timing=True)
+    host_batches = [np.asarray(b, np.int64) for b in batches]
+    for i in range(3):
+        tr.train_step(host_batches[i], rseeds[i])()
+    torch.cuda.synchronize()
+    if dist_ctx:
+        dist_ctx.barrier()
+    wall0 = time.perf_counter()
+    e2e_start.record(stream)
+    for k in range(e2e_K):
+        handles.append(tr.train_step(host_batches[W + k], rseeds[W + k], batch_in_epoch=0))
+    losses = [h() for h in handles]
+    e2e_end.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    e2e_ms = max(e2e_start.elapsed_time(e2e_end), wall * 1000.0)
+    if dist_ctx:
+        e2e_ms = dist_ctx.max_over_ranks(e2e_ms)
+    e2e_value = world * 1024 * e2e_K / (e2e_ms / 1000.0)
+    if not np.all(np.isfinite(losses)):
+        raise SystemExit("non-finite loss in bench")
+    phases = None
+    if args.phases and rank == 0:
+        phases = phase_breakdown(e, d_seeds, d_bp, d_counts, W)
+    if rank != 0:
+        return
+    cpu_base = None
+    if not args.no_cpu_baseline and world == 1:
+        budget = float(os.environ.get("HG_CPU_BASELINE_S", "20"))
+        cb, steps, secs = cpu_reference_steps(ds, batches, rseeds, budget, 200, warmup=1)
+        cpu_base = {"value": cb, "unit": UNIT, "cores": host_cores(), "kind": "port",
+                    "sample": f"{steps} C2 batches of 1024 seeds ({secs:.1f}s CPU) after 1 warm-up; oracle port of "
+                              f"the reference path (C draw loop single-threaded, numpy/OpenBLAS on all cores); "
+                              f"{cpu_model()}"}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp32", "data": "synthetic",
+            "config": dict(WORKLOAD, parallelism=f"dp{world}" if world > 1 else "single",
+                           l2_flush="inputs > L2: 0.96 GB feature table + 0.26 GB CSR, random rows per step",
+                           global_batch=1024 * world),
+            "roofline": {"bound": "hbm", "kernel": "k_agg_fwd (bottom fused gather+mean, SAGE)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": agg_ms,
+                         "block0": {"n_dst": n_dst0, "n_src": n_src0, "edges": E0},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+            "cpu_baseline": cpu_base,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": tr.feeder.h2d_bytes,
+                    "d2h_bytes_per_step": tr.d2h_bytes_per_step},
+            "gpu_launches": per_step * K if per_step >= 0 else None,
+            "kernels_per_step": per_step,
+            "clocks": clk,
+            "final_loss": losses[-1]}
+    if phases:
+        line["phases_ms"] = phases
+    print(json.dumps(line), flush=True)
+
+
+def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):
+    """Per-phase device time (ms) of one step, from a capture split at every mark."""
+    import torch
+    segs = e.capture_segments(split_at=tuple(m for m in e.MARKS))
+    tot = {n: 0.0 for n, _ in segs}
+    for r in range(reps):
+        e.seeds.copy_(d_seeds[i0 + r % d_seeds.shape[0]])
+        e.bp.copy_(d_bp[i0 + r % d_bp.shape[0]])
+        e.counts_in.copy_(d_counts)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(segs) + 1)]
+        evs[0].record()
+        for k, (_, g) in enumerate(segs):
+            g.replay()
+            evs[k + 1].record()
+        torch.cuda.synchronize()
+        for k, (n, _) in enumerate(segs):
+            tot[n] += evs[k].elapsed_time(evs[k + 1])
+    return {n: v / reps for n, v in tot.items()}
+
+
+if __name__ == "__main__":
+    main()

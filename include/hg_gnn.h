@@ -36,6 +36,8 @@ extern "C" {
 
 int hg_abi_version(void);
 int hg_last_error(char* buf, int len);
+/* kernel nodes in a captured cudaGraph_t (passed as void*); -1 on error */
+int64_t hg_graph_kernel_count(void* graph);
 
 /* ---- splitmix64 streams: kernels.py:51-70 (_mix64, derive_seed) -------- */
 uint64_t hg_mix64_host(uint64_t x);
@@ -120,12 +122,32 @@ int64_t hg_wgrad_ws_size(int32_t K, int32_t N, int32_t M_cap);
 int hg_wgrad_f32(const float* A, int32_t lda, int32_t K, const float* G, int32_t ldg, int32_t N,
                  const int32_t* d_M, int32_t M_cap, float* out, float scale, float* ws, void* stream);
 
+/* tcgen05 (5th-gen tensor core, kind::tf32, 3xTF32 split => fp32-class accuracy).
+ *  C = act(A1 op(B)[0:K1] + A2 op(B)[K1:K1+K2]); op(B)(k,n) = B[k*ldb+n] if trans_b
+ *  (forward: B = [W_self; W_neigh] stacked [K x N]) else B[n*ldb+k] (dX = dZ W^T).
+ *  B is consumed as a prebuilt swizzled hi/lo image (hg_gemm_tc_prep_b, once per
+ *  weight update; hg_gemm_tc_bimg_size bytes, 16-byte aligned). */
+int64_t hg_gemm_tc_bimg_size(int32_t K1, int32_t K2, int32_t N);
+int hg_gemm_tc_prep_b(const float* B, int32_t ldb, int32_t trans_b, int32_t K1, int32_t K2, int32_t N, void* img,
+                      void* stream);
+int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32_t lda2, int32_t K2,
+               const void* bimg, float* C, int32_t ldc, int32_t N, const int32_t* d_M, int32_t M_cap, int32_t act,
+               void* stream);
+/* process-wide tuning knobs for the tensor-core kernels (key 1: MN-major descriptor offsets) */
+int hg_set_tuning(int32_t key, int32_t value);
+/* out_s[K x N] = A_s^T G (s = 1, 2; A2 may be NULL), deterministic split-M. */
+int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int32_t n_src);
+int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32_t lda2, int32_t K, const float* G,
+                int32_t ldg, int32_t N, const int32_t* d_M, int32_t M_cap, float* out1, float* out2, float* ws,
+                void* stream);
+
 /* ---- K9/K10 loss and updates (gnnmath.py:263-312; orchestrator.py:246-255) */
 /* dlogits = (softmax - onehot) / *d_div (d_div NULL: / n); *d_loss = mean CE over
- * the n = min(*d_n, cap) rows; labels indexed by seeds[r] (seeds NULL: by r). */
+ * the n = min(*d_n, cap) rows; labels indexed by seeds[r] (seeds NULL: by r).
+ * row_ws: cap floats (per-row losses, reduced in a fixed order). */
 int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const int32_t* d_n, int32_t cap,
                     const int32_t* labels, const int32_t* seeds, const int32_t* d_div, float* dlogits,
-                    int32_t ldd, float* d_loss, void* stream);
+                    int32_t ldd, float* d_loss, float* row_ws, void* stream);
 /* per-batch row record: loss_arr[bp[3]] = *d_loss, md_arr[bp[3]] = max|dw|; resets *d_maxdelta */
 int hg_record_batch(const int64_t* bp, const float* d_loss, uint32_t* d_maxdelta, float* loss_arr,
                     float* md_arr, void* stream);

@@ -1,0 +1,572 @@
+// K8: the dense layer transforms on the 5th-generation tensor cores (tcgen05).
+//
+//   hg_gemm_tc   C[M x N] = act(A1 op(B)[:K1] + A2 op(B)[K1:])   (fwd; dX = dZ W^T)
+//   hg_wgrad_tc  dW_s[K x N] = A_s^T G  (s = 1, 2; split-M, fixed-order reduction)
+//
+// fp32 accuracy from tf32 tensor cores ("3xTF32"): every operand x is fed as
+// x (the MMA reads its top 19 bits, i.e. hi = trunc_tf32(x)) and lo = x - hi
+// (exact in fp32), and D += A_hi B_hi + A_hi B_lo + A_lo B_hi, so the product
+// error is ~2^-21 relative instead of tf32's 2^-10.  The GEMMs here are small
+// and HBM-bound (K <= 2F, N <= 256), so the 3x MMA count is free.
+//
+// Structure (one CTA = 128 output rows x BN columns, 4 warps):
+//   cp.async (16 B, zero-filled beyond M/K) stages 128-byte-swizzled operand
+//   tiles (the canonical SWIZZLE_128B layouts of the UMMA smem descriptors),
+//   threads split lo = x - trunc(x) in place, fence.proxy.async + barrier,
+//   one elected thread issues tcgen05.mma (M=128, kind::tf32, accumulator in
+//   TMEM) and tcgen05.commit's to the stage's mbarrier, which gates the reuse
+//   of that smem stage (2-stage ring: loads of tile k+1 overlap MMAs of tile k).
+//   The epilogue reads the accumulator with tcgen05.ld (32x32b: warp w owns
+//   TMEM lanes 32w..32w+31 = output rows) and applies the ReLU.
+// The wgrad kernel feeds both operands MN-major (A^T and G are read as stored,
+// row-major over the reduction dimension), which tf32 UMMA supports.
+#include "hg_common.cuh"
+#include "hg_gnn_internal.h"
+
+namespace {
+
+int g_mn_swap = 0;  // tuning knob (hg_set_tuning key 1): MN-major descriptor offset assignment
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// shared-memory matrix descriptor (start, leading/stride byte offsets, layout
+// type: 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B — the only MN-major layout
+// tf32 operands support)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
+// instruction descriptor: kind::tf32, fp32 accumulate, M=128, N, operand majors
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of (row r, 16-byte chunk c) in a K-major SWIZZLE_128B tile
+// (8-row x 128-byte atoms stacked along rows, atom stride 1024 B)
+__device__ __forceinline__ uint32_t off_k(int r, int c) {
+    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+// byte offset of (reduction row kr, 16-byte MN chunk cg) in an MN-major
+// SWIZZLE_128B_BASE32B tile holding 32 reduction rows: atoms are 4 rows x 128 B
+// (32 MN elements), 32-byte granules XOR-swizzled with the row (Swizzle<2,5,2>);
+// atom (MN group g = cg/8, K group kr/4) at (g*8 + kr/4)*512, so MN groups are
+// 4096 B apart and K groups 512 B apart.
+__device__ __forceinline__ uint32_t off_mn(int kr, int cg) {
+    const int row = kr & 3, c = cg & 7;
+    return (uint32_t)(((cg >> 3) * 8 + (kr >> 2)) * 512 + row * 128 + ((((c >> 1) ^ row)) << 5) + ((c & 1) << 4));
+}
+
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+__device__ __forceinline__ void split_lo16(const uint8_t* hi, uint8_t* lo) {
+    float4 v = *reinterpret_cast<const float4*>(hi);
+    v.x = tf32_lo(v.x); v.y = tf32_lo(v.y); v.z = tf32_lo(v.z); v.w = tf32_lo(v.w);
+    *reinterpret_cast<float4*>(lo) = v;
+}
+
+constexpr int TC_THREADS = 128;
+constexpr int A_TILE = 128 * 128;  // 128 rows x 32 fp32
+
+template <int BN>
+__host__ __device__ constexpr int gemm_stage_bytes() { return 2 * A_TILE + 2 * BN * 128; }
+
+// ---------------------------------------------------------------------------
+// B image: for every (N tile, K tile) the exact swizzled smem bytes of the
+// operand tile, hi then lo (2 * BN * 128 bytes), so CTAs stage B with plain
+// 16-byte cp.async copies.  Built once per weight update by k_prep_b.
+template <int BN>
+__global__ void k_prep_b(const float* __restrict__ B, int ldb, int trans_b, int K1, int K2, int N, int nk1, int nk,
+                         uint8_t* __restrict__ img) {
+    const int nt = blockIdx.y, kt = blockIdx.x;
+    uint8_t* base = img + ((int64_t)nt * nk + kt) * (2 * BN * 128);
+    const int K = kt < nk1 ? K1 : K2;
+    const int k0 = kt < nk1 ? kt * 32 : (kt - nk1) * 32;
+    const int kb = kt < nk1 ? k0 : K1 + k0;
+    for (int e = threadIdx.x; e < BN * 32; e += blockDim.x) {
+        int n, k;
+        if (trans_b) { k = e / BN; n = e - k * BN; }
+        else { n = e >> 5; k = e & 31; }
+        const int gn = nt * BN + n, gk = k0 + k;
+        float v = 0.f;
+        if (gn < N && gk < K) v = trans_b ? B[(int64_t)(kb + k) * ldb + gn] : B[(int64_t)gn * ldb + kb + k];
+        const uint32_t off = off_k(n, k >> 2) + (k & 3) * 4;
+        *reinterpret_cast<float*>(base + off) = v;
+        *reinterpret_cast<float*>(base + BN * 128 + off) = tf32_lo(v);
+    }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_gemm_tc(const float* __restrict__ A1, int lda1, int K1, const float* __restrict__ A2, int lda2, int K2,
+          const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N,
+          const int* __restrict__ d_M, int M_cap, int act) {
+    constexpr int STAGE = gemm_stage_bytes<BN>();
+    constexpr int B_TILE = BN * 128;
+    constexpr uint32_t NCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[2];
+    __shared__ uint32_t s_tmem;
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int M = hg_load_count(d_M, M_cap);
+    const int m0 = blockIdx.x * 128;
+    if (m0 >= M) return;
+    const int n0 = blockIdx.y * BN;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nk1 = (K1 + 31) >> 5;
+    const int nk2 = A2 ? (K2 + 31) >> 5 : 0;
+    const int nk = nk1 + nk2;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(&s_tmem, NCOLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    const uint8_t* bimg = Bimg + (int64_t)blockIdx.y * nk * (2 * B_TILE);
+    auto load_tile = [&](int kt, int st) {
+        uint8_t* base = smem + st * STAGE;
+        const float* A;
+        int lda, K, k0;
+        if (kt < nk1) { A = A1; lda = lda1; K = K1; k0 = kt * 32; }
+        else { A = A2; lda = lda2; K = K2; k0 = (kt - nk1) * 32; }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // A: 128 rows x 8 chunks of 16 B
+            const int q = tid + TC_THREADS * i;
+            const int r = q >> 3, c = q & 7;
+            const int gm = m0 + r, gk = k0 + c * 4;
+            int bytes = gm < M ? (K - gk) * 4 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            const float* src = bytes > 0 ? A + (int64_t)gm * lda + gk : A;
+            cp_async16(smem_u32(base + off_k(r, c)), src, bytes);
+        }
+        // B: the prebuilt swizzled hi|lo image of this K tile (contiguous bytes)
+        const uint8_t* bsrc = bimg + (int64_t)kt * (2 * B_TILE);
+        const uint32_t bdst = smem_u32(base + 2 * A_TILE);
+        for (int q = tid; q < (2 * B_TILE) / 16; q += TC_THREADS) cp_async16(bdst + q * 16, bsrc + q * 16, 16);
+        cp_async_commit();
+    };
+
+    uint32_t uses0 = 0, uses1 = 0;
+    load_tile(0, 0);
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt & 1;
+        if (kt + 1 < nk) {
+            const int st2 = (kt + 1) & 1;
+            if (kt + 1 >= 2) mbar_wait(&bars[st2], ((st2 ? uses1 : uses0) - 1) & 1);  // MMAs of tile kt-1 done
+            load_tile(kt + 1, st2);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        uint8_t* base = smem + st * STAGE;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = tid + TC_THREADS * i;
+            const uint32_t off = off_k(q >> 3, q & 7);
+            split_lo16(base + off, base + A_TILE + off);
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(base), a_lo = a_hi + A_TILE;
+            const uint32_t b_hi = a_hi + 2 * A_TILE, b_lo = b_hi + B_TILE;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint64_t dah = sdesc(a_hi + s * 32, 16, 1024), dal = sdesc(a_lo + s * 32, 16, 1024);
+                const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
+                mma_tf32(tmem, dah, dbh, IDESC, (kt | s) ? 1u : 0u);
+                mma_tf32(tmem, dah, dbl, IDESC, 1u);
+                mma_tf32(tmem, dal, dbh, IDESC, 1u);
+            }
+            mma_commit(&bars[st]);
+        }
+        if (st) ++uses1; else ++uses0;
+        __syncwarp();
+    }
+    {
+        const int st = (nk - 1) & 1;
+        mbar_wait(&bars[st], ((st ? uses1 : uses0) - 1) & 1);
+    }
+    tc_fence_after();
+    const int r = warp * 32 + lane;
+    const int gm = m0 + r;
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        if (gm < M) {
+            float* crow = C + (int64_t)gm * ldc + n0 + c0;
+            const int lim = N - (n0 + c0);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < lim) crow[j] = act ? fmaxf(v[j], 0.f) : v[j];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, NCOLS);
+}
+
+// ---------------------------------------------------------------------------
+// wgrad: partial[src][chunk][K x N] = A_src[rows of chunk]^T G[rows of chunk]
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2, int lda2, int K,
+           const float* __restrict__ G, int ldg, int N, const int* __restrict__ d_M, int M_cap, int rows_per_chunk,
+           int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
+    constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
+    constexpr int STAGE = 2 * A_TILE + 2 * G_TILE;
+    constexpr uint32_t NCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    constexpr uint32_t IDESC = idesc_tf32(128, BN, 1, 1);
+    constexpr int GCH = BN / 4;  // 16-byte chunks per G row
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t bars[2];
+    __shared__ uint32_t s_tmem;
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int M = hg_load_count(d_M, M_cap);
+    const int k0 = blockIdx.x * 128;
+    const int src = blockIdx.y;
+    const int chunk = blockIdx.z;
+    const int mbeg = chunk * rows_per_chunk;
+    float* P = partial + ((int64_t)src * n_chunks + chunk) * (int64_t)K * N;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (mbeg >= M) return;  // reduction skips chunks past M
+    const int mend = min(M, mbeg + rows_per_chunk);
+    const float* A = src ? A2 : A1;
+    const int lda = src ? lda2 : lda1;
+    const int nk = (mend - mbeg + 31) >> 5;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(&s_tmem, NCOLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    auto load_tile = [&](int kt, int st) {
+        uint8_t* base = smem + st * STAGE;
+        const int r0 = mbeg + kt * 32;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // A: 32 rows x 32 chunks (128 k)
+            const int q = tid + TC_THREADS * i;
+            const int r = q >> 5, cg = q & 31;
+            const int gm = r0 + r, gk = k0 + cg * 4;
+            int bytes = gm < mend ? (K - gk) * 4 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            const float* s = bytes > 0 ? A + (int64_t)gm * lda + gk : A;
+            cp_async16(smem_u32(base + off_mn(r, cg)), s, bytes);
+        }
+        uint8_t* gb = base + 2 * A_TILE;
+        for (int q = tid; q < 32 * GCH; q += TC_THREADS) {  // G: 32 rows x BN/4 chunks
+            const int r = q / GCH, cg = q - r * GCH;
+            const int gm = r0 + r, gn = cg * 4;
+            int bytes = gm < mend ? (N - gn) * 4 : 0;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            const float* s = bytes > 0 ? G + (int64_t)gm * ldg + gn : G;
+            cp_async16(smem_u32(gb + off_mn(r, cg)), s, bytes);
+        }
+        cp_async_commit();
+    };
+
+    uint32_t uses0 = 0, uses1 = 0;
+    load_tile(0, 0);
+    for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt & 1;
+        if (kt + 1 < nk) {
+            const int st2 = (kt + 1) & 1;
+            if (kt + 1 >= 2) mbar_wait(&bars[st2], ((st2 ? uses1 : uses0) - 1) & 1);
+            load_tile(kt + 1, st2);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        uint8_t* base = smem + st * STAGE;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = tid + TC_THREADS * i;
+            const uint32_t off = off_mn(q >> 5, q & 31);
+            split_lo16(base + off, base + A_TILE + off);
+        }
+        uint8_t* gb = base + 2 * A_TILE;
+        for (int q = tid; q < 32 * GCH; q += TC_THREADS) {
+            const uint32_t off = off_mn(q / GCH, q % GCH);
+            split_lo16(gb + off, gb + G_TILE + off);
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t a_hi = smem_u32(base), a_lo = a_hi + A_TILE;
+            const uint32_t g_hi = a_hi + 2 * A_TILE, g_lo = g_hi + G_TILE;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {  // 8 reduction rows (two 4-row K atoms) per MMA
+                const uint64_t dah = sdesc(a_hi + s * 1024, lbo, sbo, 1), dal = sdesc(a_lo + s * 1024, lbo, sbo, 1);
+                const uint64_t dgh = sdesc(g_hi + s * 1024, lbo, sbo, 1), dgl = sdesc(g_lo + s * 1024, lbo, sbo, 1);
+                mma_tf32(tmem, dah, dgh, IDESC, (kt | s) ? 1u : 0u);
+                mma_tf32(tmem, dah, dgl, IDESC, 1u);
+                mma_tf32(tmem, dal, dgh, IDESC, 1u);
+            }
+            mma_commit(&bars[st]);
+        }
+        if (st) ++uses1; else ++uses0;
+        __syncwarp();
+    }
+    {
+        const int st = (nk - 1) & 1;
+        mbar_wait(&bars[st], ((st ? uses1 : uses0) - 1) & 1);
+    }
+    tc_fence_after();
+    const int r = warp * 32 + lane;
+    const int gk = k0 + r;
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        if (gk < K) {
+            float* prow = P + (int64_t)gk * N + c0;
+            const int lim = N - c0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < lim) prow[j] = v[j];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, NCOLS);
+}
+
+__global__ void k_wgrad_tc_reduce(const float* __restrict__ partial, int KN, int n_src, int n_chunks,
+                                  int rows_per_chunk, const int* __restrict__ d_M, int M_cap, float* __restrict__ out1,
+                                  float* __restrict__ out2) {
+    const int M = hg_load_count(d_M, M_cap);
+    const int chunks = min(n_chunks, (M + rows_per_chunk - 1) / rows_per_chunk);
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < KN * n_src; idx += gridDim.x * blockDim.x) {
+        const int s = idx / KN, e = idx - s * KN;
+        const float* p = partial + (int64_t)s * n_chunks * KN + e;
+        float acc = 0.f;
+        for (int c = 0; c < chunks; ++c) acc += p[(int64_t)c * KN];
+        (s ? out2 : out1)[e] = acc;
+    }
+}
+
+template <int BN>
+int launch_gemm(dim3 grid, cudaStream_t s, const float* A1, int lda1, int K1, const float* A2, int lda2, int K2,
+                const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int M_cap, int act) {
+    const int smem = 2 * gemm_stage_bytes<BN>() + 1024;
+    static bool attr = false;  // idempotent; set before first launch (outside graph capture via warm-up)
+    if (!attr) {
+        cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_gemm_tc<BN><<<grid, TC_THREADS, smem, s>>>(A1, lda1, K1, A2, lda2, K2, bimg, C, ldc, N, d_M, M_cap, act);
+    return hg_check_launch("gemm_tc");
+}
+
+int gemm_bn(int N) {
+    const int Nr = (N + 15) & ~15;
+    return Nr <= 32 ? 32 : Nr <= 64 ? 64 : Nr <= 128 ? 128 : 256;
+}
+
+template <int BN>
+int launch_wgrad(dim3 grid, cudaStream_t s, const float* A1, int lda1, const float* A2, int lda2, int K,
+                 const float* G, int ldg, int N, const int* d_M, int M_cap, int rpc, int n_chunks, float* partial) {
+    const int smem = 2 * (2 * A_TILE + 2 * BN * 128) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_wgrad_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    // MN-major SWIZZLE_128B_BASE32B: LBO steps between 32-element MN atoms
+    // (4 KB apart here), SBO between 4-row K atoms (512 B apart)
+    const uint32_t lbo = g_mn_swap ? 512u : 4096u, sbo = g_mn_swap ? 4096u : 512u;
+    k_wgrad_tc<BN><<<grid, TC_THREADS, smem, s>>>(A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, rpc, n_chunks, partial,
+                                                  lbo, sbo);
+    return hg_check_launch("wgrad_tc");
+}
+
+int wgrad_rows_per_chunk(int M_cap, int ktiles, int n_src) {
+    // aim for ~2 CTAs per SM over (k-tiles x sources x chunks), 32-row multiples, >= 128 rows
+    long long want_chunks = (2LL * HG_NUM_SMS) / (ktiles * n_src);
+    if (want_chunks < 1) want_chunks = 1;
+    long long rpc = (M_cap + want_chunks - 1) / want_chunks;
+    rpc = ((rpc + 31) / 32) * 32;
+    if (rpc < 128) rpc = 128;
+    return (int)rpc;
+}
+
+}  // namespace
+
+// Byte size of the B operand image for (K1, K2, N).
+extern "C" int64_t hg_gemm_tc_bimg_size(int32_t K1, int32_t K2, int32_t N) {
+    const int bn = gemm_bn(N);
+    const int nk = hg_ceil_div(K1, 32) + (K2 > 0 ? hg_ceil_div(K2, 32) : 0);
+    return (int64_t)hg_ceil_div(N, bn) * nk * 2 * bn * 128;
+}
+
+// Build the B image: op(B)(k, n) = B[k*ldb + n] with trans_b (B stored
+// [K x N], the forward weights [W_self; W_neigh]) or B[n*ldb + k] without (B
+// stored [N x K], dX = dZ W^T); rows K1.. of op(B) feed the second A source.
+extern "C" int hg_gemm_tc_prep_b(const float* B, int32_t ldb, int32_t trans_b, int32_t K1, int32_t K2, int32_t N,
+                                 void* img, void* stream) {
+    if (N <= 0 || K1 <= 0) return HG_OK;
+    const int bn = gemm_bn(N);
+    const int nk1 = hg_ceil_div(K1, 32);
+    const int nk = nk1 + (K2 > 0 ? hg_ceil_div(K2, 32) : 0);
+    dim3 g(nk, hg_ceil_div(N, bn));
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* p = (uint8_t*)img;
+    switch (bn) {
+        case 32: k_prep_b<32><<<g, 256, 0, s>>>(B, ldb, trans_b, K1, K2, N, nk1, nk, p); break;
+        case 64: k_prep_b<64><<<g, 256, 0, s>>>(B, ldb, trans_b, K1, K2, N, nk1, nk, p); break;
+        case 128: k_prep_b<128><<<g, 256, 0, s>>>(B, ldb, trans_b, K1, K2, N, nk1, nk, p); break;
+        default: k_prep_b<256><<<g, 256, 0, s>>>(B, ldb, trans_b, K1, K2, N, nk1, nk, p); break;
+    }
+    return hg_check_launch("gemm_tc_prep_b");
+}
+
+// C[M x N] = act(A1[M x K1] op(B)[0:K1] + A2[M x K2] op(B)[K1:K1+K2]) with the
+// B image from hg_gemm_tc_prep_b.  Requirements: lda % 4 == 0, 16-byte aligned A.
+extern "C" int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32_t lda2, int32_t K2,
+                          const void* bimg, float* C, int32_t ldc, int32_t N, const int32_t* d_M, int32_t M_cap,
+                          int32_t act, void* stream) {
+    if (M_cap <= 0 || N <= 0) return HG_OK;
+    if ((lda1 & 3) || (A2 && (lda2 & 3)) || (reinterpret_cast<uintptr_t>(A1) & 15) ||
+        (A2 && (reinterpret_cast<uintptr_t>(A2) & 15)) || (reinterpret_cast<uintptr_t>(bimg) & 15)) {
+        hg_set_error("gemm_tc: A rows and the B image must be 16-byte aligned (lda %% 4 == 0)");
+        return HG_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int bn = gemm_bn(N);
+    const uint8_t* b = (const uint8_t*)bimg;
+    dim3 g(hg_ceil_div(M_cap, 128), hg_ceil_div(N, bn));
+    switch (bn) {
+        case 32: return launch_gemm<32>(g, s, A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act);
+        case 64: return launch_gemm<64>(g, s, A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act);
+        case 128: return launch_gemm<128>(g, s, A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act);
+        default: return launch_gemm<256>(g, s, A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act);
+    }
+}
+
+// process-wide tuning knobs (key 1: MN-major descriptor LBO/SBO assignment)
+extern "C" int hg_set_tuning(int32_t key, int32_t value) {
+    if (key == 1) { g_mn_swap = value ? 1 : 0; return HG_OK; }
+    hg_set_error("set_tuning: unknown key %d", key);
+    return HG_EINVAL;
+}
+
+extern "C" int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int32_t n_src) {
+    const int kt = hg_ceil_div(K > 0 ? K : 1, 128);
+    const int rpc = wgrad_rows_per_chunk(M_cap > 0 ? M_cap : 1, kt, n_src);
+    const int chunks = hg_ceil_div(M_cap > 0 ? M_cap : 1, rpc);
+    return (int64_t)n_src * chunks * K * N;
+}
+
+// out_s[K x N] = A_s[M x K]^T G[M x N] for s = 1 (A1) and, if A2, s = 2.
+// ws >= hg_wgrad_tc_ws_size(K, N, M_cap, n_src) floats.  N <= 256.
+extern "C" int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32_t lda2, int32_t K, const float* G,
+                           int32_t ldg, int32_t N, const int32_t* d_M, int32_t M_cap, float* out1, float* out2,
+                           float* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (K <= 0 || N <= 0) return HG_OK;
+    if (N > 256) { hg_set_error("wgrad_tc: N > 256"); return HG_EUNSUPPORTED; }
+    if ((lda1 & 3) || (A2 && (lda2 & 3)) || (ldg & 3)) {
+        hg_set_error("wgrad_tc: row strides must be multiples of 4");
+        return HG_EINVAL;
+    }
+    const int n_src = A2 ? 2 : 1;
+    const int kt = hg_ceil_div(K, 128);
+    const int Mc = M_cap > 0 ? M_cap : 1;
+    const int rpc = wgrad_rows_per_chunk(Mc, kt, n_src);
+    const int chunks = hg_ceil_div(Mc, rpc);
+    const int Nr = (N + 15) & ~15;
+    dim3 grid(kt, n_src, chunks);
+    int rc = HG_OK;
+    if (M_cap > 0) {
+        if (Nr <= 32) rc = launch_wgrad<32>(grid, s, A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, rpc, chunks, ws);
+        else if (Nr <= 64) rc = launch_wgrad<64>(grid, s, A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, rpc, chunks, ws);
+        else if (Nr <= 128) rc = launch_wgrad<128>(grid, s, A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, rpc, chunks, ws);
+        else rc = launch_wgrad<256>(grid, s, A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, rpc, chunks, ws);
+        if (rc) return rc;
+    }
+    k_wgrad_tc_reduce<<<hg_grid((long long)K * N * n_src, 256, 4), 256, 0, s>>>(ws, K * N, n_src, chunks, rpc, d_M,
+                                                                                M_cap, out1, out2);
+    return hg_check_launch("wgrad_tc_reduce");
+}

@@ -24,16 +24,17 @@ namespace {
 // --------------------------------------------------------------------------
 // n rows (device count, <= cap); dlogits = (p - onehot) / div where div =
 // *d_div (the global batch size; == n on one GPU, gnnmath.py:273)
-__global__ void __launch_bounds__(1024) k_xent(const float* __restrict__ logits, int ld, int C, const int* d_n,
-                                               int cap, const int* __restrict__ labels, const int* __restrict__ seeds,
-                                               const int* __restrict__ d_div, float* __restrict__ dlogits, int ldd,
-                                               float* __restrict__ d_loss) {
-    __shared__ double s_part[32];
+// one warp per row; per-row losses land in row_loss, reduced in fixed order by
+// k_xent_reduce (deterministic, no float atomics)
+__global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int ld, int C, const int* d_n,
+                                              int cap, const int* __restrict__ labels, const int* __restrict__ seeds,
+                                              const int* __restrict__ d_div, float* __restrict__ dlogits, int ldd,
+                                              float* __restrict__ row_loss) {
     const int n = hg_load_count(d_n, cap);
-    const float grad_scale = 1.0f / (float)(d_div ? *d_div : n);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double part = 0.0;
-    for (int r = w; r < n; r += nw) {
+    const float grad_scale = 1.0f / (float)(d_div ? *d_div : (n > 0 ? n : 1));
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
         const float* z = logits + (int64_t)r * ld;
         float mx = -INFINITY;
         for (int c = lane; c < C; c += 32) mx = fmaxf(mx, z[c]);
@@ -49,13 +50,23 @@ __global__ void __launch_bounds__(1024) k_xent(const float* __restrict__ logits,
             const float p = expf(z[c] - mx) * inv;
             dlogits[(int64_t)r * ldd + c] = (p - (c == y ? 1.f : 0.f)) * grad_scale;
         }
-        if (lane == 0) part += (double)(logf(se) - (z[y] - mx));  // -log softmax_y
+        if (lane == 0) row_loss[r] = logf(se) - (z[y] - mx);  // -log softmax_y
     }
-    if (lane == 0) s_part[w] = part;
+}
+
+__global__ void __launch_bounds__(1024) k_xent_reduce(const float* __restrict__ row_loss, const int* d_n, int cap,
+                                                      float* __restrict__ d_loss) {
+    __shared__ double s_part[32];
+    const int n = hg_load_count(d_n, cap);
+    double part = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) part += (double)row_loss[r];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
         double tot = 0.0;
-        for (int k = 0; k < nw; ++k) tot += s_part[k];
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += s_part[k];
         *d_loss = n > 0 ? (float)(tot / (double)n) : 0.f;
     }
 }
@@ -310,9 +321,11 @@ __global__ void k_argmax_correct(const float* __restrict__ logits, int ld, int C
 
 extern "C" int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const int32_t* d_n, int32_t cap,
                                const int32_t* labels, const int32_t* seeds, const int32_t* d_div, float* dlogits,
-                               int32_t ldd, float* d_loss, void* stream) {
+                               int32_t ldd, float* d_loss, float* row_ws, void* stream) {
     if (cap <= 0) { hg_set_error("softmax_xent: empty batch"); return HG_EINVAL; }
-    k_xent<<<1, 1024, 0, (cudaStream_t)stream>>>(logits, ld, C, d_n, cap, labels, seeds, d_div, dlogits, ldd, d_loss);
+    cudaStream_t s = (cudaStream_t)stream;
+    k_xent<<<hg_ceil_div(cap, 8), 256, 0, s>>>(logits, ld, C, d_n, cap, labels, seeds, d_div, dlogits, ldd, row_ws);
+    k_xent_reduce<<<1, 1024, 0, s>>>(row_ws, d_n, cap, d_loss);
     return hg_check_launch("softmax_xent");
 }
 

@@ -5,6 +5,7 @@
 // captured in one CUDA graph without host round trips.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "hg_common.cuh"
@@ -43,6 +44,26 @@ extern "C" uint64_t hg_derive_seed(uint64_t seed, const uint64_t* parts, int n_p
 }
 
 extern "C" int hg_abi_version(void) { return HG_ABI_VERSION; }
+
+// Number of kernel nodes in a captured CUDA graph (cudaGraph_t as void*):
+// the bench's evidence of how many of this library's kernels one step launches.
+extern "C" int64_t hg_graph_kernel_count(void* graph) {
+    if (!graph) return -1;
+    size_t n = 0;
+    if (cudaGraphGetNodes((cudaGraph_t)graph, nullptr, &n) != cudaSuccess) return -1;
+    cudaGraphNode_t* nodes = (cudaGraphNode_t*)malloc(sizeof(cudaGraphNode_t) * (n ? n : 1));
+    if (!nodes) return -1;
+    int64_t k = -1;
+    if (cudaGraphGetNodes((cudaGraph_t)graph, nodes, &n) == cudaSuccess) {
+        k = 0;
+        for (size_t i = 0; i < n; ++i) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++k;
+        }
+    }
+    free(nodes);
+    return k;
+}
 
 // ---------------------------------------------------------------------------
 // exclusive scan over int32 (reduce -> scan tile sums -> apply)

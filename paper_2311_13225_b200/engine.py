@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, dense
 from .device import DeviceGraph, pad4, ptr, stream_ptr
 from .sampler import LayerSampler
 
@@ -125,6 +125,14 @@ class HotBuffers:
             t.zero_()
 
 
+def _new_graph():
+    """A CUDA graph that keeps its cudaGraph_t (kernel-node counting)."""
+    try:
+        return torch.cuda.CUDAGraph(keep_graph=True)
+    except TypeError:
+        return torch.cuda.CUDAGraph()
+
+
 class TrainEngine:
     """Buffers + kernel sequence of one training step for a fixed model/fanout."""
 
@@ -181,13 +189,29 @@ class TrainEngine:
         self.dagg = [zf(self.cap_dst[l], self.ld[l]) if l > 0 else None for l in range(self.L)]
         self.dself = [zf(self.cap_dst[l], self.ld[l]) if (l > 0 and self.sage) else None for l in range(self.L)]
         lib = _lib.load()
-        ws = max(int(lib.hg_wgrad_ws_size(self.dims[l], self.dims[l + 1], self.cap_dst[l])) for l in range(self.L))
+        ws = max(dense.wgrad_ws_size(self.dims[l], self.dims[l + 1], self.cap_dst[l], 2 if self.sage else 1)
+                 for l in range(self.L))
         self.wgrad_ws = zf(max(ws, 1))
         self.d_loss = zf(1)
+        self.row_loss = zf(self.batch_cap)
         self.d_maxdelta = z32(1)
         self.loss_arr = zf(max(max_batches, 1))
         self.md_arr = zf(max(max_batches, 1))
+        # tensor-core B operand images, rebuilt from the current weights each step
+        nm = 1 if not self.sage else 2
+        self.img_fwd = [dense.BImage(self.dims[l], self.dims[l] if self.sage else 0, self.dims[l + 1], 1, dev)
+                        for l in range(self.L)]
+        self.img_dx = [[dense.BImage(self.dims[l + 1], 0, self.dims[l], 0, dev) for _ in range(nm)] if l > 0 else []
+                       for l in range(self.L)]
         self.graph = None
+
+    def enqueue_weight_images(self, stream=None):
+        s = stream_ptr(stream)
+        P = self.params
+        for l in range(self.L):
+            self.img_fwd[l].prep(ptr(P.view(l, 0)), self.dims[l + 1], s)
+            for m, img in enumerate(self.img_dx[l]):
+                img.prep(ptr(P.view(l, m)), self.dims[l + 1], s)
 
     # ------------------------------------------------------------------
     def frontier(self, l):
@@ -205,11 +229,17 @@ class TrainEngine:
             fr, n = self.frontier(l)
             self.samplers[l].run(fr, n, sp, l, stream)
 
-    def enqueue_step(self, stream=None):
+    #: phase boundaries enqueue_step reports through ``mark`` (for split capture / timing)
+    MARKS = ("lookup", "fwd0_agg", "fwd0_gemm", "fwd_upper", "loss", "bwd", "update")
+
+    def enqueue_step(self, stream=None, mark=None):
         s = stream_ptr(stream)
         L, P = self.L, self.params
         g = self.dg
+        mark = mark or (lambda name: None)
+        self.enqueue_weight_images(stream)
         self.enqueue_sample(stream)
+        mark("lookup")
         hot = self.hot
         inj = None
         if hot is not None and L > 1:
@@ -230,57 +260,60 @@ class TrainEngine:
             else:
                 hin, ld_in, glob = self.out[l - 1], self.ld[l], 0
             self_out = self.self_buf if (l == 0 and self.sage) else None
+            mark("fwd0_agg" if l == 0 else "fwd_upper" if l == 1 else "")
             _lib.call("hg_aggregate_fwd", model, glob, ptr(hin), ld_in, self.ld[l], ptr(fr), ptr(n),
                       self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
                       ptr(smp.nself), ptr(smp.outdeg), ptr(inj if l == 0 else None), ptr(self_out),
                       self.ld[0], ptr(self.agg[l]), self.ld[l], s)
             act = 1 if l < L - 1 else 0
-            if self.sage:
+            mark("fwd0_gemm" if l == 0 else "")
+            if self.sage:  # [h_self | mean] [W_self; W_neigh]
                 a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
-                _lib.call("hg_gemm_f32", ptr(a1), lda1, d_in, ptr(P.view(l, 0)), d_out, ptr(self.agg[l]),
-                          self.ld[l], d_in, ptr(P.view(l, 1)), d_out, 0, ptr(self.out[l]), self.ld[l + 1], d_out,
-                          ptr(n), self.cap_dst[l], act, s)
+                dense.fwd(ptr(a1), lda1, ptr(self.agg[l]), self.ld[l], d_in, ptr(P.view(l, 0)), d_out,
+                          ptr(self.out[l]), self.ld[l + 1], ptr(n), self.cap_dst[l], act, s, img=self.img_fwd[l])
             else:
-                _lib.call("hg_gemm_f32", ptr(self.agg[l]), self.ld[l], d_in, ptr(P.view(l, 0)), d_out, None, 0, 0,
-                          None, 0, 0, ptr(self.out[l]), self.ld[l + 1], d_out, ptr(n), self.cap_dst[l], act, s)
+                dense.fwd(ptr(self.agg[l]), self.ld[l], None, 0, d_in, ptr(P.view(l, 0)), d_out, ptr(self.out[l]),
+                          self.ld[l + 1], ptr(n), self.cap_dst[l], act, s, img=self.img_fwd[l])
             if l == 0 and inj is not None:
                 _lib.call("hg_inject_rows", ptr(hot.inj_mask), ptr(hot.inj_slot), ptr(n), self.cap_dst[0],
                           ptr(self.bp), ptr(hot.tab[0]), ptr(hot.tab[1]), hot.H, ptr(self.out[0]), self.ld[1], s)
         # ---------------- loss ----------------
+        mark("loss")
         C = self.dims[L]
         _lib.call("hg_softmax_xent", ptr(self.out[L - 1]), self.ld[L], C, ptr(self.counts_in[0:1]), self.batch_cap,
                   ptr(g.labels), ptr(self.seeds), ptr(self.counts_in[1:2]), ptr(self.dz[L - 1]), self.ld[L],
-                  ptr(self.d_loss), s)
+                  ptr(self.d_loss), ptr(self.row_loss), s)
         # ---------------- backward ----------------
+        mark("bwd")
         for l in range(L - 1, -1, -1):
             smp = self.samplers[l]
             fr, n = self.frontier(l)
             d_in, d_out = self.dims[l], self.dims[l + 1]
-            if self.sage:
+            if self.sage:  # dW_self = h_self^T dz, dW_neigh = mean^T dz (gnnmath.py:190-191)
                 a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
-                _lib.call("hg_wgrad_f32", ptr(a1), lda1, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(n),
-                          self.cap_dst[l], ptr(P.view(l, 0, P.grad)), 1.0, ptr(self.wgrad_ws), s)
-                _lib.call("hg_wgrad_f32", ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
-                          ptr(n), self.cap_dst[l], ptr(P.view(l, 1, P.grad)), 1.0, ptr(self.wgrad_ws), s)
-            else:
-                _lib.call("hg_wgrad_f32", ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
-                          ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), 1.0, ptr(self.wgrad_ws), s)
+                dense.wgrad(ptr(a1), lda1, ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1],
+                            d_out, ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), ptr(P.view(l, 1, P.grad)),
+                            ptr(self.wgrad_ws), s)
+            else:  # dW = agg^T dz (gnnmath.py:135)
+                dense.wgrad(ptr(self.agg[l]), self.ld[l], None, 0, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
+                            ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), s)
             if l == 0:
                 continue
             if self.sage:  # dself = dz W_self^T, dmean = dz W_neigh^T
-                _lib.call("hg_gemm_f32", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_out, None, 0,
-                          0, None, 0, 1, ptr(self.dself[l]), self.ld[l], d_in, ptr(n), self.cap_dst[l], 0, s)
-                _lib.call("hg_gemm_f32", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 1)), d_out, None, 0,
-                          0, None, 0, 1, ptr(self.dagg[l]), self.ld[l], d_in, ptr(n), self.cap_dst[l], 0, s)
+                dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dself[l]),
+                         self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
+                dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 1)), d_in, ptr(self.dagg[l]),
+                         self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][1])
             else:
-                _lib.call("hg_gemm_f32", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_out, None, 0,
-                          0, None, 0, 1, ptr(self.dagg[l]), self.ld[l], d_in, ptr(n), self.cap_dst[l], 0, s)
+                dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dagg[l]),
+                         self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
             _lib.call("hg_aggregate_bwd", model, ptr(self.dagg[l]), self.ld[l], ptr(self.dself[l]), self.ld[l],
                       self.ld[l], ptr(fr), ptr(n), self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots),
                       ptr(smp.nself), ptr(smp.outdeg), ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end),
                       ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]), self.ld[l],
                       ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]), self.ld[l], s)
         # ---------------- update ----------------
+        mark("update")
         if self.allreduce is not None:
             self.allreduce(P.grad)
         if self.optimizer == "sgd":
@@ -308,6 +341,43 @@ class TrainEngine:
         torch.cuda.synchronize(self.device)
         self.graph = g
         return g
+
+    def capture_segments(self, split_at=(), stream: torch.cuda.Stream | None = None):
+        """Capture the step as consecutive graphs split before the marks in
+        ``split_at`` (so a caller can record CUDA events between segments, e.g.
+        around the dominant kernel).  Returns [(first_mark, graph), ...]."""
+        stream = stream or torch.cuda.Stream(device=self.device)
+        saved = self._save_state()
+        stream.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(stream):
+            self.enqueue_step()
+        torch.cuda.current_stream(self.device).wait_stream(stream)
+        torch.cuda.synchronize(self.device)
+        self._restore_state(saved)
+        segs = []
+        cur = {"g": _new_graph(), "name": "start"}
+
+        def mark(name):
+            if name in split_at:
+                cur["g"].capture_end()
+                segs.append((cur["name"], cur["g"]))
+                cur["g"], cur["name"] = _new_graph(), name
+                cur["g"].capture_begin()
+
+        with torch.cuda.stream(stream):
+            cur["g"].capture_begin()
+            self.enqueue_step(mark=mark)
+            cur["g"].capture_end()
+            segs.append((cur["name"], cur["g"]))
+        for _, g in segs:
+            if hasattr(g, "instantiate"):
+                try:
+                    g.instantiate()
+                except RuntimeError:
+                    pass
+        torch.cuda.synchronize(self.device)
+        self.segments = segs
+        return segs
 
     def _save_state(self):
         st = {"flat": self.params.flat.clone(), "md": self.d_maxdelta.clone(),

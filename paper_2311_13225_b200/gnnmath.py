@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, dense
 from .device import pad4, ptr, require_cuda, stream_ptr
 from .seeds import derive_seed
 
@@ -170,12 +170,13 @@ def _layer_forward_dev(model, db, hin, d_in, d_out, W, activation, inj=None):
         _lib.call("hg_aggregate_fwd", code, 0, ptr(hin), ld_in, ld_in, ptr(db.dst), ptr(db.d_n_dst), db.n_dst, db.f,
                   ptr(db.counts), ptr(db.slot_g), ptr(db.slot_local), ptr(db.nself), ptr(db.outdeg), ptr(inj), None,
                   0, ptr(agg), ld_in, s)
-        if code == 0:
-            _lib.call("hg_gemm_f32", ptr(hin), ld_in, d_in, ptr(W[0]), d_out, ptr(agg), ld_in, d_in, ptr(W[1]), d_out,
-                      0, ptr(out), ld_out, d_out, ptr(db.d_n_dst), db.n_dst, int(activation), s)
+        if code == 0:  # [h_self | mean] [W_self; W_neigh]
+            wst = torch.cat([W[0], W[1]], 0).contiguous()
+            dense.fwd(ptr(hin), ld_in, ptr(agg), ld_in, d_in, ptr(wst), d_out, ptr(out), ld_out, ptr(db.d_n_dst),
+                      db.n_dst, int(activation), s)
         else:
-            _lib.call("hg_gemm_f32", ptr(agg), ld_in, d_in, ptr(W[0]), d_out, None, 0, 0, None, 0, 0, ptr(out), ld_out,
-                      d_out, ptr(db.d_n_dst), db.n_dst, int(activation), s)
+            dense.fwd(ptr(agg), ld_in, None, 0, d_in, ptr(W[0]), d_out, ptr(out), ld_out, ptr(db.d_n_dst), db.n_dst,
+                      int(activation), s)
     cache = LayerActivations(dblock=db, h_in=hin, agg=agg, out=out, activation=activation, d_in=d_in, d_out=d_out)
     return out, cache
 
@@ -234,29 +235,27 @@ def backward_batch(caches, dlogits, params: ModelParams):
         if c.activation:  # d_out * (z > 0): the mask is folded in when d was produced (below)
             pass
         ld_in, ld_out = c.h_in.shape[1], dz.shape[1]
-        gl = []
-        mats = [c.h_in, c.agg] if code == 0 else [c.agg]
-        for A in mats:
-            g = torch.zeros((c.d_in, c.d_out), dtype=torch.float32, device=dev)
-            ws = torch.zeros(max(int(_lib.fn("hg_wgrad_ws_size")(c.d_in, c.d_out, db.n_dst)), 1),
-                             dtype=torch.float32, device=dev)
-            _lib.call("hg_wgrad_f32", ptr(A), ld_in, c.d_in, ptr(dz), ld_out, c.d_out, ptr(db.d_n_dst), db.n_dst,
-                      ptr(g), 1.0, ptr(ws), s)
-            gl.append(g.double().cpu().numpy())
-        grads[l] = gl
+        nsrc = 2 if code == 0 else 1
+        g = [torch.zeros((c.d_in, c.d_out), dtype=torch.float32, device=dev) for _ in range(nsrc)]
+        ws = torch.zeros(max(dense.wgrad_ws_size(c.d_in, c.d_out, db.n_dst, nsrc), 1), dtype=torch.float32,
+                         device=dev)
+        if code == 0:  # dW_self = h_self^T dz, dW_neigh = mean^T dz
+            dense.wgrad(ptr(c.h_in), ld_in, ptr(c.agg), ld_in, c.d_in, ptr(dz), ld_out, c.d_out, ptr(db.d_n_dst),
+                        db.n_dst, ptr(g[0]), ptr(g[1]), ptr(ws), s)
+        else:
+            dense.wgrad(ptr(c.agg), ld_in, None, 0, c.d_in, ptr(dz), ld_out, c.d_out, ptr(db.d_n_dst), db.n_dst,
+                        ptr(g[0]), None, ptr(ws), s)
+        grads[l] = [x.double().cpu().numpy() for x in g]
         if l == 0:
             break
         n = max(db.n_dst, 1)
         dagg = torch.zeros((n, ld_in), dtype=torch.float32, device=dev)
         dself = torch.zeros((n, ld_in), dtype=torch.float32, device=dev) if code == 0 else None
         if code == 0:
-            _lib.call("hg_gemm_f32", ptr(dz), ld_out, c.d_out, ptr(W[0]), c.d_out, None, 0, 0, None, 0, 1, ptr(dself),
-                      ld_in, c.d_in, ptr(db.d_n_dst), db.n_dst, 0, s)
-            _lib.call("hg_gemm_f32", ptr(dz), ld_out, c.d_out, ptr(W[1]), c.d_out, None, 0, 0, None, 0, 1, ptr(dagg),
-                      ld_in, c.d_in, ptr(db.d_n_dst), db.n_dst, 0, s)
+            dense.dx(ptr(dz), ld_out, c.d_out, ptr(W[0]), c.d_in, ptr(dself), ld_in, ptr(db.d_n_dst), db.n_dst, s)
+            dense.dx(ptr(dz), ld_out, c.d_out, ptr(W[1]), c.d_in, ptr(dagg), ld_in, ptr(db.d_n_dst), db.n_dst, s)
         else:
-            _lib.call("hg_gemm_f32", ptr(dz), ld_out, c.d_out, ptr(W[0]), c.d_out, None, 0, 0, None, 0, 1, ptr(dagg),
-                      ld_in, c.d_in, ptr(db.d_n_dst), db.n_dst, 0, s)
+            dense.dx(ptr(dz), ld_out, c.d_out, ptr(W[0]), c.d_in, ptr(dagg), ld_in, ptr(db.d_n_dst), db.n_dst, s)
         below = caches[l - 1]
         dx = torch.zeros((max(db.n_src, 1), ld_in), dtype=torch.float32, device=dev)
         _lib.call("hg_aggregate_bwd", code, ptr(dagg), ld_in, ptr(dself), ld_in, ld_in, ptr(db.dst), ptr(db.d_n_dst),
@@ -276,8 +275,9 @@ def loss_and_grad(logits, labels):
     lab = torch.as_tensor(np.asarray(labels, np.int32), device=dev)
     dl = torch.zeros_like(z)
     loss = torch.zeros(1, dtype=torch.float32, device=dev)
+    rows = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
     _lib.call("hg_softmax_xent", ptr(z), z.shape[1], C, None, n, ptr(lab), None, None, ptr(dl), z.shape[1], ptr(loss),
-              stream_ptr())
+              ptr(rows), stream_ptr())
     return float(loss.item()), dl[:n, :C].double().cpu().numpy()
 
 

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _lib, runplan
+from . import _lib, dense, runplan
 from .device import DeviceGraph, pad4, ptr, stream_ptr, u64_tensor
 from .engine import BatchFeeder, HotBuffers, TrainEngine
 from .gnnmath import init_params
@@ -158,6 +158,7 @@ class HotProducer:
         self.agg = zf(self.cap, e.ld[0])
         self.emb = zf(self.cap, e.ld[1])
         self.snaps = zf(max(n_snaps, 1), e.params.bottom_numel)
+        self.img = dense.BImage(e.dims[0], e.dims[0] if e.sage else 0, e.dims[1], 1, dev)
         self.d_n = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def snapshot(self, j: int):
@@ -176,12 +177,13 @@ class HotProducer:
                   ptr(self.smp.outdeg), None, ptr(self.self_buf), e.ld[0], ptr(self.agg), e.ld[0], s)
         w = self.snaps[snap]
         act = 1 if e.L > 1 else 0
+        self.img.prep(ptr(w), d1, s)
         if e.sage:
-            _lib.call("hg_gemm_f32", ptr(self.self_buf), e.ld[0], d0, ptr(w[:d0 * d1]), d1, ptr(self.agg), e.ld[0], d0,
-                      ptr(w[d0 * d1:2 * d0 * d1]), d1, 0, ptr(self.emb), e.ld[1], d1, None, c, act, s)
+            dense.fwd(ptr(self.self_buf), e.ld[0], ptr(self.agg), e.ld[0], d0, ptr(w), d1, ptr(self.emb), e.ld[1],
+                      None, c, act, s, img=self.img)
         else:
-            _lib.call("hg_gemm_f32", ptr(self.agg), e.ld[0], d0, ptr(w[:d0 * d1]), d1, None, 0, 0, None, 0, 0,
-                      ptr(self.emb), e.ld[1], d1, None, c, act, s)
+            dense.fwd(ptr(self.agg), e.ld[0], None, 0, d0, ptr(w), d1, ptr(self.emb), e.ld[1], None, c, act, s,
+                      img=self.img)
         _lib.call("hg_store_put", ptr(ids), None, c, ptr(self.emb), e.ld[1], hot.H, ptr(hot.slot_of),
                   ptr(hot.tab[table]), ptr(hot.ver[table]), ptr(hot.stamp[table]), int(version), int(stamp),
                   ptr(hot.puts), s)
@@ -378,6 +380,36 @@ class Trainer:
     def weights(self):
         return self.engine.params.to_numpy()
 
+    # ------------------------------------------------------------------
+    def train_step(self, seeds: np.ndarray, batch_seed: int, batch_in_epoch: int = 0):
+        """One public training step from HOST seed ids (orchestrator._train_batch +
+        the sampling call before it, orchestrator.py:461-468, 236-256): pinned H2D
+        of the inputs, one graph replay, async D2H of the batch loss into a pinned
+        slot.  Returns a handle; ``handle()`` synchronises and yields the loss."""
+        if not hasattr(self, "_loss_pin"):
+            self._loss_pin = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(8)]
+            self._loss_k = 0
+        gb = self.version
+        n_div = self.dist.global_batch(seeds) if self.dist else None
+        self.feeder.feed(seeds, batch_seed, gb, batch_in_epoch, n_div=n_div)
+        self.engine.run_step()
+        self.version += 1
+        k = self._loss_k
+        self._loss_k = (k + 1) % len(self._loss_pin)
+        pin = self._loss_pin[k]
+        pin.copy_(self.engine.d_loss, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+
+        def handle():
+            ev.synchronize()
+            return float(pin.item())
+        return handle
+
+    @property
+    def d2h_bytes_per_step(self) -> int:
+        return 4
+
 
 def evaluate(trainer_or_graph, weights=None, model=None) -> dict:
     """orchestrator.py:669-680: full-graph, full-neighbour inference accuracy."""
@@ -411,11 +443,10 @@ def full_graph_forward(dg: DeviceGraph, params, val_mask, test_mask, return_logi
         out = torch.zeros((V, ld_out), dtype=torch.float32, device=dev)
         act = 1 if l < params.L - 1 else 0
         if sage:
-            _lib.call("hg_gemm_f32", ptr(h), ld, d_in, ptr(params.view(l, 0)), d_out, ptr(agg), ld, d_in,
-                      ptr(params.view(l, 1)), d_out, 0, ptr(out), ld_out, d_out, ptr(nV), V, act, s)
+            dense.fwd(ptr(h), ld, ptr(agg), ld, d_in, ptr(params.view(l, 0)), d_out, ptr(out), ld_out, ptr(nV), V,
+                      act, s)
         else:
-            _lib.call("hg_gemm_f32", ptr(agg), ld, d_in, ptr(params.view(l, 0)), d_out, None, 0, 0, None, 0, 0,
-                      ptr(out), ld_out, d_out, ptr(nV), V, act, s)
+            dense.fwd(ptr(agg), ld, None, 0, d_in, ptr(params.view(l, 0)), d_out, ptr(out), ld_out, ptr(nV), V, act, s)
         h, ld = out, ld_out
         del agg
     C = params.dims[-1]
