@@ -175,7 +175,32 @@ __global__ void __launch_bounds__(256) k_agg_bwd(
                 else if (slot_g[e] != frontier[d]) { my_row = d; my_w = 1.0f / (float)nself[d]; }
             }
             const int m = min(LPR, end - j0);
-            for (int j = 0; j < m; ++j) {
+            int j = 0;
+            for (; j + 4 <= m; j += 4) {  // four rows in flight, consumed in order
+                int r[4]; float w[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    r[t] = __shfl_sync(gmask, my_row, j + t, LPR);
+                    w[t] = __shfl_sync(gmask, my_w, j + t, LPR);
+                }
+                float4 x[4][NV];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float4* rp = reinterpret_cast<const float4*>(dagg + (int64_t)(r[t] < 0 ? 0 : r[t]) * ld_dagg);
+#pragma unroll
+                    for (int k = 0; k < NV; ++k) {
+                        const int c = lr + k * LPR;
+                        x[t][k] = (r[t] >= 0 && c < F4) ? __ldg(rp + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (r[t] >= 0) {
+#pragma unroll
+                        for (int k = 0; k < NV; ++k) acc[k] = f4_fma(w[t], x[t][k], acc[k]);
+                    }
+            }
+            for (; j < m; ++j) {
                 const int r = __shfl_sync(gmask, my_row, j, LPR);
                 const float w = __shfl_sync(gmask, my_w, j, LPR);
                 if (r >= 0) {

@@ -413,17 +413,31 @@ k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2,
     if (warp == 0) tmem_dealloc(tmem, NCOLS);
 }
 
-__global__ void k_wgrad_tc_reduce(const float* __restrict__ partial, int KN, int n_src, int n_chunks,
-                                  int rows_per_chunk, const int* __restrict__ d_M, int M_cap, float* __restrict__ out1,
-                                  float* __restrict__ out2) {
+// Fixed-order reduction of the per-chunk partials: block = 32 consecutive
+// outputs x 8 warps; warp w sums chunks w, w+8, ... (coalesced 128-byte rows),
+// then warp 0 adds the 8 warp sums in order.  Deterministic.
+__global__ void __launch_bounds__(256) k_wgrad_tc_reduce(const float* __restrict__ partial, int KN, int n_src,
+                                                         int n_chunks, int rows_per_chunk, const int* __restrict__ d_M,
+                                                         int M_cap, float* __restrict__ out1, float* __restrict__ out2) {
+    __shared__ float s_part[8][33];
     const int M = hg_load_count(d_M, M_cap);
     const int chunks = min(n_chunks, (M + rows_per_chunk - 1) / rows_per_chunk);
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < KN * n_src; idx += gridDim.x * blockDim.x) {
-        const int s = idx / KN, e = idx - s * KN;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int per_src = (KN + 31) / 32;
+    const int s = blockIdx.x / per_src;
+    const int e = (blockIdx.x - s * per_src) * 32 + lane;
+    float acc = 0.f;
+    if (e < KN) {
         const float* p = partial + (int64_t)s * n_chunks * KN + e;
-        float acc = 0.f;
-        for (int c = 0; c < chunks; ++c) acc += p[(int64_t)c * KN];
-        (s ? out2 : out1)[e] = acc;
+        for (int c = w; c < chunks; c += 8) acc += p[(int64_t)c * KN];
+    }
+    s_part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && e < KN) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += s_part[k][lane];
+        (s ? out2 : out1)[e] = t;
     }
 }
 
@@ -566,7 +580,7 @@ extern "C" int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32
         else rc = launch_wgrad<256>(grid, s, A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, rpc, chunks, ws);
         if (rc) return rc;
     }
-    k_wgrad_tc_reduce<<<hg_grid((long long)K * N * n_src, 256, 4), 256, 0, s>>>(ws, K * N, n_src, chunks, rpc, d_M,
-                                                                                M_cap, out1, out2);
+    k_wgrad_tc_reduce<<<n_src * hg_ceil_div(K * N, 32), 256, 0, s>>>(ws, K * N, n_src, chunks, rpc, d_M, M_cap, out1,
+                                                                     out2);
     return hg_check_launch("wgrad_tc_reduce");
 }

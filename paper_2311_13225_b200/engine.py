@@ -197,12 +197,23 @@ class TrainEngine:
         self.d_maxdelta = z32(1)
         self.loss_arr = zf(max(max_batches, 1))
         self.md_arr = zf(max(max_batches, 1))
+        self.side = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
         # tensor-core B operand images, rebuilt from the current weights each step
-        nm = 1 if not self.sage else 2
         self.img_fwd = [dense.BImage(self.dims[l], self.dims[l] if self.sage else 0, self.dims[l + 1], 1, dev)
                         for l in range(self.L)]
-        self.img_dx = [[dense.BImage(self.dims[l + 1], 0, self.dims[l], 0, dev) for _ in range(nm)] if l > 0 else []
-                       for l in range(self.L)]
+        # SAGE dX: one GEMM against the stacked [W_self; W_neigh] gives [dself | dmean]
+        # side by side (when d_in keeps both halves 16-byte aligned)
+        self.fused_dx = [self.sage and l > 0 and self.dims[l] % 4 == 0 for l in range(self.L)]
+        self.dcat = [zf(self.cap_dst[l], 2 * self.dims[l]) if self.fused_dx[l] else None for l in range(self.L)]
+        self.img_dx = []
+        for l in range(self.L):
+            if l == 0:
+                self.img_dx.append([])
+            elif self.fused_dx[l]:
+                self.img_dx.append([dense.BImage(self.dims[l + 1], 0, 2 * self.dims[l], 0, dev)])
+            else:
+                nm = 2 if self.sage else 1
+                self.img_dx.append([dense.BImage(self.dims[l + 1], 0, self.dims[l], 0, dev) for _ in range(nm)])
         self.graph = None
 
     def enqueue_weight_images(self, stream=None):
@@ -233,12 +244,26 @@ class TrainEngine:
     MARKS = ("lookup", "fwd0_agg", "fwd0_gemm", "fwd_upper", "loss", "bwd", "update")
 
     def enqueue_step(self, stream=None, mark=None):
-        s = stream_ptr(stream)
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = main.cuda_stream
         L, P = self.L, self.params
         g = self.dg
         mark = mark or (lambda name: None)
-        self.enqueue_weight_images(stream)
-        self.enqueue_sample(stream)
+        # fork: the weight images and the transposed (backward) block views do not
+        # sit on the sampling critical path; they run on side streams (parallel
+        # branches of the captured graph) and join before the first dense op.
+        sw, sc = self.side
+        sw.wait_stream(main)
+        self.enqueue_weight_images(sw)
+        for l in range(L - 1, -1, -1):
+            fr, n = self.frontier(l)
+            self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False)
+            if l > 0:
+                sc.wait_stream(main)
+                self.samplers[l].build_csc(n, sc)
+        main.wait_stream(sw)
+        if L > 1:
+            main.wait_stream(sc)
         mark("lookup")
         hot = self.hot
         inj = None
@@ -299,16 +324,22 @@ class TrainEngine:
                             ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), s)
             if l == 0:
                 continue
-            if self.sage:  # dself = dz W_self^T, dmean = dz W_neigh^T
+            if self.fused_dx[l]:  # [dself | dmean] = dz [W_self; W_neigh]^T in one GEMM
+                dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), 2 * d_in, ptr(self.dcat[l]),
+                         2 * d_in, ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
+                dsp, dsl = self.dcat[l].data_ptr(), 2 * d_in
+                dap, dal = dsp + 4 * d_in, 2 * d_in
+            elif self.sage:  # dself = dz W_self^T, dmean = dz W_neigh^T
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dself[l]),
                          self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 1)), d_in, ptr(self.dagg[l]),
                          self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][1])
+                dsp, dsl, dap, dal = ptr(self.dself[l]), self.ld[l], ptr(self.dagg[l]), self.ld[l]
             else:
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dagg[l]),
                          self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
-            _lib.call("hg_aggregate_bwd", model, ptr(self.dagg[l]), self.ld[l], ptr(self.dself[l]), self.ld[l],
-                      self.ld[l], ptr(fr), ptr(n), self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots),
+                dsp, dsl, dap, dal = None, 0, ptr(self.dagg[l]), self.ld[l]
+            _lib.call("hg_aggregate_bwd", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n), self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots),
                       ptr(smp.nself), ptr(smp.outdeg), ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end),
                       ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]), self.ld[l],
                       ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]), self.ld[l], s)

@@ -136,8 +136,11 @@ class LayerSampler:
             self.seg_end = z(self.cap_src)
             self.csc_ws = z(lib.hg_csc_ws_size(self.cap_dst, self.f))
 
-    def run(self, frontier, d_n_dst, d_seed, layer: int, stream=None, cap_dst: int | None = None):
-        """Enqueue the block build for `frontier` (device int32, count *d_n_dst)."""
+    def run(self, frontier, d_n_dst, d_seed, layer: int, stream=None, cap_dst: int | None = None,
+            with_csc: bool = True):
+        """Enqueue the block build for `frontier` (device int32, count *d_n_dst).
+        ``with_csc=False`` defers the transposed view to ``build_csc`` (e.g. on a
+        side stream, off the forward critical path)."""
         cap = self.cap_dst if cap_dst is None else int(cap_dst)
         assert cap <= self.cap_dst
         cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
@@ -150,10 +153,15 @@ class LayerSampler:
         _lib.call("hg_dedup_relabel", ptr(frontier), ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slots),
                   ptr(self.slot_local), ptr(self.minpos), ptr(self.src), ptr(self.n_src), cap_src, ptr(self.nself),
                   ptr(self.outdeg), ptr(self.ws), s)
-        if self.need_csc:
-            _lib.call("hg_build_csc", ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slot_local), cap_src,
-                      ptr(self.csc_slot), ptr(self.seg_beg), ptr(self.seg_end), ptr(self.csc_ws), s)
+        if self.need_csc and with_csc:
+            self.build_csc(d_n_dst, stream, cap)
         return self
+
+    def build_csc(self, d_n_dst, stream=None, cap_dst: int | None = None):
+        cap = self.cap_dst if cap_dst is None else int(cap_dst)
+        cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
+        _lib.call("hg_build_csc", ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slot_local), cap_src,
+                  ptr(self.csc_slot), ptr(self.seg_beg), ptr(self.seg_end), ptr(self.csc_ws), stream_ptr(stream))
 
     # -- host views (sync) ---------------------------------------------------
     def to_block(self, frontier_np: np.ndarray, stream=None) -> Block:
