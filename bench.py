@@ -229,10 +229,12 @@ def main():
                       strategy="case1", hot_ratio=0.0, use_graph=True, seed=0)
     tr = Trainer(ds, cfg, dist=dist_ctx)
     e = tr.engine
-    # segments split around the dominant kernel (bottom fused gather+aggregate)
-    segs = e.capture_segments(split_at=("fwd0_agg", "fwd0_gemm"))
-    names = [n for n, _ in segs]
-    assert names == ["start", "fwd0_agg", "fwd0_gemm"], names
+    # per sample set: the sample-half graph and the train half split around the
+    # dominant kernel (bottom fused gather+aggregate), so CUDA events bracket it
+    # (train half = [store lookup (none here) + bottom aggregate | rest])
+    parts = [e.capture_segments(split_at=("fwd0_gemm",), set_index=k) for k in range(len(e.sets))]
+    for _, segs in parts:
+        assert [n for n, _ in segs] == ["start", "fwd0_gemm"], [n for n, _ in segs]
     K, W = args.steps, args.warmup
     batches, rseeds = epoch_batches(ds, W + K, rank=rank, world=world)
     # stage every step's inputs in HBM (value = device-resident inputs)
@@ -245,23 +247,53 @@ def main():
     n_div = 1024 * world
     d_counts = torch.tensor([1024, n_div], dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
+    ss, st = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    nset = len(e.sets)
+    sampled = [torch.cuda.Event() for _ in range(nset)]
+    trained = [None] * nset
     ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
 
-    def step(i, timed_idx=None):
-        e.seeds.copy_(d_seeds[i], non_blocking=True)
-        e.bp.copy_(d_bp[i], non_blocking=True)
-        e.counts_in.copy_(d_counts, non_blocking=True)
-        segs[0][1].replay()
-        if timed_idx is not None:
-            ev_a[timed_idx].record(stream)
-        segs[1][1].replay()
-        if timed_idx is not None:
-            ev_b[timed_idx].record(stream)
-        segs[2][1].replay()
+    def sample(i):
+        k = i % nset
+        if trained[k] is not None:
+            ss.wait_event(trained[k])
+        with torch.cuda.stream(ss):
+            s = e.sets[k]
+            s.seeds.copy_(d_seeds[i], non_blocking=True)
+            s.bp.copy_(d_bp[i], non_blocking=True)
+            s.counts_in.copy_(d_counts, non_blocking=True)
+            parts[k][0].replay()
+            sampled[k].record(ss)
 
-    for i in range(W):
-        step(i)
+    def train(i, timed_idx=None):
+        k = i % nset
+        st.wait_event(sampled[k])
+        segs = parts[k][1]
+        with torch.cuda.stream(st):
+            if timed_idx is not None:
+                ev_a[timed_idx].record(st)
+            segs[0][1].replay()
+            if timed_idx is not None:
+                ev_b[timed_idx].record(st)
+            segs[1][1].replay()
+            ev = torch.cuda.Event()
+            ev.record(st)
+            trained[k] = ev
+
+    def run(lo, hi, timed=False):
+        """Software pipeline: sample batch i+1 (stream ss) while batch i trains (st)."""
+        ss.wait_stream(stream)
+        st.wait_stream(stream)
+        sample(lo)
+        for i in range(lo, hi):
+            if i + 1 < hi:
+                sample(i + 1)
+            train(i, (i - lo) if timed else None)
+        stream.wait_stream(ss)
+        stream.wait_stream(st)
+
+    run(0, W)
     torch.cuda.synchronize()
     if dist_ctx:
         dist_ctx.barrier()
@@ -272,8 +304,7 @@ def main():
     t_end = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     t_start.record(stream)
-    for k in range(K):
-        step(W + k, k)
+    run(W, W + K, timed=True)
     t_end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -284,15 +315,16 @@ def main():
         ms = dist_ctx.max_over_ranks(ms)
     value = world * 1024 * K / (ms / 1000.0)
     agg_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]))
-    # algorithmic bytes of the dominant kernel per launch (DESIGN.md §4):
+    # algorithmic bytes of the dominant kernel per launch (DESIGN.md §3):
     # unique src rows read + edge ids + per-dst metadata + [self | mean] rows written
     F = ds.feat_dim
     sizes = []
+    e.cur = 0
     for i in range(min(K, 16)):
         e.seeds.copy_(d_seeds[W + i])
         e.bp.copy_(d_bp[W + i])
         e.counts_in.copy_(d_counts)
-        segs[0][1].replay()
+        parts[0][0].replay()
         torch.cuda.synchronize()
         n_dst0 = int(e.samplers[1].n_src.item())
         n_src0 = int(e.samplers[0].n_src.item())
@@ -310,7 +342,7 @@ def main():
     # kernels per step (graph kernel nodes) -> launches in the timed region
     lib = _lib.load()
     per_step = 0
-    for _, g in segs:
+    for g in [parts[0][0]] + [g for _, g in parts[0][1]]:
         try:
             per_step += int(lib.hg_graph_kernel_count(g.raw_cuda_graph()))
         except Exception:
@@ -318,20 +350,17 @@ def main():
             break
     # ---- e2e through the public API from host seed ids ----
     e2e_K = K
-    handles = []
     torch.cuda.synchronize()
     e2e_start = torch.cuda.Event(enable_timing=True)
     e2e_end = torch.cuda.Event(enable_timing=True)
     host_batches = [np.asarray(b, np.int64) for b in batches]
-    for i in range(3):
-        tr.train_step(host_batches[i], rseeds[i])()
+    [h() for h in tr.train_batches([(host_batches[i], rseeds[i]) for i in range(3)])]
     torch.cuda.synchronize()
     if dist_ctx:
         dist_ctx.barrier()
     wall0 = time.perf_counter()
     e2e_start.record(stream)
-    for k in range(e2e_K):
-        handles.append(tr.train_step(host_batches[W + k], rseeds[W + k], batch_in_epoch=0))
+    handles = tr.train_batches([(host_batches[W + k], rseeds[W + k]) for k in range(e2e_K)])
     losses = [h() for h in handles]
     e2e_end.record(stream)
     torch.cuda.synchronize()
@@ -379,10 +408,14 @@ def main():
 
 
 def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):
-    """Per-phase device time (ms) of one step, from a capture split at every mark."""
+    """Per-phase device time (ms) of one step run SEQUENTIALLY (sample half, then
+    the train half split at every mark; no cross-batch overlap)."""
     import torch
-    segs = e.capture_segments(split_at=tuple(m for m in e.MARKS))
+    marks = tuple(m for m in e.MARKS if e.hot is not None or m != "fwd0_agg")  # no empty segments
+    gs, segs = e.capture_segments(split_at=marks)
+    segs = [("sample", gs)] + [(("train_start" if n == "start" else n), g) for n, g in segs]
     tot = {n: 0.0 for n, _ in segs}
+    e.cur = 0
     for r in range(reps):
         e.seeds.copy_(d_seeds[i0 + r % d_seeds.shape[0]])
         e.bp.copy_(d_bp[i0 + r % d_bp.shape[0]])

@@ -153,31 +153,128 @@ __device__ __forceinline__ bool pos_item(long long p, int n, int f, const int* f
     return true;
 }
 
-// flag[p] = (position p holds the first occurrence of its id)
-__global__ void k_mark(const int* __restrict__ frontier, const int* d_n, int cap, int f,
-                       const int* __restrict__ counts, const int* __restrict__ slots,
-                       const int* __restrict__ minpos, int* __restrict__ flags) {
-    const int n = hg_load_count(d_n, cap);
-    const long long P = (long long)n * (f + 1);
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
-         p += (long long)gridDim.x * blockDim.x) {
-        int u;
-        flags[p] = (pos_item(p, n, f, frontier, counts, slots, u) && minpos[u] == (int)p) ? 1 : 0;
-    }
+// ---------------------------------------------------------------------------
+// Single-pass first-occurrence compaction (replaces flag -> 3-kernel scan ->
+// emit): each 2048-position tile marks its first occurrences (minpos[u] == p),
+// scans them in the block, resolves its global offset by decoupled look-back
+// over the predecessors' published (aggregate | inclusive prefix) words, then
+// writes rank[p] and src_vertices[rank] = u.  The tile that holds position P-1
+// writes n_src.  Status words carry a generation (bits 34..63) so the array
+// never needs clearing: generation = *d_gen + 1, bumped by the relabel kernel.
+// ---------------------------------------------------------------------------
+constexpr int MS_THREADS = 256;
+constexpr int MS_ITEMS = 8;
+constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
+
+__device__ __forceinline__ unsigned long long ms_word(uint32_t gen, uint32_t flag, uint32_t v) {
+    return ((unsigned long long)gen << 34) | ((unsigned long long)flag << 32) | v;
 }
 
-// src_vertices[rank[p]] = id, for first occurrences (rank = exclusive scan of flags)
-__global__ void k_emit_src(const int* __restrict__ frontier, const int* d_n, int cap, int f,
-                           const int* __restrict__ counts, const int* __restrict__ slots,
-                           const int* __restrict__ minpos, const int* __restrict__ rank,
-                           int* __restrict__ src_vertices) {
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__ frontier, const int* d_n, int cap,
+                                                         int f, const int* __restrict__ counts,
+                                                         const int* __restrict__ slots,
+                                                         const int* __restrict__ minpos, int* __restrict__ rank,
+                                                         int* __restrict__ src_vertices, int* __restrict__ d_n_src,
+                                                         unsigned long long* __restrict__ status,
+                                                         const int* __restrict__ d_gen) {
+    __shared__ int s_warp[MS_THREADS / 32];
+    __shared__ int s_prefix;
     const int n = hg_load_count(d_n, cap);
     const long long P = (long long)n * (f + 1);
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < P;
-         p += (long long)gridDim.x * blockDim.x) {
-        int u;
-        if (pos_item(p, n, f, frontier, counts, slots, u) && minpos[u] == (int)p) src_vertices[rank[p]] = u;
+    const int t = blockIdx.x;
+    const long long p0 = (long long)t * MS_TILE;
+    if (p0 >= P) {
+        if (t == 0 && threadIdx.x == 0) *d_n_src = 0;
+        return;  // no later tile waits on this one
     }
+    const uint32_t gen = (uint32_t)(*d_gen) + 1u;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int u[MS_ITEMS];
+    unsigned flags = 0;
+    int cnt = 0;
+    const long long my0 = p0 + (long long)threadIdx.x * MS_ITEMS;
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        const long long p = my0 + k;
+        int x = -1;
+        if (p < P && pos_item(p, n, f, frontier, counts, slots, x) && minpos[x] == (int)p) {
+            flags |= 1u << k;
+            ++cnt;
+        }
+        u[k] = x;
+    }
+    // block exclusive scan of per-thread counts
+    int x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < MS_THREADS / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < MS_THREADS / 32) s_warp[lane] = w;
+    }
+    __syncthreads();
+    const int tile_total = s_warp[MS_THREADS / 32 - 1];
+    int local = (wid ? s_warp[wid - 1] : 0) + x - cnt;
+    if (wid == 0) {  // decoupled look-back
+        int excl = 0;
+        if (t == 0) {
+            if (lane == 0) st_release_u64(&status[0], ms_word(gen, 2, (uint32_t)tile_total));
+        } else {
+            if (lane == 0) st_release_u64(&status[t], ms_word(gen, 1, (uint32_t)tile_total));
+            int idx = t - 1;
+            while (true) {
+                const int j = idx - lane;
+                unsigned long long w = 0;
+                uint32_t fl = 2, val = 0;
+                if (j >= 0) {
+                    do {
+                        w = ld_acquire_u64(&status[j]);
+                    } while ((uint32_t)(w >> 34) != gen || ((w >> 32) & 3u) == 0u);
+                    fl = (uint32_t)((w >> 32) & 3u);
+                    val = (uint32_t)w;
+                }
+                const unsigned incl = __ballot_sync(0xffffffffu, fl == 2u);
+                const int stop = incl ? (__ffs(incl) - 1) : 32;
+                int contrib = lane <= stop ? (int)val : 0;  // lanes past the first inclusive word ignored
+#pragma unroll
+                for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+                excl += contrib;
+                if (incl) break;
+                idx -= 32;
+            }
+            if (lane == 0) st_release_u64(&status[t], ms_word(gen, 2, (uint32_t)(excl + tile_total)));
+        }
+        if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    local += s_prefix;
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        if (flags & (1u << k)) {
+            rank[my0 + k] = local;
+            src_vertices[local] = u[k];
+            ++local;
+        }
+    }
+    if (p0 + MS_TILE >= P && threadIdx.x == 0) *d_n_src = s_prefix + tile_total;
 }
 
 // per destination: local id = rank[minpos[id]]; sort the segment by local id
@@ -251,8 +348,9 @@ __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* 
 }
 
 __global__ void k_reset_minpos(const int* __restrict__ src_vertices, const int* d_n_src, int cap,
-                               int* __restrict__ minpos) {
+                               int* __restrict__ minpos, int* __restrict__ d_gen) {
     const int n = hg_load_count(d_n_src, cap);
+    if (d_gen && blockIdx.x == 0 && threadIdx.x == 0) *d_gen += 1;  // next k_markscan generation
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
         minpos[src_vertices[k]] = HG_INT_MAX;
 }
@@ -357,9 +455,12 @@ extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, c
 // ws: >= hg_dedup_ws_size(cap_dst, fanout) ints.  Produces src_vertices[0..n_src),
 // *d_n_src, sorted slots / slot_local, nself (nullable), outdeg (nullable; must be
 // zeroed over cap_src by the caller), and restores minpos.
+// ws layout (ints): rank[P] | pad | status (uint64)[tiles] | generation counter.
+// The workspace must be zero-filled once when allocated and then kept.
 extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
     long long P = (long long)cap_dst * (fanout + 1);
-    return (int64_t)(P + (long long)hg_scan_ws_ints(P) + 16);
+    long long tiles = (P + MS_TILE - 1) / MS_TILE;
+    return (int64_t)(((P + 1) & ~1LL) + 2 * tiles + 4);
 }
 
 extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
@@ -369,13 +470,12 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
     cudaStream_t s = (cudaStream_t)stream;
     if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("dedup(empty)"); }
     const long long P = (long long)cap_dst * (fanout + 1);
-    int* flags = ws;
-    int* scan_ws = ws + P;
-    const int g = hg_grid(P, 256, 8);
-    k_mark<<<g, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos, flags);
-    int rc = hg_scan_launch(flags, flags, d_n_dst, fanout + 1, P, d_n_src, scan_ws, s);
-    if (rc) return rc;
-    k_emit_src<<<g, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos, flags, src_vertices);
+    const long long tiles = (P + MS_TILE - 1) / MS_TILE;
+    int* flags = ws;  // rank of each first-occurrence position
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + ((P + 1) & ~1LL));
+    int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
+    k_markscan<<<(unsigned)tiles, MS_THREADS, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos,
+                                                      flags, src_vertices, d_n_src, status, d_gen);
     if (fanout <= 32) {
         const int W = seg_width(fanout);
         const int grid = hg_grid((long long)cap_dst * W, 256, 8);
@@ -389,7 +489,7 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
         k_relabel_sort_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
                                                                     slot_local, minpos, flags, nself, outdeg);
     }
-    k_reset_minpos<<<hg_grid(cap_src, 256, 8), 256, 0, s>>>(src_vertices, d_n_src, cap_src, minpos);
+    k_reset_minpos<<<hg_grid(cap_src, 256, 8), 256, 0, s>>>(src_vertices, d_n_src, cap_src, minpos, d_gen);
     return hg_check_launch("dedup_relabel");
 }
 

@@ -133,12 +133,28 @@ def _new_graph():
         return torch.cuda.CUDAGraph()
 
 
+@dataclass
+class SampleSet:
+    """One batch's sampled blocks plus its per-batch device inputs."""
+
+    samplers: list
+    seeds: torch.Tensor      # int32 [batch_cap]
+    counts_in: torch.Tensor  # int32 [2]: n_seeds, gradient divisor (global batch)
+    bp: torch.Tensor         # int64 [BP_SIZE] parameter block
+
+
 class TrainEngine:
     """Buffers + kernel sequence of one training step for a fixed model/fanout."""
 
+    # the current sample set's views (eager steps, capture and host planning use set `cur`)
+    samplers = property(lambda self: self.sets[self.cur].samplers)
+    seeds = property(lambda self: self.sets[self.cur].seeds)
+    counts_in = property(lambda self: self.sets[self.cur].counts_in)
+    bp = property(lambda self: self.sets[self.cur].bp)
+
     def __init__(self, dg: DeviceGraph, model: str, dims, fanouts, batch_cap: int, lr: float,
                  optimizer: str = "sgd", weights=None, hot: HotBuffers | None = None, max_batches: int = 1,
-                 allreduce=None):
+                 allreduce=None, n_sets: int = 2):
         _lib.load()
         if model not in ("gcn", "sage"):
             raise ValueError(f"unknown model {model!r}")
@@ -167,14 +183,20 @@ class TrainEngine:
             self.cap_src[l] = int(min(V, self.cap_dst[l] * (self.fan[l] + 1)))
             if l > 0:
                 self.cap_dst[l - 1] = self.cap_src[l]
-        self.samplers = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage,
-                                      need_outdeg=not self.sage, need_csc=l > 0) for l in range(self.L)]
-        # ---- per-batch inputs ----
+        # ---- two sample sets (blocks + per-batch inputs): batch k+1 is sampled into
+        # one while batch k trains from the other (the reference's sampler/trainer
+        # overlap, SPEC pipelining; sampling never reads weights, so results are
+        # bit-identical to the sequential order) ----
         z32 = lambda *s: torch.zeros(*s, dtype=torch.int32, device=dev)  # noqa: E731
         zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
-        self.seeds = z32(self.batch_cap)
-        self.counts_in = z32(2)  # [n_seeds, n_div]
-        self.bp = torch.zeros(BP_SIZE, dtype=torch.int64, device=dev)
+        self.sets = []
+        for k in range(n_sets):
+            mp = None if k == 0 else torch.full_like(dg.minpos, 2**31 - 1)
+            smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage, need_outdeg=not self.sage,
+                                need_csc=l > 0, minpos=mp) for l in range(self.L)]
+            self.sets.append(SampleSet(samplers=smp, seeds=z32(self.batch_cap), counts_in=z32(2),
+                                       bp=torch.zeros(BP_SIZE, dtype=torch.int64, device=dev)))
+        self.cur = 0
         # ---- parameters ----
         self.params = DenseParams(model, self.dims, weights, dev)
         if optimizer == "adam":
@@ -215,6 +237,9 @@ class TrainEngine:
                 nm = 2 if self.sage else 1
                 self.img_dx.append([dense.BImage(self.dims[l + 1], 0, self.dims[l], 0, dev) for _ in range(nm)])
         self.graph = None
+        self.g_sample = None
+        self.g_train = None
+        self.enqueue_weight_images()
 
     def enqueue_weight_images(self, stream=None):
         s = stream_ptr(stream)
@@ -241,30 +266,34 @@ class TrainEngine:
             self.samplers[l].run(fr, n, sp, l, stream)
 
     #: phase boundaries enqueue_step reports through ``mark`` (for split capture / timing)
-    MARKS = ("lookup", "fwd0_agg", "fwd0_gemm", "fwd_upper", "loss", "bwd", "update")
+    MARKS = ("fwd0_agg", "fwd0_gemm", "fwd_upper", "loss", "bwd", "update")
 
     def enqueue_step(self, stream=None, mark=None):
+        """One whole batch (sample + train) on one stream."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        s = main.cuda_stream
-        L, P = self.L, self.params
-        g = self.dg
-        mark = mark or (lambda name: None)
-        # fork: the weight images and the transposed (backward) block views do not
-        # sit on the sampling critical path; they run on side streams (parallel
-        # branches of the captured graph) and join before the first dense op.
-        sw, sc = self.side
-        sw.wait_stream(main)
-        self.enqueue_weight_images(sw)
-        for l in range(L - 1, -1, -1):
+        self.enqueue_sample_part(main)
+        self.enqueue_train_part(main, mark)
+
+    def enqueue_sample_part(self, stream=None):
+        """Blocks L-1..0 of the current set; the transposed (backward) views are
+        built on a side stream (a parallel graph branch) joined at the end."""
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        sc = self.side[1]
+        for l in range(self.L - 1, -1, -1):
             fr, n = self.frontier(l)
             self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False)
             if l > 0:
                 sc.wait_stream(main)
                 self.samplers[l].build_csc(n, sc)
-        main.wait_stream(sw)
-        if L > 1:
+        if self.L > 1:
             main.wait_stream(sc)
-        mark("lookup")
+
+    def enqueue_train_part(self, stream=None, mark=None):
+        main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        s = main.cuda_stream
+        L, P = self.L, self.params
+        g = self.dg
+        mark = mark or (lambda name: None)
         hot = self.hot
         inj = None
         if hot is not None and L > 1:
@@ -354,37 +383,61 @@ class TrainEngine:
                       0.9, 0.999, 1e-8, ptr(self.adam_t), ptr(self.d_maxdelta), s)
         _lib.call("hg_record_batch", ptr(self.bp), ptr(self.d_loss), ptr(self.d_maxdelta), ptr(self.loss_arr),
                   ptr(self.md_arr), s)
+        # tensor-core B images of the updated weights, ready for the next step
+        self.enqueue_weight_images(main)
 
     # ------------------------------------------------------------------
-    def capture(self, stream: torch.cuda.Stream | None = None):
-        """Capture enqueue_step into a CUDA graph (one launch per batch)."""
-        stream = stream or torch.cuda.Stream(device=self.device)
+    def _warmup(self, stream):
+        """Run one eager step outside capture (lazy module loads, smem attributes),
+        then undo its side effects."""
         saved = self._save_state()
         stream.wait_stream(torch.cuda.current_stream(self.device))
-        with torch.cuda.stream(stream):  # warm-up outside capture (lazy module loads)
-            self.enqueue_step()
+        with torch.cuda.stream(stream):
+            for k in range(len(self.sets)):
+                self.cur = k
+                self.enqueue_step(stream)
+        self.cur = 0
         torch.cuda.current_stream(self.device).wait_stream(stream)
         torch.cuda.synchronize(self.device)
         self._restore_state(saved)
+
+    def capture(self, stream: torch.cuda.Stream | None = None):
+        """Capture enqueue_step (set 0) into one CUDA graph, and the sample /
+        train halves of every set into separate graphs for pipelined replay."""
+        stream = stream or torch.cuda.Stream(device=self.device)
+        self._warmup(stream)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             self.enqueue_step()
+        self.g_sample, self.g_train = [], []
+        for k in range(len(self.sets)):
+            self.cur = k
+            gs, gt = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gs, stream=stream):
+                self.enqueue_sample_part()
+            with torch.cuda.graph(gt, stream=stream):
+                self.enqueue_train_part()
+            self.g_sample.append(gs)
+            self.g_train.append(gt)
+        self.cur = 0
         torch.cuda.synchronize(self.device)
         self.graph = g
         return g
 
-    def capture_segments(self, split_at=(), stream: torch.cuda.Stream | None = None):
-        """Capture the step as consecutive graphs split before the marks in
-        ``split_at`` (so a caller can record CUDA events between segments, e.g.
-        around the dominant kernel).  Returns [(first_mark, graph), ...]."""
+    def capture_segments(self, split_at=(), stream: torch.cuda.Stream | None = None, set_index: int = 0):
+        """Capture the TRAIN half of set ``set_index`` as consecutive graphs split
+        before the marks in ``split_at`` (so a caller can record CUDA events between
+        segments, e.g. around the dominant kernel), plus its sample half.
+        Returns (sample_graph, [(first_mark, graph), ...])."""
         stream = stream or torch.cuda.Stream(device=self.device)
-        saved = self._save_state()
-        stream.wait_stream(torch.cuda.current_stream(self.device))
+        if self.g_sample is None:
+            self._warmup(stream)
+        self.cur = set_index
+        gs = _new_graph()
         with torch.cuda.stream(stream):
-            self.enqueue_step()
-        torch.cuda.current_stream(self.device).wait_stream(stream)
-        torch.cuda.synchronize(self.device)
-        self._restore_state(saved)
+            gs.capture_begin()
+            self.enqueue_sample_part()
+            gs.capture_end()
         segs = []
         cur = {"g": _new_graph(), "name": "start"}
 
@@ -397,18 +450,18 @@ class TrainEngine:
 
         with torch.cuda.stream(stream):
             cur["g"].capture_begin()
-            self.enqueue_step(mark=mark)
+            self.enqueue_train_part(mark=mark)
             cur["g"].capture_end()
             segs.append((cur["name"], cur["g"]))
-        for _, g in segs:
+        self.cur = 0
+        for g in [gs] + [g for _, g in segs]:
             if hasattr(g, "instantiate"):
                 try:
                     g.instantiate()
                 except RuntimeError:
                     pass
         torch.cuda.synchronize(self.device)
-        self.segments = segs
-        return segs
+        return gs, segs
 
     def _save_state(self):
         st = {"flat": self.params.flat.clone(), "md": self.d_maxdelta.clone(),
@@ -437,13 +490,69 @@ class TrainEngine:
             h.batch_miss.copy_(st["miss"])
             h.batch_warm.copy_(st["warm"])
             h.stats.copy_(st["stats"])
+        self.enqueue_weight_images()
         torch.cuda.synchronize(self.device)
 
     def run_step(self, stream=None):
+        """Sequential step on the current stream (set 0)."""
         if self.graph is not None:
             self.graph.replay()
         else:
+            self.cur = 0
             self.enqueue_step(stream)
+
+
+class Pipeline:
+    """Two-stream software pipeline over batches: the sample half of batch k+1
+    runs on ``ss`` while the train half of batch k runs on ``st``; sample set
+    k % 2 is reused only after batch k-2 finished training."""
+
+    def __init__(self, engine: TrainEngine):
+        self.e = engine
+        dev = engine.device
+        self.ss = torch.cuda.Stream(device=dev)
+        self.st = torch.cuda.Stream(device=dev)
+        n = len(engine.sets)
+        self.sampled = [torch.cuda.Event() for _ in range(n)]
+        self.trained = [None] * n
+
+    def sample(self, k: int, feed):
+        """``feed(set_index)`` stages batch k's inputs (on the sampling stream)."""
+        e, st = self.e, k % len(self.e.sets)
+        self.ss.wait_stream(torch.cuda.current_stream(e.device))
+        if self.trained[st] is not None:
+            self.ss.wait_event(self.trained[st])
+        with torch.cuda.stream(self.ss):
+            feed(st)
+            if e.g_sample is not None:
+                e.g_sample[st].replay()
+            else:
+                e.cur = st
+                e.enqueue_sample_part(self.ss)
+                e.cur = 0
+            self.sampled[st].record(self.ss)
+
+    def train(self, k: int, before=None):
+        """Train batch k; ``before(stream)`` enqueues work that must precede it on
+        the training stream (store tags, weight snapshots)."""
+        e, st = self.e, k % len(self.e.sets)
+        self.st.wait_event(self.sampled[st])
+        with torch.cuda.stream(self.st):
+            if before is not None:
+                before(self.st)
+            if e.g_train is not None:
+                e.g_train[st].replay()
+            else:
+                e.cur = st
+                e.enqueue_train_part(self.st)
+                e.cur = 0
+            ev = torch.cuda.Event()
+            ev.record(self.st)
+            self.trained[st] = ev
+
+    def drain(self):
+        torch.cuda.current_stream(self.e.device).wait_stream(self.st)
+        torch.cuda.current_stream(self.e.device).wait_stream(self.ss)
 
 
 class BatchFeeder:
@@ -462,7 +571,8 @@ class BatchFeeder:
         self.h2d_bytes = 0
 
     def feed(self, seeds: np.ndarray, rng_seed: int, reading_batch: int, batch_in_epoch: int, cpu_tag: int = -1,
-             table_sel: int = 0, cur_stamp: int = -1, warm: int = 0, n_div: int | None = None):
+             table_sel: int = 0, cur_stamp: int = -1, warm: int = 0, n_div: int | None = None,
+             set_index: int | None = None):
         k = self.k
         self.k = (k + 1) % len(self.seeds)
         if self.events[k] is not None:
@@ -475,7 +585,7 @@ class BatchFeeder:
         rs = int(rng_seed) & 0xFFFFFFFFFFFFFFFF
         self.bp[k].numpy()[:] = np.array([rs], dtype=np.uint64).view(np.int64)[0], n, reading_batch, \
             batch_in_epoch, cpu_tag, table_sel, cur_stamp, warm
-        e = self.e
+        e = self.e.sets[self.e.cur if set_index is None else set_index]
         e.seeds[:n].copy_(self.seeds[k][:n], non_blocking=True)
         e.counts_in.copy_(self.counts[k], non_blocking=True)
         e.bp.copy_(self.bp[k], non_blocking=True)

@@ -27,7 +27,7 @@ import torch
 
 from . import _lib, dense, runplan
 from .device import DeviceGraph, pad4, ptr, stream_ptr, u64_tensor
-from .engine import BatchFeeder, HotBuffers, TrainEngine
+from .engine import BatchFeeder, HotBuffers, Pipeline, TrainEngine
 from .gnnmath import init_params
 from .hotness import estimate_hotness, select_hot
 from .sampler import Fanouts, LayerSampler
@@ -231,6 +231,7 @@ class Trainer:
         self.tag_serial = 0
         self.stamp_serial = 0
         self.feeder = BatchFeeder(self.engine)
+        self.pipeline = Pipeline(self.engine)
         self.prod_stream = torch.cuda.Stream(device=dev) if config.execution == "pipelined" else None
         self.batch_to_group = {}
         if config.use_graph:
@@ -308,46 +309,73 @@ class Trainer:
         for g in range(len(plan.groups)):
             self.stamp_serial += 1
             stamps[g] = self.stamp_serial
-        prod_done = None
+        # flattened schedule: per batch its super-batch, store window parameters and
+        # producer chunk (orchestrator.py:421-545)
+        sched = []
         for g, group in enumerate(plan.groups):
             q_next_n = plan.queue_sizes.get(g + 1, 0) if self.use_hot else 0
             bounds = runplan.chunk_bounds(q_next_n, len(group)) if q_next_n else []
             cpu_tag = -1
             if self.use_hot and g > 0 and plan.queue_sizes.get(g, 0) > 0:
                 cpu_tag = self._new_tag()
-                _lib.call("hg_tag_vertices", ptr(plan.queues[g]), None, plan.queue_sizes[g], ptr(hot.cpu_tag_of),
-                          cpu_tag, stream_ptr())
-            if prod_done is not None:  # staging for this super-batch must be complete (:555-559)
-                main.wait_event(prod_done)
-                prod_done = None
             for j, b in enumerate(group):
                 gb = plan.first_global_batch + b
                 self.batch_to_group[gb] = g
-                warm = 1 if (self.layer_based and g == 0 and self.hot_list.size) else 0
-                self.feeder.feed(plan.batches[b], plan.batch_seeds[b], gb, b, cpu_tag=cpu_tag, table_sel=g % 2,
-                                 cur_stamp=stamps[g], warm=warm,
-                                 n_div=self.dist.global_batch(plan.batches[b]) if self.dist else None)
-                if bounds and bounds[j][1] > bounds[j][0]:
-                    lo, hi = bounds[j]
+                chunk = bounds[j] if (bounds and bounds[j][1] > bounds[j][0]) else None
+                sched.append(dict(g=g, j=j, b=b, gb=gb, cpu_tag=cpu_tag, first=j == 0, last=j == len(group) - 1,
+                                  chunk=chunk, warm=1 if (self.layer_based and g == 0 and self.hot_list.size) else 0))
+        pipe = self.pipeline
+        state = {"prod_done": None}
+
+        def feed_fn(it):
+            seeds = plan.batches[it["b"]]
+            return lambda set_index: self.feeder.feed(
+                seeds, plan.batch_seeds[it["b"]], it["gb"], it["b"], cpu_tag=it["cpu_tag"], table_sel=it["g"] % 2,
+                cur_stamp=stamps[it["g"]], warm=it["warm"],
+                n_div=self.dist.global_batch(seeds) if self.dist else None, set_index=set_index)
+
+        def before_fn(it):
+            def before(stream):
+                g = it["g"]
+                if it["first"]:
+                    if it["cpu_tag"] >= 0:  # cpu_set of this super-batch (orchestrator.py:447-449)
+                        _lib.call("hg_tag_vertices", ptr(plan.queues[g]), None, plan.queue_sizes[g],
+                                  ptr(hot.cpu_tag_of), it["cpu_tag"], stream.cuda_stream)
+                    if state["prod_done"] is not None:  # staging complete before use (:555-559)
+                        stream.wait_event(state["prod_done"])
+                        state["prod_done"] = None
+                if it["chunk"] is not None:
+                    lo, hi = it["chunk"]
                     c = hi - lo
-                    self.producer.snapshot(j)
-                    args = (plan.queues[g + 1][lo:hi], c, hot_seed_dev[g + 1], j, gb, stamps[g + 1], (g + 1) % 2)
+                    self.producer.snapshot(it["j"])  # _ParamCell.publish: weights before this batch
+                    args = (plan.queues[g + 1][lo:hi], c, hot_seed_dev[g + 1], it["j"], it["gb"], stamps[g + 1],
+                            (g + 1) % 2)
                     if self.prod_stream is not None:
                         ev = torch.cuda.Event()
-                        ev.record(main)
+                        ev.record(stream)
                         self.prod_stream.wait_event(ev)
                         with torch.cuda.stream(self.prod_stream):
                             self.producer.run_chunk(*args, stream=self.prod_stream)
                     else:
-                        self.producer.run_chunk(*args)
-                    rep.stage_events.append((g + 1, gb, c))
-                e.run_step()
-                self.version += 1
-            if self.prod_stream is not None and bounds:
-                prod_done = torch.cuda.Event()
-                prod_done.record(self.prod_stream)
-        if prod_done is not None:
-            main.wait_event(prod_done)
+                        self.producer.run_chunk(*args, stream=stream)
+                    rep.stage_events.append((g + 1, it["gb"], c))
+            return before
+
+        if sched:
+            pipe.sample(0, feed_fn(sched[0]))
+        for k, it in enumerate(sched):
+            if k + 1 < len(sched):
+                pipe.sample(k + 1, feed_fn(sched[k + 1]))
+            pipe.train(k, before_fn(it))
+            self.version += 1
+            if it["last"] and self.prod_stream is not None and it["g"] + 1 in plan.queue_sizes \
+                    and plan.queue_sizes.get(it["g"] + 1, 0) > 0:
+                ev = torch.cuda.Event()
+                ev.record(self.prod_stream)
+                state["prod_done"] = ev
+        pipe.drain()
+        if state["prod_done"] is not None:
+            main.wait_event(state["prod_done"])
         torch.cuda.synchronize(dev)
         rep.losses = e.loss_arr[:nb].double().cpu().tolist()
         rep.max_weight_deltas = e.md_arr[:nb].double().cpu().tolist()
@@ -405,6 +433,42 @@ class Trainer:
             ev.synchronize()
             return float(pin.item())
         return handle
+
+    def train_batches(self, batches):
+        """Public pipelined training over HOST batches [(seed ids, batch rng seed), ...]:
+        every step stages its seed ids pinned-H2D, the sample half of batch i+1
+        overlaps the train half of batch i, and each step's loss is copied D2H into
+        its own pinned slot.  Returns one handle per batch (call -> float loss)."""
+        pipe, e = self.pipeline, self.engine
+        n = len(batches)
+        pin = torch.zeros(max(n, 1), dtype=torch.float32).pin_memory()
+        v0 = self.version
+
+        def feed(i):
+            seeds, rs = batches[i]
+            n_div = self.dist.global_batch(seeds) if self.dist else None
+            return lambda set_index: self.feeder.feed(np.asarray(seeds), rs, v0 + i, 0, n_div=n_div,
+                                                      set_index=set_index)
+
+        done = torch.cuda.Event()
+        if n:
+            pipe.sample(0, feed(0))
+        for i in range(n):
+            if i + 1 < n:
+                pipe.sample(i + 1, feed(i + 1))
+            pipe.train(i)
+            with torch.cuda.stream(pipe.st):
+                pin[i:i + 1].copy_(e.d_loss, non_blocking=True)
+        done.record(pipe.st)
+        pipe.drain()
+        self.version += n
+
+        def handle(i):
+            def get():
+                done.synchronize()
+                return float(pin[i].item())
+            return get
+        return [handle(i) for i in range(n)]
 
     @property
     def d2h_bytes_per_step(self) -> int:
