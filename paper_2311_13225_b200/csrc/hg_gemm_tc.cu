@@ -131,7 +131,8 @@ __device__ __forceinline__ void split_lo16(const uint8_t* hi, uint8_t* lo) {
     *reinterpret_cast<float4*>(lo) = v;
 }
 
-constexpr int TC_THREADS = 128;
+constexpr int TC_THREADS = 256;    // wgrad CTAs
+constexpr int GEMM_THREADS = 256;  // forward / dX CTAs (8 warps: more loads and splits in flight)
 constexpr int A_TILE = 128 * 128;  // 128 rows x 32 fp32
 
 template <int BN>
@@ -163,30 +164,46 @@ __global__ void k_prep_b(const float* __restrict__ B, int ldb, int trans_b, int 
 }
 
 template <int BN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__host__ __device__ constexpr int gemm_stages() { return BN <= 64 ? 4 : (BN <= 128 ? 3 : 2); }
+template <int BN>
+__host__ __device__ constexpr int wgrad_stages() { return BN <= 64 ? 4 : (BN <= 128 ? 3 : 2); }
+
+// Persistent CTAs: CTA b walks M tiles b, b+G, ... and the flattened (tile, k)
+// iteration space streams through an S-stage cp.async ring (loads run S-1
+// iterations ahead, a stage is refilled once the MMAs that read it committed).
+// Two TMEM accumulators alternate between tiles, so the epilogue of tile t
+// (tcgen05.ld + ReLU + stores) runs while tile t+1's MMAs are in flight.
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
 k_gemm_tc(const float* __restrict__ A1, int lda1, int K1, const float* __restrict__ A2, int lda2, int K2,
           const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N,
           const int* __restrict__ d_M, int M_cap, int act) {
+    constexpr int S = gemm_stages<BN>();
     constexpr int STAGE = gemm_stage_bytes<BN>();
     constexpr int B_TILE = BN * 128;
-    constexpr uint32_t NCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    constexpr uint32_t NCOLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
     constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bars[2];
+    __shared__ uint64_t bars[S];
+    __shared__ uint64_t accbar[2];
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int M = hg_load_count(d_M, M_cap);
-    const int m0 = blockIdx.x * 128;
-    if (m0 >= M) return;
+    const int n_mt = (M + 127) >> 7;
+    if ((int)blockIdx.x >= n_mt) return;
+    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int n0 = blockIdx.y * BN;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nk1 = (K1 + 31) >> 5;
     const int nk2 = A2 ? (K2 + 31) >> 5 : 0;
     const int nk = nk1 + nk2;
+    const int iters = n_my * nk;
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+#pragma unroll
+        for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
+        mbar_init(&accbar[0], 1);
+        mbar_init(&accbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 0) tmem_alloc(&s_tmem, NCOLS);
@@ -196,15 +213,17 @@ k_gemm_tc(const float* __restrict__ A1, int lda1, int K1, const float* __restric
     const uint32_t tmem = s_tmem;
 
     const uint8_t* bimg = Bimg + (int64_t)blockIdx.y * nk * (2 * B_TILE);
-    auto load_tile = [&](int kt, int st) {
-        uint8_t* base = smem + st * STAGE;
+    auto load_iter = [&](int it) {
+        const int tile = it / nk, kt = it - tile * nk;
+        const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
+        uint8_t* base = smem + (it % S) * STAGE;
         const float* A;
         int lda, K, k0;
         if (kt < nk1) { A = A1; lda = lda1; K = K1; k0 = kt * 32; }
         else { A = A2; lda = lda2; K = K2; k0 = (kt - nk1) * 32; }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {  // A: 128 rows x 8 chunks of 16 B
-            const int q = tid + TC_THREADS * i;
+        for (int i = 0; i < 1024 / GEMM_THREADS; ++i) {  // A: 128 rows x 8 chunks of 16 B
+            const int q = tid + GEMM_THREADS * i;
             const int r = q >> 3, c = q & 7;
             const int gm = m0 + r, gk = k0 + c * 4;
             int bytes = gm < M ? (K - gk) * 4 : 0;
@@ -215,26 +234,53 @@ k_gemm_tc(const float* __restrict__ A1, int lda1, int K1, const float* __restric
         // B: the prebuilt swizzled hi|lo image of this K tile (contiguous bytes)
         const uint8_t* bsrc = bimg + (int64_t)kt * (2 * B_TILE);
         const uint32_t bdst = smem_u32(base + 2 * A_TILE);
-        for (int q = tid; q < (2 * B_TILE) / 16; q += TC_THREADS) cp_async16(bdst + q * 16, bsrc + q * 16, 16);
-        cp_async_commit();
+        for (int q = tid; q < (2 * B_TILE) / 16; q += GEMM_THREADS) cp_async16(bdst + q * 16, bsrc + q * 16, 16);
+    };
+    auto epilogue = [&](int tile) {
+        const int acc = tile & 1;
+        mbar_wait(&accbar[acc], (uint32_t)((tile >> 1) & 1));
+        tc_fence_after();
+        const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
+        // warp w reads TMEM lanes 32*(w%4).. (its rows); warps w and w+4 split the columns
+        const int gm = m0 + (warp & 3) * 32 + lane;
+        const int cbeg = (warp >> 2) * (BN / 2);
+#pragma unroll
+        for (int c0 = cbeg; c0 < cbeg + BN / 2; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+            if (gm < M) {
+                float* crow = C + (int64_t)gm * ldc + n0 + c0;
+                const int lim = N - (n0 + c0);
+                if (lim >= 16 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0)) {
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
+                        *reinterpret_cast<float4*>(crow + j) = o;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < lim) crow[j] = act ? fmaxf(v[j], 0.f) : v[j];
+                }
+            }
+        }
+        tc_fence_before();
     };
 
-    uint32_t uses0 = 0, uses1 = 0;
-    load_tile(0, 0);
-    for (int kt = 0; kt < nk; ++kt) {
-        const int st = kt & 1;
-        if (kt + 1 < nk) {
-            const int st2 = (kt + 1) & 1;
-            if (kt + 1 >= 2) mbar_wait(&bars[st2], ((st2 ? uses1 : uses0) - 1) & 1);  // MMAs of tile kt-1 done
-            load_tile(kt + 1, st2);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+#pragma unroll
+    for (int p = 0; p < S - 1; ++p) {
+        if (p < iters) load_iter(p);
+        cp_async_commit();
+    }
+    for (int it = 0; it < iters; ++it) {
+        const int st = it % S;
+        const int tile = it / nk, kt = it - tile * nk;
+        cp_async_wait<S - 2>();  // the group of iteration `it` has landed
         uint8_t* base = smem + st * STAGE;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int q = tid + TC_THREADS * i;
+        for (int i = 0; i < 1024 / GEMM_THREADS; ++i) {
+            const int q = tid + GEMM_THREADS * i;
             const uint32_t off = off_k(q >> 3, q & 7);
             split_lo16(base + off, base + A_TILE + off);
         }
@@ -242,41 +288,31 @@ k_gemm_tc(const float* __restrict__ A1, int lda1, int K1, const float* __restric
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)((tile & 1) * BN);
             const uint32_t a_hi = smem_u32(base), a_lo = a_hi + A_TILE;
             const uint32_t b_hi = a_hi + 2 * A_TILE, b_lo = b_hi + B_TILE;
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 const uint64_t dah = sdesc(a_hi + s * 32, 16, 1024), dal = sdesc(a_lo + s * 32, 16, 1024);
                 const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
-                mma_tf32(tmem, dah, dbh, IDESC, (kt | s) ? 1u : 0u);
-                mma_tf32(tmem, dah, dbl, IDESC, 1u);
-                mma_tf32(tmem, dal, dbh, IDESC, 1u);
+                mma_tf32(d, dah, dbh, IDESC, (kt | s) ? 1u : 0u);
+                mma_tf32(d, dah, dbl, IDESC, 1u);
+                mma_tf32(d, dal, dbh, IDESC, 1u);
             }
             mma_commit(&bars[st]);
+            if (kt == nk - 1) mma_commit(&accbar[tile & 1]);
         }
-        if (st) ++uses1; else ++uses0;
         __syncwarp();
+        // refill the stage consumed by iteration it-1 with iteration it+S-1
+        const int nxt = it + S - 1;
+        if (nxt < iters && it >= 1)  // use number (it-1)/S of that stage's barrier
+            mbar_wait(&bars[(it - 1) % S], (uint32_t)(((it - 1) / S) & 1));
+        if (nxt < iters) load_iter(nxt);
+        cp_async_commit();
+        // epilogue of the previous tile overlaps this tile's MMAs
+        if (kt == 0 && tile > 0) epilogue(tile - 1);
     }
-    {
-        const int st = (nk - 1) & 1;
-        mbar_wait(&bars[st], ((st ? uses1 : uses0) - 1) & 1);
-    }
-    tc_fence_after();
-    const int r = warp * 32 + lane;
-    const int gm = m0 + r;
-#pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-        if (gm < M) {
-            float* crow = C + (int64_t)gm * ldc + n0 + c0;
-            const int lim = N - (n0 + c0);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (j < lim) crow[j] = act ? fmaxf(v[j], 0.f) : v[j];
-        }
-    }
-    tc_fence_before();
+    if (iters > 0) epilogue(n_my - 1);
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, NCOLS);
 }
@@ -290,11 +326,12 @@ k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2,
            int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
     constexpr int STAGE = 2 * A_TILE + 2 * G_TILE;
+    constexpr int WS = wgrad_stages<BN>();
     constexpr uint32_t NCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
     constexpr uint32_t IDESC = idesc_tf32(128, BN, 1, 1);
     constexpr int GCH = BN / 4;  // 16-byte chunks per G row
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t bars[2];
+    __shared__ uint64_t bars[WS];
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int M = hg_load_count(d_M, M_cap);
@@ -311,8 +348,8 @@ k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2,
     const int nk = (mend - mbeg + 31) >> 5;
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+#pragma unroll
+        for (int i = 0; i < WS; ++i) mbar_init(&bars[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 0) tmem_alloc(&s_tmem, NCOLS);
@@ -325,7 +362,7 @@ k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2,
         uint8_t* base = smem + st * STAGE;
         const int r0 = mbeg + kt * 32;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {  // A: 32 rows x 32 chunks (128 k)
+        for (int i = 0; i < 1024 / TC_THREADS; ++i) {  // A: 32 rows x 32 chunks (128 k)
             const int q = tid + TC_THREADS * i;
             const int r = q >> 5, cg = q & 31;
             const int gm = r0 + r, gk = k0 + cg * 4;
@@ -346,21 +383,17 @@ k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2,
         cp_async_commit();
     };
 
-    uint32_t uses0 = 0, uses1 = 0;
-    load_tile(0, 0);
+#pragma unroll
+    for (int p = 0; p < WS - 1; ++p) {
+        if (p < nk) load_tile(p, p);
+        else cp_async_commit();
+    }
     for (int kt = 0; kt < nk; ++kt) {
-        const int st = kt & 1;
-        if (kt + 1 < nk) {
-            const int st2 = (kt + 1) & 1;
-            if (kt + 1 >= 2) mbar_wait(&bars[st2], ((st2 ? uses1 : uses0) - 1) & 1);
-            load_tile(kt + 1, st2);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        const int st = kt % WS;
+        cp_async_wait<WS - 2>();  // tile kt landed
         uint8_t* base = smem + st * STAGE;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 1024 / TC_THREADS; ++i) {
             const int q = tid + TC_THREADS * i;
             const uint32_t off = off_mn(q >> 5, q & 31);
             split_lo16(base + off, base + A_TILE + off);
@@ -386,20 +419,24 @@ k_wgrad_tc(const float* __restrict__ A1, int lda1, const float* __restrict__ A2,
             }
             mma_commit(&bars[st]);
         }
-        if (st) ++uses1; else ++uses0;
         __syncwarp();
+        const int nxt = kt + WS - 1;  // refill the stage tile kt-1 used
+        if (nxt < nk) {
+            if (kt >= 1) mbar_wait(&bars[(kt - 1) % WS], (uint32_t)(((kt - 1) / WS) & 1));
+            load_tile(nxt, nxt % WS);
+        } else {
+            cp_async_commit();
+        }
     }
-    {
-        const int st = (nk - 1) & 1;
-        mbar_wait(&bars[st], ((st ? uses1 : uses0) - 1) & 1);
-    }
+    mbar_wait(&bars[(nk - 1) % WS], (uint32_t)(((nk - 1) / WS) & 1));  // all MMAs done
     tc_fence_after();
-    const int r = warp * 32 + lane;
+    const int r = (warp & 3) * 32 + lane;  // TMEM lane quarter of this warp
     const int gk = k0 + r;
+    const int cbeg = (warp >> 2) * (BN / (TC_THREADS / 128));
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = cbeg; c0 < cbeg + BN / (TC_THREADS / 128); c0 += 16) {
         float v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0, v);
         if (gk < K) {
             float* prow = P + (int64_t)gk * N + c0;
             const int lim = N - c0;
@@ -444,13 +481,14 @@ __global__ void __launch_bounds__(256) k_wgrad_tc_reduce(const float* __restrict
 template <int BN>
 int launch_gemm(dim3 grid, cudaStream_t s, const float* A1, int lda1, int K1, const float* A2, int lda2, int K2,
                 const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int M_cap, int act) {
-    const int smem = 2 * gemm_stage_bytes<BN>() + 1024;
+    const int smem = gemm_stages<BN>() * gemm_stage_bytes<BN>() + 1024;
+    grid.x = grid.x < (unsigned)HG_NUM_SMS ? grid.x : (unsigned)HG_NUM_SMS;  // persistent: <= 1 CTA per SM
     static bool attr = false;  // idempotent; set before first launch (outside graph capture via warm-up)
     if (!attr) {
         cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_gemm_tc<BN><<<grid, TC_THREADS, smem, s>>>(A1, lda1, K1, A2, lda2, K2, bimg, C, ldc, N, d_M, M_cap, act);
+    k_gemm_tc<BN><<<grid, GEMM_THREADS, smem, s>>>(A1, lda1, K1, A2, lda2, K2, bimg, C, ldc, N, d_M, M_cap, act);
     return hg_check_launch("gemm_tc");
 }
 
@@ -462,7 +500,7 @@ int gemm_bn(int N) {
 template <int BN>
 int launch_wgrad(dim3 grid, cudaStream_t s, const float* A1, int lda1, const float* A2, int lda2, int K,
                  const float* G, int ldg, int N, const int* d_M, int M_cap, int rpc, int n_chunks, float* partial) {
-    const int smem = 2 * (2 * A_TILE + 2 * BN * 128) + 1024;
+    const int smem = wgrad_stages<BN>() * (2 * A_TILE + 2 * BN * 128) + 1024;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_wgrad_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
