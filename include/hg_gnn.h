@@ -130,6 +130,8 @@ int hg_wgrad_f32(const float* A, int32_t lda, int32_t K, const float* G, int32_t
 int64_t hg_gemm_tc_bimg_size(int32_t K1, int32_t K2, int32_t N);
 int hg_gemm_tc_prep_b(const float* B, int32_t ldb, int32_t trans_b, int32_t K1, int32_t K2, int32_t N, void* img,
                       void* stream);
+/* up to 8 images in one launch; host_desc: n rows of int64 {B, ldb, trans_b, K1, K2, N, img} */
+int hg_gemm_tc_prep_b_many(int32_t n, const int64_t* host_desc, void* stream);
 int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32_t lda2, int32_t K2,
                const void* bimg, float* C, int32_t ldc, int32_t N, const int32_t* d_M, int32_t M_cap, int32_t act,
                void* stream);

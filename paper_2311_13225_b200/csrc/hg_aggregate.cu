@@ -88,17 +88,21 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
                     else if (sg != v) { my_row = GLOBAL ? sg : sl; my_w = wd; }  // non-self edge
                 }
                 const int m = min(LPR, cnt - j0);
-                int j = 0;
-                for (; j + 4 <= m; j += 4) {
-                    int r[4]; float w[4];
+                // U rows in flight (a whole fanout-15 segment in one batch for F <= 128),
+                // consumed in edge order; slots past m are masked
+                constexpr int U = NV >= 8 ? 2 : 16 / NV;
+                for (int j = 0; j < m; j += U) {
+                    int r[U]; float w[U];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        r[t] = __shfl_sync(gmask, my_row, j + t, LPR);
-                        w[t] = __shfl_sync(gmask, my_w, j + t, LPR);
+                    for (int t = 0; t < U; ++t) {
+                        const int src = j + t < LPR ? j + t : LPR - 1;
+                        const int rr = __shfl_sync(gmask, my_row, src, LPR);
+                        w[t] = __shfl_sync(gmask, my_w, src, LPR);
+                        r[t] = j + t < m ? rr : -1;
                     }
-                    float4 x[4][NV];
+                    float4 x[U][NV];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
+                    for (int t = 0; t < U; ++t) {
                         const float4* rp = reinterpret_cast<const float4*>(hin + (int64_t)(r[t] < 0 ? 0 : r[t]) * ld_in);
 #pragma unroll
                         for (int k = 0; k < NV; ++k) {
@@ -107,23 +111,11 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
                         }
                     }
 #pragma unroll
-                    for (int t = 0; t < 4; ++t)
+                    for (int t = 0; t < U; ++t)
                         if (r[t] >= 0) {
 #pragma unroll
                             for (int k = 0; k < NV; ++k) acc[k] = f4_fma(w[t], x[t][k], acc[k]);
                         }
-                }
-                for (; j < m; ++j) {
-                    const int r = __shfl_sync(gmask, my_row, j, LPR);
-                    const float w = __shfl_sync(gmask, my_w, j, LPR);
-                    if (r >= 0) {
-                        const float4* rp = reinterpret_cast<const float4*>(hin + (int64_t)r * ld_in);
-#pragma unroll
-                        for (int k = 0; k < NV; ++k) {
-                            const int c = lr + k * LPR;
-                            if (c < F4) acc[k] = f4_fma(w, __ldg(rp + c), acc[k]);
-                        }
-                    }
                 }
             }
         } else if (GLOBAL && self_out) {

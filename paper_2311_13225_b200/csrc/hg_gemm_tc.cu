@@ -139,6 +139,41 @@ template <int BN>
 __host__ __device__ constexpr int gemm_stage_bytes() { return 2 * A_TILE + 2 * BN * 128; }
 
 // ---------------------------------------------------------------------------
+// Several B images in one launch (blockIdx.z = image): the per-step rebuild of
+// every layer's forward / dX images costs one kernel node instead of five.
+struct PrepDesc {
+    const float* B;
+    uint8_t* img;
+    int ldb, trans_b, K1, K2, N, bn, nk1, nk, nnt;
+};
+constexpr int MAX_PREP = 8;
+struct PrepBatch {
+    PrepDesc d[MAX_PREP];
+};
+
+__global__ void k_prep_b_many(const __grid_constant__ PrepBatch pb) {
+    const PrepDesc& d = pb.d[blockIdx.z];
+    const int kt = blockIdx.x, nt = blockIdx.y;
+    if (kt >= d.nk || nt >= d.nnt) return;
+    const int BN = d.bn;
+    uint8_t* base = d.img + ((int64_t)nt * d.nk + kt) * (2 * BN * 128);
+    const int K = kt < d.nk1 ? d.K1 : d.K2;
+    const int k0 = kt < d.nk1 ? kt * 32 : (kt - d.nk1) * 32;
+    const int kb = kt < d.nk1 ? k0 : d.K1 + k0;
+    for (int e = threadIdx.x; e < BN * 32; e += blockDim.x) {
+        int n, k;
+        if (d.trans_b) { k = e / BN; n = e - k * BN; }
+        else { n = e >> 5; k = e & 31; }
+        const int gn = nt * BN + n, gk = k0 + k;
+        float v = 0.f;
+        if (gn < d.N && gk < K)
+            v = d.trans_b ? d.B[(int64_t)(kb + k) * d.ldb + gn] : d.B[(int64_t)gn * d.ldb + kb + k];
+        const uint32_t off = off_k(n, k >> 2) + (k & 3) * 4;
+        *reinterpret_cast<float*>(base + off) = v;
+        *reinterpret_cast<float*>(base + BN * 128 + off) = tf32_lo(v);
+    }
+}
+
 // B image: for every (N tile, K tile) the exact swizzled smem bytes of the
 // operand tile, hi then lo (2 * BN * 128 bytes), so CTAs stage B with plain
 // 16-byte cp.async copies.  Built once per weight update by k_prep_b.
@@ -552,6 +587,34 @@ extern "C" int hg_gemm_tc_prep_b(const float* B, int32_t ldb, int32_t trans_b, i
         default: k_prep_b<256><<<g, 256, 0, s>>>(B, ldb, trans_b, K1, K2, N, nk1, nk, p); break;
     }
     return hg_check_launch("gemm_tc_prep_b");
+}
+
+// Batched hg_gemm_tc_prep_b: host_desc holds n rows of 7 int64
+// (B, ldb, trans_b, K1, K2, N, img); n <= 8.
+extern "C" int hg_gemm_tc_prep_b_many(int32_t n, const int64_t* host_desc, void* stream) {
+    if (n <= 0) return HG_OK;
+    if (n > MAX_PREP) { hg_set_error("gemm_tc_prep_b_many: at most %d images", MAX_PREP); return HG_EINVAL; }
+    PrepBatch pb{};
+    int gx = 1, gy = 1;
+    for (int i = 0; i < n; ++i) {
+        const int64_t* r = host_desc + 7 * i;
+        PrepDesc& d = pb.d[i];
+        d.B = reinterpret_cast<const float*>(r[0]);
+        d.ldb = (int)r[1];
+        d.trans_b = (int)r[2];
+        d.K1 = (int)r[3];
+        d.K2 = (int)r[4];
+        d.N = (int)r[5];
+        d.img = reinterpret_cast<uint8_t*>(r[6]);
+        d.bn = gemm_bn(d.N);
+        d.nk1 = hg_ceil_div(d.K1, 32);
+        d.nk = d.nk1 + (d.K2 > 0 ? hg_ceil_div(d.K2, 32) : 0);
+        d.nnt = hg_ceil_div(d.N, d.bn);
+        gx = d.nk > gx ? d.nk : gx;
+        gy = d.nnt > gy ? d.nnt : gy;
+    }
+    k_prep_b_many<<<dim3(gx, gy, n), 256, 0, (cudaStream_t)stream>>>(pb);
+    return hg_check_launch("gemm_tc_prep_b_many");
 }
 
 // C[M x N] = act(A1[M x K1] op(B)[0:K1] + A2[M x K2] op(B)[K1:K1+K2]) with the

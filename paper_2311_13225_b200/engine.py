@@ -242,12 +242,25 @@ class TrainEngine:
         self.enqueue_weight_images()
 
     def enqueue_weight_images(self, stream=None):
+        """Rebuild every tensor-core B image from the current weights (one launch)."""
         s = stream_ptr(stream)
         P = self.params
+        jobs = []
         for l in range(self.L):
-            self.img_fwd[l].prep(ptr(P.view(l, 0)), self.dims[l + 1], s)
+            jobs.append((self.img_fwd[l], ptr(P.view(l, 0))))
             for m, img in enumerate(self.img_dx[l]):
-                img.prep(ptr(P.view(l, m)), self.dims[l + 1], s)
+                jobs.append((img, ptr(P.view(l, m))))
+        if dense.BACKEND == "simt":
+            return
+        for i in range(0, len(jobs), 8):
+            part = jobs[i:i + 8]
+            desc = np.array([[w, self._ldb_of(img), img.trans_b, img.K1, img.K2, img.N, img.buf.data_ptr()]
+                             for img, w in part], dtype=np.int64)
+            _lib.call("hg_gemm_tc_prep_b_many", len(part), desc.ctypes.data, s)
+
+    def _ldb_of(self, img):
+        """Row stride of the weight matrix an image is built from."""
+        return img.N if img.trans_b else img.K1
 
     # ------------------------------------------------------------------
     def frontier(self, l):
