@@ -202,12 +202,18 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phases", action="store_true", help="also report a per-phase time breakdown")
+    ap.add_argument("--epoch-mode", default=None, metavar="SPEC",
+                    help="extra measurement (not the driver's line): whole epochs through Trainer.run_epoch, "
+                         "SPEC = 'c2:sage:hot=0.2:n=4' or 'c3:gcn:hot=0.2:n=4:fan=4,4:bs=10000'")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.epoch_mode:
+        run_epoch_mode(args.epoch_mode)
         return
 
     import torch
@@ -405,6 +411,51 @@ def main():
     if phases:
         line["phases_ms"] = phases
     print(json.dumps(line), flush=True)
+
+
+def run_epoch_mode(spec: str):
+    """Whole training epochs (hot-embedding schedule included: queue replay,
+    producer stream, store lookups/injection) through Trainer.run_epoch; reports
+    seeds/s of the timed epoch, reuse statistics and full-graph accuracy."""
+    import torch
+    from paper_2311_13225_b200.datagen import make_dataset
+    from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer, evaluate
+    parts = spec.split(":")
+    opts = dict(p.split("=", 1) for p in parts[2:] if "=" in p)
+    name, model = parts[0], parts[1]
+    fan = tuple(int(x) for x in opts.get("fan", "15,10,5").split(","))
+    hot = float(opts.get("hot", 0.0))
+    cfg = TrainConfig(model=model, layers=len(fan), fanouts=fan, hidden_dim=int(opts.get("hidden", 64 if name != "c3" else 256)),
+                      batch_size=int(opts.get("bs", 1024)), lr=float(opts.get("lr", 0.01)),
+                      strategy="layer-based" if hot > 0 else "case1", hot_ratio=hot,
+                      super_batch_n=int(opts.get("n", 4)), presample_rounds=int(opts.get("rounds", 2)),
+                      execution=opts.get("exec", "pipelined"), seed=0, use_graph=True)
+    ds = make_dataset(name, cache_dir=CACHE)
+    t0 = time.perf_counter()
+    tr = Trainer(ds, cfg)
+    setup_s = time.perf_counter() - t0
+    res = []
+    first = 0
+    for epoch in range(int(opts.get("epochs", 2))):
+        plan = tr.build_epoch_plan(epoch, first)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        ev0.record()
+        rep = tr.run_epoch(plan)
+        ev1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        n_seeds = sum(b.shape[0] for b in plan.batches)
+        res.append({"epoch": epoch, "batches": len(plan.batches), "seeds_per_s": n_seeds / wall,
+                    "gpu_ms": ev0.elapsed_time(ev1), "wall_s": wall, "reuse_hits": rep.reuse_hits,
+                    "fallbacks": rep.fallbacks, "max_gap": rep.max_gap, "first_loss": rep.losses[0],
+                    "last_loss": rep.losses[-1]})
+        first += len(plan.batches)
+    acc = evaluate(tr)
+    print(json.dumps({"mode": "epoch", "spec": spec, "config": cfg.to_dict(), "vertices": ds.num_vertices,
+                      "edges": ds.num_edges, "hot_list": int(tr.hot_list.shape[0]), "setup_s": setup_s,
+                      "epochs": res, "val_accuracy": acc["val"], "test_accuracy": acc["test"]}), flush=True)
 
 
 def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):

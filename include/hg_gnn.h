@@ -112,7 +112,13 @@ int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const fl
                      const int32_t* counts, const int32_t* slot_g, const int32_t* nself, const int32_t* outdeg,
                      const int32_t* csc_slot, const int32_t* seg_beg, const int32_t* seg_end,
                      const int32_t* d_n_src, int32_t cap_src, const float* hmask, int32_t ld_hmask,
-                     const uint8_t* inj_mask, float* dx, int32_t ld_dx, void* stream);
+                     const uint8_t* inj_mask, float* dx, int32_t ld_dx, const int32_t* csc_dst,
+                     const float* csc_w, void* stream);
+/* per sorted transposed edge: (dst, weight), dst = -1 for empty slots / SAGE self edges;
+ * optional input of hg_aggregate_bwd (csc_dst/csc_w NULL => derived on the fly) */
+int hg_csc_weights(int32_t model, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
+                   const int32_t* frontier, const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself,
+                   const int32_t* outdeg, const int32_t* csc_slot, int32_t* csc_dst, float* csc_w, void* stream);
 
 /* ---- K8 dense transforms (gnnmath.py:121,135,139,173,190-198) ---------- */
 int hg_gemm_f32(const float* A1, int32_t lda1, int32_t K1, const float* B1, int32_t ldb1, const float* A2,

@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(256) k_agg_bwd(
     const int* __restrict__ slot_g, const int* __restrict__ nself, const int* __restrict__ outdeg,
     const int* __restrict__ csc_slot, const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
     const int* d_n_src, int cap_src, const float* __restrict__ hmask, int ld_hmask,
-    const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx) {
+    const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx, const int* __restrict__ csc_dst,
+    const float* __restrict__ csc_w) {
     const int n_src = hg_load_count(d_n_src, cap_src);
     const int n_dst = hg_load_count(d_n_dst, cap_dst);
     const int lane = threadIdx.x & 31;
@@ -161,10 +162,15 @@ __global__ void __launch_bounds__(256) k_agg_bwd(
             int my_row = -1;
             float my_w = 0.f;
             if (j0 + lr < end) {
-                const int e = csc_slot[j0 + lr];
-                const int d = e / f;
-                if (GCN) { my_row = d; my_w = gcn_w(outdeg[s], counts[d]); }
-                else if (slot_g[e] != frontier[d]) { my_row = d; my_w = 1.0f / (float)nself[d]; }
+                if (csc_dst) {  // precomputed (dst, weight) of the sorted edge (hg_csc_weights)
+                    my_row = csc_dst[j0 + lr];
+                    my_w = csc_w[j0 + lr];
+                } else {
+                    const int e = csc_slot[j0 + lr];
+                    const int d = e / f;
+                    if (GCN) { my_row = d; my_w = gcn_w(outdeg[s], counts[d]); }
+                    else if (slot_g[e] != frontier[d]) { my_row = d; my_w = 1.0f / (float)nself[d]; }
+                }
             }
             const int m = min(LPR, end - j0);
             int j = 0;
@@ -290,12 +296,13 @@ int launch_bwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* dagg, int l
                int ld_dself, int F4, const int* frontier, const int* d_n_dst, int cap_dst, int f, const int* counts,
                const int* slot_g, const int* nself, const int* outdeg, const int* csc_slot, const int* seg_beg,
                const int* seg_end, const int* d_n_src, int cap_src, const float* hmask, int ld_hmask,
-               const uint8_t* inj, float* dx, int ld_dx) {
+               const uint8_t* inj, float* dx, int ld_dx, const int* csc_dst, const float* csc_w) {
 #define HG_BWD(L, V)                                                                                            \
     if (LPR == L && NV == V) {                                                                                  \
         k_agg_bwd<L, V, GCN><<<g, 256, 0, s>>>(dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, \
                                                f, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end,    \
-                                               d_n_src, cap_src, hmask, ld_hmask, inj, dx, ld_dx);              \
+                                               d_n_src, cap_src, hmask, ld_hmask, inj, dx, ld_dx, csc_dst,      \
+                                               csc_w);                                                          \
         return HG_OK;                                                                                           \
     }
     HG_BWD(8, 1) HG_BWD(16, 1) HG_BWD(32, 1) HG_BWD(32, 2) HG_BWD(32, 4) HG_BWD(32, 8)
@@ -352,7 +359,7 @@ extern "C" int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dag
                                 const int32_t* nself, const int32_t* outdeg, const int32_t* csc_slot,
                                 const int32_t* seg_beg, const int32_t* seg_end, const int32_t* d_n_src,
                                 int32_t cap_src, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
-                                float* dx, int32_t ld_dx, void* stream) {
+                                float* dx, int32_t ld_dx, const int32_t* csc_dst, const float* csc_w, void* stream) {
     if (F % 4 || ld_dagg % 4 || ld_dx % 4) { hg_set_error("aggregate_bwd: widths must be multiples of 4"); return HG_EINVAL; }
     if (F > 1024) { hg_set_error("aggregate_bwd: F > 1024 unsupported"); return HG_EUNSUPPORTED; }
     if (cap_src == 0) return HG_OK;
@@ -361,10 +368,48 @@ extern "C" int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dag
     pick_lanes(F4, LPR, NV);
     dim3 g(hg_grid((long long)cap_src * LPR, 256, 8));
     cudaStream_t s = (cudaStream_t)stream;
-    int rc = model ? launch_bwd<true>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx)
-                   : launch_bwd<false>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx);
+    int rc = model ? launch_bwd<true>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx, csc_dst, csc_w)
+                   : launch_bwd<false>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx, csc_dst, csc_w);
     if (rc) { hg_set_error("aggregate_bwd: unsupported width"); return rc; }
     return hg_check_launch("aggregate_bwd");
+}
+
+namespace {
+// (dst, weight) of every sorted transposed edge: the backward gather then needs
+// one dependent load per edge instead of three (built off the critical path).
+// Empty slots and SAGE self edges get dst = -1.
+__global__ void k_csc_weights(int model, const int* d_n_dst, int cap_dst, int f, const int* __restrict__ counts,
+                              const int* __restrict__ frontier, const int* __restrict__ slot_g,
+                              const int* __restrict__ slot_local, const int* __restrict__ nself,
+                              const int* __restrict__ outdeg, const int* __restrict__ csc_slot,
+                              int* __restrict__ csc_dst, float* __restrict__ csc_w) {
+    const int n = hg_load_count(d_n_dst, cap_dst);
+    const long long Q = (long long)cap_dst * f;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < Q; k += (long long)gridDim.x * blockDim.x) {
+        const int e = csc_slot[k];
+        const int d = e / f, j = e - d * f;
+        int dst = -1;
+        float w = 0.f;
+        if (d < n && j < counts[d]) {
+            if (model) { dst = d; w = gcn_w(outdeg[slot_local[e]], counts[d]); }
+            else if (slot_g[e] != frontier[d]) { dst = d; w = 1.0f / (float)nself[d]; }
+        }
+        csc_dst[k] = dst;
+        csc_w[k] = w;
+    }
+}
+}  // namespace
+
+extern "C" int hg_csc_weights(int32_t model, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                              const int32_t* counts, const int32_t* frontier, const int32_t* slot_g,
+                              const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg,
+                              const int32_t* csc_slot, int32_t* csc_dst, float* csc_w, void* stream) {
+    const long long Q = (long long)cap_dst * fanout;
+    if (Q <= 0) return HG_OK;
+    k_csc_weights<<<hg_grid(Q, 256, 8), 256, 0, (cudaStream_t)stream>>>(model, d_n_dst, cap_dst, fanout, counts,
+                                                                       frontier, slot_g, slot_local, nself, outdeg,
+                                                                       csc_slot, csc_dst, csc_w);
+    return hg_check_launch("csc_weights");
 }
 
 extern "C" int64_t hg_swr_ws_size(int64_t n_edges, int32_t n_out) {

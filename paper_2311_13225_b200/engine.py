@@ -297,7 +297,7 @@ class TrainEngine:
             self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False)
             if l > 0:
                 sc.wait_stream(main)
-                self.samplers[l].build_csc(n, sc)
+                self.samplers[l].build_csc(n, sc, frontier=fr)
         if self.L > 1:
             main.wait_stream(sc)
 
@@ -381,10 +381,11 @@ class TrainEngine:
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dagg[l]),
                          self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
                 dsp, dsl, dap, dal = None, 0, ptr(self.dagg[l]), self.ld[l]
-            _lib.call("hg_aggregate_bwd", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n), self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots),
-                      ptr(smp.nself), ptr(smp.outdeg), ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end),
-                      ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]), self.ld[l],
-                      ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]), self.ld[l], s)
+            _lib.call("hg_aggregate_bwd", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n), self.cap_dst[l],
+                      self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.nself), ptr(smp.outdeg),
+                      ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end), ptr(smp.n_src), self.cap_src[l],
+                      ptr(self.out[l - 1]), self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]),
+                      self.ld[l], ptr(smp.csc_dst), ptr(smp.csc_w), s)
         # ---------------- update ----------------
         mark("update")
         if self.allreduce is not None:

@@ -261,7 +261,8 @@ def backward_batch(caches, dlogits, params: ModelParams):
         _lib.call("hg_aggregate_bwd", code, ptr(dagg), ld_in, ptr(dself), ld_in, ld_in, ptr(db.dst), ptr(db.d_n_dst),
                   db.n_dst, db.f, ptr(db.counts), ptr(db.slot_g), ptr(db.nself), ptr(db.outdeg), ptr(db.csc_slot),
                   ptr(db.seg_beg), ptr(db.seg_end), ptr(db.d_n_src), db.n_src,
-                  ptr(below.out) if below.activation else None, ld_in, ptr(below.inj_dev), ptr(dx), ld_in, s)
+                  ptr(below.out) if below.activation else None, ld_in, ptr(below.inj_dev), ptr(dx), ld_in, None,
+                  None, s)
         d = dx
     return grads
 

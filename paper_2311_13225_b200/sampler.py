@@ -135,6 +135,8 @@ class LayerSampler:
             self.seg_beg = z(self.cap_src)
             self.seg_end = z(self.cap_src)
             self.csc_ws = z(lib.hg_csc_ws_size(self.cap_dst, self.f))
+            self.csc_dst = z(cap_dst * self.f)
+            self.csc_w = torch.zeros(max(cap_dst * self.f, 1), dtype=torch.float32, device=dev)
 
     def run(self, frontier, d_n_dst, d_seed, layer: int, stream=None, cap_dst: int | None = None,
             with_csc: bool = True):
@@ -157,11 +159,19 @@ class LayerSampler:
             self.build_csc(d_n_dst, stream, cap)
         return self
 
-    def build_csc(self, d_n_dst, stream=None, cap_dst: int | None = None):
+    def build_csc(self, d_n_dst, stream=None, cap_dst: int | None = None, frontier=None):
+        """Stable src-major view; with ``frontier`` also the per-edge (dst, weight)
+        table the backward gather reads (SAGE if nself is tracked, else GCN)."""
         cap = self.cap_dst if cap_dst is None else int(cap_dst)
         cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
+        s = stream_ptr(stream)
         _lib.call("hg_build_csc", ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slot_local), cap_src,
-                  ptr(self.csc_slot), ptr(self.seg_beg), ptr(self.seg_end), ptr(self.csc_ws), stream_ptr(stream))
+                  ptr(self.csc_slot), ptr(self.seg_beg), ptr(self.seg_end), ptr(self.csc_ws), s)
+        if frontier is not None:
+            model = 0 if self.nself is not None else 1
+            _lib.call("hg_csc_weights", model, ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(frontier),
+                      ptr(self.slots), ptr(self.slot_local), ptr(self.nself), ptr(self.outdeg), ptr(self.csc_slot),
+                      ptr(self.csc_dst), ptr(self.csc_w), s)
 
     # -- host views (sync) ---------------------------------------------------
     def to_block(self, frontier_np: np.ndarray, stream=None) -> Block:
