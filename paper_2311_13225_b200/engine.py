@@ -352,18 +352,23 @@ class TrainEngine:
                   ptr(self.d_loss), ptr(self.row_loss), s)
         # ---------------- backward ----------------
         mark("bwd")
+        # weight gradients of layer l only need dz[l]: they run on a side stream (a
+        # parallel graph branch) while dX of layer l and everything below proceed
+        sw = self.side[0]
         for l in range(L - 1, -1, -1):
             smp = self.samplers[l]
             fr, n = self.frontier(l)
             d_in, d_out = self.dims[l], self.dims[l + 1]
+            sw.wait_stream(main)
+            ws_ = sw.cuda_stream
             if self.sage:  # dW_self = h_self^T dz, dW_neigh = mean^T dz (gnnmath.py:190-191)
                 a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
                 dense.wgrad(ptr(a1), lda1, ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1],
                             d_out, ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), ptr(P.view(l, 1, P.grad)),
-                            ptr(self.wgrad_ws), s)
+                            ptr(self.wgrad_ws), ws_)
             else:  # dW = agg^T dz (gnnmath.py:135)
                 dense.wgrad(ptr(self.agg[l]), self.ld[l], None, 0, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
-                            ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), s)
+                            ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), ws_)
             if l == 0:
                 continue
             if self.fused_dx[l]:  # [dself | dmean] = dz [W_self; W_neigh]^T in one GEMM
@@ -386,6 +391,7 @@ class TrainEngine:
                       ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end), ptr(smp.n_src), self.cap_src[l],
                       ptr(self.out[l - 1]), self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]),
                       self.ld[l], ptr(smp.csc_dst), ptr(smp.csc_w), s)
+        main.wait_stream(sw)
         # ---------------- update ----------------
         mark("update")
         if self.allreduce is not None:
