@@ -48,12 +48,17 @@ uint64_t hg_derive_seed(uint64_t seed, const uint64_t* host_parts, int n_parts);
  *      stream is derive_seed(seed, 0x5A, layer) (sampler.py:143); layer < 0:
  *      *d_seed is the stream seed itself.  Writes counts[i] = min(deg, f) and
  *      the drawn global ids into slots[i*f + j] (emission order), and
- *      atomicMin's first-occurrence positions into minpos[V] (all INT32_MAX at
- *      rest).  scratch: cap_dst*2*fanout ints, used only when fanout > 32. */
+ *      atomicMin's (tag << 32 | position) into the first-occurrence table
+ *      minpos[V] (all ~0 when allocated, never reset; tag = 0xFFFFFFFE -
+ *      *tag_ctr).  scratch: cap_dst*2*fanout ints, used only when fanout > 32. */
 int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
                     const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
-                    int32_t layer, int32_t* counts, int32_t* slots, int32_t* minpos, int32_t* scratch,
-                    void* stream);
+                    int32_t layer, int32_t* counts, int32_t* slots, uint64_t* minpos, int32_t* tag_ctr,
+                    int32_t* scratch, void* stream);
+
+/* Retires the current first-occurrence tag after a draw that is not followed
+ * by hg_dedup_relabel (which retires it itself). */
+int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream);
 
 /* ---- K2/K3 dedup + relabel + (dst, src) order: kernels.py:166-180
  *      (stable_unique) and sampler.py:104-118 (_expand_frontier lexsort).
@@ -61,11 +66,11 @@ int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_
  *      *d_n_src, slots re-ordered by local src id with slot_local, per-dst
  *      non-self counts `nself` (gnnmath.py:145-154; nullable) and block
  *      out-degrees `outdeg` (gnnmath.py:96; nullable, zeroed by caller), and
- *      restores minpos. */
+ *      bumps *tag_ctr so the next use of minpos starts clean. */
 int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout);
 int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                     const int32_t* counts, int32_t* slots, int32_t* slot_local, int32_t* minpos,
-                     int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
+                     const int32_t* counts, int32_t* slots, int32_t* slot_local, const uint64_t* minpos,
+                     int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
                      int32_t* outdeg, int32_t* ws, void* stream);
 
 /* Block.edge_src / edge_dst (sampler.py:45-78) from the slot form. */

@@ -21,14 +21,20 @@
 // "last writer" table, pointer jumping and __match_any_sync (see k_sample_seg).
 //
 // Dedup: positions follow the reference's emission order (frontier first,
-// then draws in (dst, draw) order).  A dense int32 minpos[V] table (all
-// INT_MAX at rest) receives atomicMin(position) for every emitted id; an id's
-// first occurrence is the position that won.  The table is restored by
-// k_reset_minpos, touching only the ids of this block.
+// then draws in (dst, draw) order).  A dense uint64 first-occurrence table
+// minpos[V] receives atomicMin((tag << 32) | position) for every emitted id; an
+// id's first occurrence is the position that won.  The tag decreases with every
+// use of the table (a device counter bumped by the relabel kernel), so entries
+// left by earlier blocks always lose and the table never needs resetting.
 #include "hg_common.cuh"
 #include "hg_gnn_internal.h"
 
 namespace {
+
+__device__ __forceinline__ uint32_t fo_tag(const int* ctr) { return 0xFFFFFFFEu - (uint32_t)(*ctr); }
+__device__ __forceinline__ unsigned long long fo_key(uint32_t tag, long long pos) {
+    return ((unsigned long long)tag << 32) | (unsigned long long)(uint32_t)pos;
+}
 
 // --------------------------------------------------------------------------
 // draw kernel, fanout <= 32: one W-lane segment per destination
@@ -39,9 +45,11 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
                                                     const int* __restrict__ frontier, const int* d_n,
                                                     int cap, int f, const uint64_t* __restrict__ d_seed,
                                                     int layer, int* __restrict__ counts,
-                                                    int* __restrict__ slots, int* __restrict__ minpos) {
+                                                    int* __restrict__ slots, unsigned long long* __restrict__ minpos,
+                                                    const int* __restrict__ tag_ctr) {
     __shared__ int s_last[256];
     const int n = hg_load_count(d_n, cap);
+    const uint32_t tag = fo_tag(tag_ctr);
     const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
     const uint64_t base = hg_mix64(stream + HG_GOLDEN);  // kernels.py:153
     const int lane = threadIdx.x & 31;
@@ -54,7 +62,7 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
         const int i = i0 + threadIdx.x / W;
         if (i >= n) continue;  // segment-uniform
         const int v = frontier[i];
-        if (sub == 0) atomicMin(&minpos[v], i);  // frontier position i
+        if (sub == 0) atomicMin(&minpos[v], fo_key(tag, i));  // frontier position i
         const int64_t off = offsets[v];
         const int64_t deg = offsets[v + 1] - off;
         const int cnt = deg < f ? (int)deg : f;
@@ -90,7 +98,7 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
         }
         if (sub < cnt) {
             slots[(int64_t)i * f + sub] = u;
-            atomicMin(&minpos[u], n + i * f + sub);
+            atomicMin(&minpos[u], fo_key(tag, (long long)n + (long long)i * f + sub));
         }
     }
 }
@@ -102,13 +110,15 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
 __global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __restrict__ targets,
                              const int* __restrict__ frontier, const int* d_n, int cap, int f,
                              const uint64_t* __restrict__ d_seed, int layer, int* __restrict__ counts,
-                             int* __restrict__ slots, int* __restrict__ minpos, int* __restrict__ scratch) {
+                             int* __restrict__ slots, unsigned long long* __restrict__ minpos,
+                             const int* __restrict__ tag_ctr, int* __restrict__ scratch) {
     const int n = hg_load_count(d_n, cap);
+    const uint32_t tag = fo_tag(tag_ctr);
     const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
     const uint64_t base = hg_mix64(stream + HG_GOLDEN);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int v = frontier[i];
-        atomicMin(&minpos[v], i);
+        atomicMin(&minpos[v], fo_key(tag, i));
         const int64_t off = offsets[v];
         const int64_t deg = offsets[v + 1] - off;
         const int cnt = deg < f ? (int)deg : f;
@@ -138,7 +148,7 @@ __global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __r
                 sp[j] = targets[off + vp];
             }
         }
-        for (int j = 0; j < cnt; ++j) atomicMin(&minpos[sp[j]], n + i * f + j);
+        for (int j = 0; j < cnt; ++j) atomicMin(&minpos[sp[j]], fo_key(tag, (long long)n + (long long)i * f + j));
     }
 }
 
@@ -182,13 +192,15 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__ frontier, const int* d_n, int cap,
                                                          int f, const int* __restrict__ counts,
                                                          const int* __restrict__ slots,
-                                                         const int* __restrict__ minpos, int* __restrict__ rank,
+                                                         const unsigned long long* __restrict__ minpos,
+                                                         const int* __restrict__ tag_ctr, int* __restrict__ rank,
                                                          int* __restrict__ src_vertices, int* __restrict__ d_n_src,
                                                          unsigned long long* __restrict__ status,
                                                          const int* __restrict__ d_gen) {
     __shared__ int s_warp[MS_THREADS / 32];
     __shared__ int s_prefix;
     const int n = hg_load_count(d_n, cap);
+    const uint32_t tag = fo_tag(tag_ctr);
     const long long P = (long long)n * (f + 1);
     const int t = blockIdx.x;
     const long long p0 = (long long)t * MS_TILE;
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
     for (int k = 0; k < MS_ITEMS; ++k) {
         const long long p = my0 + k;
         int x = -1;
-        if (p < P && pos_item(p, n, f, frontier, counts, slots, x) && minpos[x] == (int)p) {
+        if (p < P && pos_item(p, n, f, frontier, counts, slots, x) && minpos[x] == fo_key(tag, p)) {
             flags |= 1u << k;
             ++cnt;
         }
@@ -285,10 +297,15 @@ template <int W>
 __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict__ frontier, const int* d_n,
                                                           int cap, int f, const int* __restrict__ counts,
                                                           int* __restrict__ slots, int* __restrict__ slot_local,
-                                                          const int* __restrict__ minpos,
+                                                          const unsigned long long* __restrict__ minpos,
                                                           const int* __restrict__ rank,
-                                                          int* __restrict__ nself, int* __restrict__ outdeg) {
+                                                          int* __restrict__ nself, int* __restrict__ outdeg,
+                                                          int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
     const int n = hg_load_count(d_n, cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // retire this use of the table and of the scan status
+        *tag_ctr += 1;
+        *d_gen += 1;
+    }
     const int lane = threadIdx.x & 31;
     const int sub = lane & (W - 1);
     const int seg0 = lane & ~(W - 1);
@@ -302,7 +319,7 @@ __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict_
         int u = -1, loc = HG_INT_MAX;
         if (sub < cnt) {
             u = slots[(int64_t)i * f + sub];
-            loc = rank[minpos[u]];
+            loc = rank[(uint32_t)minpos[u]];
         }
         int r = 0;
         for (int k = 0; k < cnt; ++k) {
@@ -322,10 +339,14 @@ __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict_
 
 __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* d_n, int cap, int f,
                                    const int* __restrict__ counts, int* __restrict__ slots,
-                                   int* __restrict__ slot_local, const int* __restrict__ minpos,
+                                   int* __restrict__ slot_local, const unsigned long long* __restrict__ minpos,
                                    const int* __restrict__ rank, int* __restrict__ nself,
-                                   int* __restrict__ outdeg) {
+                                   int* __restrict__ outdeg, int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
     const int n = hg_load_count(d_n, cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *tag_ctr += 1;
+        *d_gen += 1;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int cnt = counts[i];
         const int v = frontier[i];
@@ -333,7 +354,7 @@ __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* 
         int* lp = slot_local + (int64_t)i * f;
         int ns = 0;
         for (int j = 0; j < cnt; ++j) {
-            lp[j] = rank[minpos[sp[j]]];
+            lp[j] = rank[(uint32_t)minpos[sp[j]]];
             ns += sp[j] != v;
         }
         for (int j = 1; j < cnt; ++j) {  // stable insertion sort by local id
@@ -347,13 +368,7 @@ __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* 
     }
 }
 
-__global__ void k_reset_minpos(const int* __restrict__ src_vertices, const int* d_n_src, int cap,
-                               int* __restrict__ minpos, int* __restrict__ d_gen) {
-    const int n = hg_load_count(d_n_src, cap);
-    if (d_gen && blockIdx.x == 0 && threadIdx.x == 0) *d_gen += 1;  // next k_markscan generation
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-        minpos[src_vertices[k]] = HG_INT_MAX;
-}
+__global__ void k_fo_advance(int* __restrict__ tag_ctr) { *tag_ctr += 1; }
 
 // compacted edges (Block.edge_src / edge_dst) from the slot form; starts =
 // exclusive scan of counts
@@ -429,7 +444,7 @@ int seg_width(int f) { return f <= 4 ? 4 : f <= 8 ? 8 : f <= 16 ? 16 : 32; }
 extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
                                const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
                                const uint64_t* d_seed, int32_t layer, int32_t* counts, int32_t* slots,
-                               int32_t* minpos, int32_t* scratch, void* stream) {
+                               uint64_t* minpos, int32_t* tag_ctr, int32_t* scratch, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (fanout < 1 || cap_dst < 0) { hg_set_error("sample_layer: bad fanout/cap"); return HG_EINVAL; }
     if ((long long)cap_dst * (fanout + 1) >= 0x7fffffffLL) { hg_set_error("sample_layer: cap too large"); return HG_EINVAL; }
@@ -438,23 +453,30 @@ extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, c
         const int W = seg_width(fanout);
         const int grid = hg_grid((long long)cap_dst * W, 256, 8);
         switch (W) {
-            case 4: k_sample_seg<4><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
-            case 8: k_sample_seg<8><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
-            case 16: k_sample_seg<16><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
-            default: k_sample_seg<32><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, minpos); break;
+            case 4: k_sample_seg<4><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            case 8: k_sample_seg<8><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            case 16: k_sample_seg<16><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            default: k_sample_seg<32><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
         }
     } else {
         if (!scratch) { hg_set_error("sample_layer: fanout > 32 needs scratch"); return HG_EINVAL; }
         k_sample_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout,
-                                                              d_seed, layer, counts, slots, minpos, scratch);
+                                                              d_seed, layer, counts, slots, (unsigned long long*)minpos,
+                                                              tag_ctr, scratch);
     }
     return hg_check_launch("sample_layer");
+}
+
+// Retire a first-occurrence tag without a dedup pass (a bare draw).
+extern "C" int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream) {
+    k_fo_advance<<<1, 1, 0, (cudaStream_t)stream>>>(tag_ctr);
+    return hg_check_launch("first_occurrence_advance");
 }
 
 // Dedup + relabel + per-dst sort (kernels.py:166-180, sampler.py:106-118).
 // ws: >= hg_dedup_ws_size(cap_dst, fanout) ints.  Produces src_vertices[0..n_src),
 // *d_n_src, sorted slots / slot_local, nself (nullable), outdeg (nullable; must be
-// zeroed over cap_src by the caller), and restores minpos.
+// zeroed over cap_src by the caller), and retires the first-occurrence tag.
 // ws layout (ints): rank[P] | pad | status (uint64)[tiles] | generation counter.
 // The workspace must be zero-filled once when allocated and then kept.
 extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
@@ -464,8 +486,8 @@ extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
 }
 
 extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                                const int32_t* counts, int32_t* slots, int32_t* slot_local, int32_t* minpos,
-                                int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
+                                const int32_t* counts, int32_t* slots, int32_t* slot_local, const uint64_t* minpos,
+                                int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
                                 int32_t* outdeg, int32_t* ws, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("dedup(empty)"); }
@@ -474,22 +496,23 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
     int* flags = ws;  // rank of each first-occurrence position
     unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + ((P + 1) & ~1LL));
     int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
-    k_markscan<<<(unsigned)tiles, MS_THREADS, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos,
-                                                      flags, src_vertices, d_n_src, status, d_gen);
+    k_markscan<<<(unsigned)tiles, MS_THREADS, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
+                                                      (const unsigned long long*)minpos, tag_ctr, flags, src_vertices,
+                                                      d_n_src, status, d_gen);
     if (fanout <= 32) {
         const int W = seg_width(fanout);
         const int grid = hg_grid((long long)cap_dst * W, 256, 8);
         switch (W) {
-            case 4: k_relabel_sort_seg<4><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
-            case 8: k_relabel_sort_seg<8><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
-            case 16: k_relabel_sort_seg<16><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
-            default: k_relabel_sort_seg<32><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, flags, nself, outdeg); break;
+            case 4: k_relabel_sort_seg<4><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            case 8: k_relabel_sort_seg<8><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            case 16: k_relabel_sort_seg<16><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            default: k_relabel_sort_seg<32><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
         }
     } else {
         k_relabel_sort_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
-                                                                    slot_local, minpos, flags, nself, outdeg);
+                                                                    slot_local, (const unsigned long long*)minpos,
+                                                                    flags, nself, outdeg, tag_ctr, d_gen);
     }
-    k_reset_minpos<<<hg_grid(cap_src, 256, 8), 256, 0, s>>>(src_vertices, d_n_src, cap_src, minpos, d_gen);
     return hg_check_launch("dedup_relabel");
 }
 

@@ -50,6 +50,26 @@ def u64_tensor(values, device):
     return torch.as_tensor(arr.view(np.int64), device=device)
 
 
+class FirstOccurrenceTable:
+    """Dense per-vertex first-occurrence table of the dedup kernels.
+
+    ``table`` holds uint64 keys ``(tag << 32) | position`` (all ~0 when
+    allocated); ``tag`` is the device counter the relabel kernel bumps after
+    each use, so stale keys always lose and the table is never reset.  Users
+    that may run concurrently (different streams) need separate tables.
+    """
+
+    def __init__(self, num_vertices: int, device):
+        self.table = torch.full((max(int(num_vertices), 1),), -1, dtype=torch.int64, device=device)
+        self.tag = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def like(self):
+        return FirstOccurrenceTable(self.table.numel(), self.table.device)
+
+    def nbytes(self) -> int:
+        return self.table.numel() * 8 + 4
+
+
 class DeviceGraph:
     """HBM layout of one dataset (see graph.py docstring):
     offsets int64[V+1], targets int32[E], features fp32[V, F_pad], labels int32[V]."""
@@ -76,15 +96,15 @@ class DeviceGraph:
             x[:, :F] = torch.as_tensor(np.ascontiguousarray(feats, dtype=np.float32), device=self.device)
             self.features = x
         self.labels = None if labels is None else i32(labels, self.device)
-        # first-occurrence table for the dedup kernel: INT32_MAX at rest
-        self.minpos = torch.full((self.num_vertices,), 2**31 - 1, dtype=torch.int32, device=self.device)
+        # first-occurrence table for the dedup kernel (shared by sequential users)
+        self.minpos = FirstOccurrenceTable(self.num_vertices, self.device)
 
     @classmethod
     def from_dataset(cls, ds, device=None):
         return cls(ds.offsets, ds.targets, ds.features, ds.labels, device=device)
 
     def nbytes(self) -> int:
-        n = self.offsets.numel() * 8 + self.targets.numel() * 4 + self.minpos.numel() * 4
+        n = self.offsets.numel() * 8 + self.targets.numel() * 4 + self.minpos.nbytes()
         if self.features is not None:
             n += self.features.numel() * 4
         if self.labels is not None:

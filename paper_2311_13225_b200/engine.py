@@ -191,7 +191,7 @@ class TrainEngine:
         zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
         self.sets = []
         for k in range(n_sets):
-            mp = None if k == 0 else torch.full_like(dg.minpos, 2**31 - 1)
+            mp = None if k == 0 else dg.minpos.like()
             smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage, need_outdeg=not self.sage,
                                 need_csc=l > 0, minpos=mp) for l in range(self.L)]
             self.sets.append(SampleSet(samplers=smp, seeds=z32(self.batch_cap), counts_in=z32(2),

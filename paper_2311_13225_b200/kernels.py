@@ -58,9 +58,9 @@ def sample_layer(offsets, targets, dst_globals, fanout, stream_seed):
     seed = u64_tensor(stream_seed, dev)
     s = stream_ptr()
     _lib.call("hg_sample_layer", ptr(dg.offsets), ptr(dg.targets), ptr(fr), None, n, f, ptr(seed), -1,
-              ptr(counts), ptr(slots), ptr(dg.minpos), ptr(scratch), s)
-    # this call does not dedup: restore the first-occurrence table
-    dg.minpos.fill_(2**31 - 1)
+              ptr(counts), ptr(slots), ptr(dg.minpos.table), ptr(dg.minpos.tag), ptr(scratch), s)
+    # this call does not dedup: retire the first-occurrence tag
+    _lib.call("hg_first_occurrence_advance", ptr(dg.minpos.tag), s)
     ed, es, ne = z(n * f), z(n * f), z(1)
     ws = z(_lib.fn("hg_block_edges_ws_size")(n))
     _lib.call("hg_raw_edges", None, n, f, ptr(counts), ptr(slots), ptr(ed), ptr(es), ptr(ne), ptr(ws), s)

@@ -152,7 +152,7 @@ class HotProducer:
         # own first-occurrence table: the producer runs concurrently with the
         # training stream's samplers
         self.smp = LayerSampler(e.dg, self.cap, e.fan[0], need_nself=e.sage, need_outdeg=not e.sage,
-                                minpos=torch.full_like(e.dg.minpos, 2**31 - 1))
+                                minpos=e.dg.minpos.like())
         zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
         self.self_buf = zf(self.cap, e.ld[0]) if e.sage else None
         self.agg = zf(self.cap, e.ld[0])

@@ -115,8 +115,8 @@ class LayerSampler:
         lib = _lib.load()
         dev = dg.device
         self.dg, self.f, self.cap_dst = dg, int(fanout), int(cap_dst)
-        # first-occurrence table (INT32_MAX at rest); samplers that may run
-        # concurrently on different streams need their own
+        # first-occurrence table (device.FirstOccurrenceTable); samplers that may
+        # run concurrently on different streams need their own
         self.minpos = dg.minpos if minpos is None else minpos
         self.cap_src = int(min(dg.num_vertices, self.cap_dst * (self.f + 1)))
         z = lambda n: torch.zeros(max(int(n), 1), dtype=torch.int32, device=dev)  # noqa: E731
@@ -151,9 +151,10 @@ class LayerSampler:
         if self.outdeg is not None:
             self.outdeg.zero_()
         _lib.call("hg_sample_layer", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
-                  ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos), ptr(self.scratch), s)
+                  ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos.table),
+                  ptr(self.minpos.tag), ptr(self.scratch), s)
         _lib.call("hg_dedup_relabel", ptr(frontier), ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slots),
-                  ptr(self.slot_local), ptr(self.minpos), ptr(self.src), ptr(self.n_src), cap_src, ptr(self.nself),
+                  ptr(self.slot_local), ptr(self.minpos.table), ptr(self.minpos.tag), ptr(self.src), ptr(self.n_src), cap_src, ptr(self.nself),
                   ptr(self.outdeg), ptr(self.ws), s)
         if self.need_csc and with_csc:
             self.build_csc(d_n_dst, stream, cap)

@@ -49,6 +49,6 @@ def test_workspace_sizes_monotone():
 
 def test_error_string_roundtrip():
     # invalid fanout is rejected before any device work
-    rc = _lib.fn("hg_sample_layer")(None, None, None, None, 10, 0, None, 0, None, None, None, None, None)
+    rc = _lib.fn("hg_sample_layer")(None, None, None, None, 10, 0, None, 0, None, None, None, None, None, None)
     assert rc == -1
     assert "fanout" in _lib.last_error()
