@@ -345,6 +345,11 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (agg_ms / 1000.0) / 1e9
+    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    try:
+        traffic = float(json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["traffic_bytes_per_launch"])
+    except Exception:
+        pass
     # kernels per step (graph kernel nodes) -> launches in the timed region
     lib = _lib.load()
     per_step = 0
@@ -398,7 +403,8 @@ def main():
                            global_batch=1024 * world),
             "roofline": {"bound": "hbm", "kernel": "k_agg_fwd (bottom fused gather+mean, SAGE)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": agg_ms,
+                         "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": agg_ms,
                          "block0": {"n_dst": n_dst0, "n_src": n_src0, "edges": E0},
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
             "cpu_baseline": cpu_base,
