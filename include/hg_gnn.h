@@ -146,7 +146,9 @@ int hg_gemm_tc_prep_b_many(int32_t n, const int64_t* host_desc, void* stream);
 int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32_t lda2, int32_t K2,
                const void* bimg, float* C, int32_t ldc, int32_t N, const int32_t* d_M, int32_t M_cap, int32_t act,
                void* stream);
-/* process-wide tuning knobs for the tensor-core kernels (key 1: MN-major descriptor offsets) */
+/* process-wide tuning knobs for the tensor-core kernels (key 1: MN-major descriptor offsets;
+ * key 2: 1 = legacy cp.async GEMM kernels instead of the warp-specialised TMA pipelines;
+ * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem) */
 int hg_set_tuning(int32_t key, int32_t value);
 /* out_s[K x N] = A_s^T G (s = 1, 2; A2 may be NULL), deterministic split-M. */
 int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int32_t n_src);

@@ -22,114 +22,13 @@
 // row-major over the reduction dimension), which tf32 UMMA supports.
 #include "hg_common.cuh"
 #include "hg_gnn_internal.h"
+#include "hg_tc.cuh"
 
 namespace {
+using namespace hgtc;
 
 int g_mn_swap = 0;  // tuning knob (hg_set_tuning key 1): MN-major descriptor offset assignment
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
-                 "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
-}
-
-// shared-memory matrix descriptor (start, leading/stride byte offsets, layout
-// type: 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B — the only MN-major layout
-// tf32 operands support)
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-    d |= (uint64_t)layout << 61;
-    return d;
-}
-
-// instruction descriptor: kind::tf32, fp32 accumulate, M=128, N, operand majors
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(da), "l"(db), "r"(idesc), "r"(acc)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// byte offset of (row r, 16-byte chunk c) in a K-major SWIZZLE_128B tile
-// (8-row x 128-byte atoms stacked along rows, atom stride 1024 B)
-__device__ __forceinline__ uint32_t off_k(int r, int c) {
-    return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
-}
-// byte offset of (reduction row kr, 16-byte MN chunk cg) in an MN-major
-// SWIZZLE_128B_BASE32B tile holding 32 reduction rows: atoms are 4 rows x 128 B
-// (32 MN elements), 32-byte granules XOR-swizzled with the row (Swizzle<2,5,2>);
-// atom (MN group g = cg/8, K group kr/4) at (g*8 + kr/4)*512, so MN groups are
-// 4096 B apart and K groups 512 B apart.
-__device__ __forceinline__ uint32_t off_mn(int kr, int cg) {
-    const int row = kr & 3, c = cg & 7;
-    return (uint32_t)(((cg >> 3) * 8 + (kr >> 2)) * 512 + row * 128 + ((((c >> 1) ^ row)) << 5) + ((c & 1) << 4));
-}
-
-__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
-
-__device__ __forceinline__ void split_lo16(const uint8_t* hi, uint8_t* lo) {
-    float4 v = *reinterpret_cast<const float4*>(hi);
-    v.x = tf32_lo(v.x); v.y = tf32_lo(v.y); v.z = tf32_lo(v.z); v.w = tf32_lo(v.w);
-    *reinterpret_cast<float4*>(lo) = v;
-}
+int g_legacy = 0;   // tuning knob (hg_set_tuning key 2): 1 = the cp.async kernels below instead of hg_gemm_tma.cu
 
 constexpr int TC_THREADS = 256;    // wgrad CTAs
 constexpr int GEMM_THREADS = 256;  // forward / dX CTAs (8 warps: more loads and splits in flight)
@@ -631,6 +530,7 @@ extern "C" int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float
     cudaStream_t s = (cudaStream_t)stream;
     const int bn = gemm_bn(N);
     const uint8_t* b = (const uint8_t*)bimg;
+    if (!g_legacy) return hg_gemm_tma_launch(A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act, s);
     dim3 g(hg_ceil_div(M_cap, 128), hg_ceil_div(N, bn));
     switch (bn) {
         case 32: return launch_gemm<32>(g, s, A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act);
@@ -643,6 +543,9 @@ extern "C" int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float
 // process-wide tuning knobs (key 1: MN-major descriptor LBO/SBO assignment)
 extern "C" int hg_set_tuning(int32_t key, int32_t value) {
     if (key == 1) { g_mn_swap = value ? 1 : 0; return HG_OK; }
+    if (key == 2) { g_legacy = value ? 1 : 0; return HG_OK; }
+    if (key == 3) { hg_tma_set_fwd_form(value ? 1 : 0); return HG_OK; }
+    if (key == 9) { hg_tma_set_dbg(value); return HG_OK; }
     hg_set_error("set_tuning: unknown key %d", key);
     return HG_EINVAL;
 }
@@ -651,7 +554,8 @@ extern "C" int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int3
     const int kt = hg_ceil_div(K > 0 ? K : 1, 128);
     const int rpc = wgrad_rows_per_chunk(M_cap > 0 ? M_cap : 1, kt, n_src);
     const int chunks = hg_ceil_div(M_cap > 0 ? M_cap : 1, rpc);
-    return (int64_t)n_src * chunks * K * N;
+    const int tchunks = hg_wgrad_tma_chunks(K, n_src);
+    return (int64_t)n_src * (chunks > tchunks ? chunks : tchunks) * K * N;
 }
 
 // out_s[K x N] = A_s[M x K]^T G[M x N] for s = 1 (A1) and, if A2, s = 2.
@@ -666,6 +570,8 @@ extern "C" int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32
         hg_set_error("wgrad_tc: row strides must be multiples of 4");
         return HG_EINVAL;
     }
+    const uint32_t lbo = g_mn_swap ? 512u : 4096u, sbo = g_mn_swap ? 4096u : 512u;
+    if (!g_legacy) return hg_wgrad_tma_launch(A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, out1, out2, ws, lbo, sbo, s);
     const int n_src = A2 ? 2 : 1;
     const int kt = hg_ceil_div(K, 128);
     const int Mc = M_cap > 0 ? M_cap : 1;

@@ -1,0 +1,736 @@
+// K8, warp-specialised TMA pipelines for the dense layer transforms.
+//
+// Same contracts as hg_gemm_tc.cu (fwd / dX: C = act(A1 op(B)[:K1] + A2 op(B)[K1:]);
+// wgrad: dW_s = A_s^T G) and the same 3xTF32 arithmetic (x fed raw = its
+// truncated tf32 "hi", lo = x - hi split in shared memory, D += AhBh + AhBl + AlBh),
+// but the GEMMs here are HBM streams (K <= 2F, N <= 256), so the kernels are
+// built to keep the memory system busy:
+//
+//   warp 0 (one lane)  TMA producer: cp.async.bulk.tensor 2-D tiles of A (and G)
+//                      straight into the 128-byte-swizzled UMMA layouts, the
+//                      prebuilt B image with one cp.async.bulk; completion via
+//                      mbarrier transaction counts; runs up to S stages ahead.
+//   warp 1 (one lane)  MMA issuer: tcgen05.mma kind::tf32 into TMEM, commits free
+//                      the stage (and, per output tile, hand the accumulator to
+//                      the epilogue).
+//   4 split warps      lo = x - trunc_tf32(x) of each landed stage (layout-agnostic,
+//                      linear 16-byte chunks), zeroing reduction rows past M (wgrad).
+//   4 epilogue warps   (fwd) tcgen05.ld of the previous tile's accumulator + ReLU +
+//                      stores, overlapping the next tile's loads and MMAs (two TMEM
+//                      accumulators).
+//
+// No __syncthreads inside the main loops: every hand-off is an mbarrier
+// (full -> split -> MMA -> empty -> producer; tfull -> epilogue -> tempty -> MMA).
+// wgrad splits the reduction over M into a fixed number of chunks sized from the
+// device-side row count, then reduces the partials in a fixed order
+// (deterministic).
+#include <cuda.h>
+
+#include "hg_common.cuh"
+#include "hg_gnn_internal.h"
+#include "hg_tc.cuh"
+
+namespace {
+using namespace hgtc;
+
+constexpr int FWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-5 split, w6-9 epilogue
+constexpr int WG_THREADS = 192;   // w0 TMA, w1 MMA, w2-5 split (+ final epilogue)
+constexpr int A_BYTES = 128 * 128;  // 128 rows x 32 fp32 (fwd) / 32 rows x 128 fp32 (wgrad)
+
+template <int BN>
+__host__ __device__ constexpr int fwd_stages() { return BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2; }
+template <int BN>
+__host__ __device__ constexpr int fwd_stage_bytes() { return 2 * A_BYTES + 2 * BN * 128; }
+template <int BN>
+__host__ __device__ constexpr int wg_stages() { return BN <= 64 ? 4 : BN <= 128 ? 3 : 2; }
+template <int BN>
+__host__ __device__ constexpr int wg_stage_bytes() { return 2 * A_BYTES + 2 * BN * 128; }
+template <int C>
+__host__ __device__ constexpr uint32_t tmem_cols() { return C <= 32 ? 32 : C <= 64 ? 64 : C <= 128 ? 128 : C <= 256 ? 256 : 512; }
+
+// profiling knob (hg_set_tuning key 9): bit 0 skips the MMAs, bit 1 the split
+// work (pipelines still run; results are wrong) — isolates the bound stage
+__constant__ int c_dbg;
+
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// forward / dX: persistent CTAs over 128-row M tiles (blockIdx.y = BN-wide N tile)
+template <int BN>
+__global__ void __launch_bounds__(FWD_THREADS, 1)
+k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
+           const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
+           int M_cap, int act) {
+    constexpr int S = fwd_stages<BN>();
+    constexpr int STAGE = fwd_stage_bytes<BN>();
+    constexpr int B_BYTES = 2 * BN * 128;
+    constexpr int B_TILE = BN * 128;
+    constexpr uint32_t NCOLS = tmem_cols<2 * BN>();
+    constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[S], splt[S], empty[S], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int M = hg_load_count(d_M, M_cap);
+    const int n_mt = (M + 127) >> 7;
+    if ((int)blockIdx.x >= n_mt) return;
+    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int nk = nk1 + nk2;
+    const int iters = n_my * nk;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.y * BN;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&splt[i], 4);
+            mbar_init(&empty[i], 1);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init_fence();
+        tma_prefetch_desc(&tmA1);
+        if (nk2) tma_prefetch_desc(&tmA2);
+    }
+    if (warp == 1) tmem_alloc(&s_tmem, NCOLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            const uint8_t* bimg = Bimg + (int64_t)blockIdx.y * nk * B_BYTES;
+            for (int it = 0; it < iters; ++it) {
+                const int st = it % S;
+                if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
+                const int tile = it / nk, kt = it - tile * nk;
+                const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
+                uint8_t* base = smem + st * STAGE;
+                mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
+                if (kt < nk1) tma_load_2d(smem_u32(base), &tmA1, kt * 32, m0, &full[st]);
+                else tma_load_2d(smem_u32(base), &tmA2, (kt - nk1) * 32, m0, &full[st]);
+                bulk_load(smem_u32(base + 2 * A_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            int it = 0;
+            for (int tile = 0; tile < n_my; ++tile) {
+                const int acc = tile & 1;
+                if (tile >= 2) mbar_wait(&tempty[acc], (uint32_t)(((tile >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kt = 0; kt < nk; ++kt, ++it) {
+                    const int st = it % S;
+                    mbar_wait(&splt[st], (uint32_t)((it / S) & 1));
+                    tc_fence_after();
+                    const uint32_t a_hi = smem_u32(smem + st * STAGE), a_lo = a_hi + A_BYTES;
+                    const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_TILE;
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) {
+                        const uint64_t dah = sdesc(a_hi + s * 32, 16, 1024), dal = sdesc(a_lo + s * 32, 16, 1024);
+                        const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
+                        mma_tf32(d, dah, dbh, IDESC, (kt | s) ? 1u : 0u);
+                        mma_tf32(d, dah, dbl, IDESC, 1u);
+                        mma_tf32(d, dal, dbh, IDESC, 1u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp < 6) {  // ---- split warps
+        const int t = threadIdx.x - 64;
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % S;
+            mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+            uint8_t* base = smem + st * STAGE;
+#pragma unroll
+            for (int i = 0; i < A_BYTES / 16 / 128; ++i) {
+                const int off = (t + 128 * i) * 16;
+                split_lo16(base + off, base + A_BYTES + off);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&splt[st]);
+        }
+    } else {  // ---- epilogue warps: TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+        for (int tile = 0; tile < n_my; ++tile) {
+            const int acc = tile & 1;
+            mbar_wait(&tfull[acc], (uint32_t)((tile >> 1) & 1));
+            tc_fence_after();
+            const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
+            const int gm = m0 + q * 32 + lane;
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r0[16], r1[16];
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
+                tmem_ld16_nowait(ta, r0);
+                tmem_ld16_nowait(ta + 16, r1);
+                tmem_wait_ld();
+                if (gm < M && n0 + c0 < N) {
+                    float* crow = C + (int64_t)gm * ldc + n0 + c0;
+                    const int lim = N - (n0 + c0);
+                    if (vec && lim >= 32) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 o = make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]),
+                                                   __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
+                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
+                            *reinterpret_cast<float4*>(crow + j) = o;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 o = make_float4(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1]),
+                                                   __uint_as_float(r1[j + 2]), __uint_as_float(r1[j + 3]));
+                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
+                            *reinterpret_cast<float4*>(crow + 16 + j) = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (j < lim) crow[j] = act ? fmaxf(__uint_as_float(r0[j]), 0.f) : __uint_as_float(r0[j]);
+                            if (16 + j < lim)
+                                crow[16 + j] = act ? fmaxf(__uint_as_float(r1[j]), 0.f) : __uint_as_float(r1[j]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, NCOLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// forward / dX, "TS" form (BN <= 128): the split warps read each landed A tile
+// once from shared memory (one 128-byte row per thread), and write hi and lo
+// straight into TMEM with tcgen05.st; the MMAs take A from TMEM and only B from
+// shared memory.  Shared-memory traffic per K tile drops from ~136 KB (A hi/lo
+// written, A read by 8 of 12 MMAs, lo written) to ~72 KB, which is what bounds
+// the SS form at N = 64.  TMEM: 2 accumulators (2*BN columns) + S A stages of
+// 64 columns (hi 32 | lo 32).
+template <int BN>
+__host__ __device__ constexpr int ts_stages() { return BN <= 64 ? 6 : 4; }
+template <int BN>
+__host__ __device__ constexpr int ts_stage_bytes() { return A_BYTES + 2 * BN * 128; }
+
+template <int BN>
+__global__ void __launch_bounds__(FWD_THREADS, 1)
+k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
+              const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
+              int M_cap, int act) {
+    constexpr int S = ts_stages<BN>();
+    constexpr int STAGE = ts_stage_bytes<BN>();
+    constexpr int B_BYTES = 2 * BN * 128;
+    constexpr int B_TILE = BN * 128;
+    constexpr uint32_t A_COL0 = 2 * BN;  // first TMEM column of the A stages
+    static_assert(2 * BN + S * 64 <= 512, "TMEM budget");
+    constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[S], splt[S], empty[S], tfull[2], tempty[2];
+    __shared__ uint32_t s_tmem;
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int M = hg_load_count(d_M, M_cap);
+    const int n_mt = (M + 127) >> 7;
+    if ((int)blockIdx.x >= n_mt) return;
+    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int nk = nk1 + nk2;
+    const int iters = n_my * nk;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.y * BN;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&splt[i], 4);
+            mbar_init(&empty[i], 1);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init_fence();
+        tma_prefetch_desc(&tmA1);
+        if (nk2) tma_prefetch_desc(&tmA2);
+    }
+    if (warp == 1) tmem_alloc(&s_tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            const uint8_t* bimg = Bimg + (int64_t)blockIdx.y * nk * B_BYTES;
+            for (int it = 0; it < iters; ++it) {
+                const int st = it % S;
+                if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
+                const int tile = it / nk, kt = it - tile * nk;
+                const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
+                uint8_t* base = smem + st * STAGE;
+                mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
+                if (kt < nk1) tma_load_2d(smem_u32(base), &tmA1, kt * 32, m0, &full[st]);
+                else tma_load_2d(smem_u32(base), &tmA2, (kt - nk1) * 32, m0, &full[st]);
+                bulk_load(smem_u32(base + A_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer (A from TMEM)
+            int it = 0;
+            for (int tile = 0; tile < n_my; ++tile) {
+                const int acc = tile & 1;
+                if (tile >= 2) mbar_wait(&tempty[acc], (uint32_t)(((tile >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kt = 0; kt < nk; ++kt, ++it) {
+                    const int st = it % S;
+                    mbar_wait(&splt[st], (uint32_t)((it / S) & 1));
+                    tc_fence_after();
+                    const uint32_t ta = tmem + A_COL0 + (uint32_t)(st * 64);
+                    const uint32_t b_hi = smem_u32(smem + st * STAGE + A_BYTES), b_lo = b_hi + B_TILE;
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) {
+                        const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
+                        mma_tf32_ts(d, ta + s * 8, dbh, IDESC, (kt | s) ? 1u : 0u);
+                        mma_tf32_ts(d, ta + s * 8, dbl, IDESC, 1u);
+                        mma_tf32_ts(d, ta + 32 + s * 8, dbh, IDESC, 1u);
+                    }
+                    mma_commit(&empty[st]);
+                }
+                mma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp < 6) {  // ---- split warps: one tile row per thread, hi|lo -> TMEM
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % S;
+            mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+            const uint8_t* base = smem + st * STAGE;
+            uint32_t hi[32], lo[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(base + off_k(r, c));
+                hi[4 * c + 0] = __float_as_uint(v.x);
+                hi[4 * c + 1] = __float_as_uint(v.y);
+                hi[4 * c + 2] = __float_as_uint(v.z);
+                hi[4 * c + 3] = __float_as_uint(v.w);
+            }
+#pragma unroll
+            for (int k = 0; k < 32; ++k) lo[k] = __float_as_uint(tf32_lo(__uint_as_float(hi[k])));
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(st * 64);
+            tmem_st32(ta, hi);
+            tmem_st32(ta + 32, lo);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&splt[st]);
+        }
+    } else {  // ---- epilogue warps: TMEM lane quarter = warp % 4
+        const int q = warp & 3;
+        const bool vec = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0);
+        for (int tile = 0; tile < n_my; ++tile) {
+            const int acc = tile & 1;
+            mbar_wait(&tfull[acc], (uint32_t)((tile >> 1) & 1));
+            tc_fence_after();
+            const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
+            const int gm = m0 + q * 32 + lane;
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t r0[16], r1[16];
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
+                tmem_ld16_nowait(ta, r0);
+                tmem_ld16_nowait(ta + 16, r1);
+                tmem_wait_ld();
+                if (gm < M && n0 + c0 < N) {
+                    float* crow = C + (int64_t)gm * ldc + n0 + c0;
+                    const int lim = N - (n0 + c0);
+                    if (vec && lim >= 32) {
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 o = make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]),
+                                                   __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
+                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
+                            *reinterpret_cast<float4*>(crow + j) = o;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            float4 o = make_float4(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1]),
+                                                   __uint_as_float(r1[j + 2]), __uint_as_float(r1[j + 3]));
+                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
+                            *reinterpret_cast<float4*>(crow + 16 + j) = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (j < lim) crow[j] = act ? fmaxf(__uint_as_float(r0[j]), 0.f) : __uint_as_float(r0[j]);
+                            if (16 + j < lim)
+                                crow[16 + j] = act ? fmaxf(__uint_as_float(r1[j]), 0.f) : __uint_as_float(r1[j]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// wgrad: CTA (unit = (src, 128-row K tile), chunk) accumulates
+//   partial[src][chunk][K x N] = A_src[rows of chunk]^T G[rows of chunk]
+// with both operands MN-major (SWIZZLE_128B_BASE32B atoms: 32 MN elements x 4
+// reduction rows, loaded by TMA with the matching 32-byte-atom swizzle).
+__device__ __forceinline__ int wg_rows_per_chunk(int M, int n_chunks) {
+    int r = (M + n_chunks - 1) / n_chunks;
+    return ((r + 31) / 32) * 32;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(WG_THREADS, 1)
+k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
+            const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
+            int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
+    constexpr int S = wg_stages<BN>();
+    constexpr int STAGE = wg_stage_bytes<BN>();
+    constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
+    constexpr int NG = BN / 32;       // G boxes (32 columns each) per stage
+    constexpr uint32_t NCOLS = tmem_cols<BN>();
+    constexpr uint32_t IDESC = idesc_tf32(128, BN, 1, 1);
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[S], splt[S], empty[S], done;
+    __shared__ uint32_t s_tmem;
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int M = hg_load_count(d_M, M_cap);
+    const int rpc = wg_rows_per_chunk(M, n_chunks);
+    const int chunk = blockIdx.y;
+    const int mbeg = chunk * rpc;
+    if (mbeg >= M) return;  // the reduction skips chunks past M
+    const int mend = min(M, mbeg + rpc);
+    const int src = blockIdx.x / ktiles, kt = blockIdx.x - src * ktiles;
+    const CUtensorMap* tmA = src ? &tmA2 : &tmA1;
+    const int nsteps = (mend - mbeg + 31) >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&splt[i], 4);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(&done, 1);
+        mbar_init_fence();
+        tma_prefetch_desc(tmA);
+        tma_prefetch_desc(&tmG);
+    }
+    if (warp == 1) tmem_alloc(&s_tmem, NCOLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer: 4 A boxes (32 k x 32 rows) + NG G boxes per step
+            for (int j = 0; j < nsteps; ++j) {
+                const int st = j % S;
+                if (j >= S) mbar_wait(&empty[st], (uint32_t)(((j / S) - 1) & 1));
+                uint8_t* base = smem + st * STAGE;
+                const int y = mbeg + 32 * j;
+                mbar_expect_tx(&full[st], A_BYTES + G_TILE);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) tma_load_2d(smem_u32(base + g * 4096), tmA, kt * 128 + g * 32, y, &full[st]);
+#pragma unroll
+                for (int g = 0; g < NG; ++g)
+                    tma_load_2d(smem_u32(base + 2 * A_BYTES + g * 4096), &tmG, g * 32, y, &full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            for (int j = 0; j < nsteps; ++j) {
+                const int st = j % S;
+                mbar_wait(&splt[st], (uint32_t)((j / S) & 1));
+                tc_fence_after();
+                const uint32_t a_hi = smem_u32(smem + st * STAGE), a_lo = a_hi + A_BYTES;
+                const uint32_t g_hi = a_hi + 2 * A_BYTES, g_lo = g_hi + G_TILE;
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {  // 8 reduction rows (two 4-row K atoms) per MMA
+                    if (c_dbg & 1) break;
+                    const uint64_t dah = sdesc(a_hi + s * 1024, lbo, sbo, 1), dal = sdesc(a_lo + s * 1024, lbo, sbo, 1);
+                    const uint64_t dgh = sdesc(g_hi + s * 1024, lbo, sbo, 1), dgl = sdesc(g_lo + s * 1024, lbo, sbo, 1);
+                    mma_tf32(tmem, dah, dgh, IDESC, (j | s) ? 1u : 0u);
+                    mma_tf32(tmem, dah, dgl, IDESC, 1u);
+                    mma_tf32(tmem, dal, dgh, IDESC, 1u);
+                }
+                mma_commit(&empty[st]);
+            }
+            mma_commit(&done);
+        }
+    } else {  // ---- split warps (reduction rows past M are zeroed in hi and lo)
+        const int t = threadIdx.x - 64;
+        for (int j = 0; j < nsteps; ++j) {
+            const int st = j % S;
+            mbar_wait(&full[st], (uint32_t)((j / S) & 1));
+            uint8_t* base = smem + st * STAGE;
+            const int valid = mend - (mbeg + 32 * j);  // rows < valid are real
+#pragma unroll
+            for (int i = 0; i < ((c_dbg & 2) ? 0 : A_BYTES / 16 / 128); ++i) {
+                const int off = (t + 128 * i) * 16;
+                if (((off & 4095) >> 7) < valid) {
+                    split_lo16(base + off, base + A_BYTES + off);
+                } else {
+                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                    *reinterpret_cast<float4*>(base + off) = z;
+                    *reinterpret_cast<float4*>(base + A_BYTES + off) = z;
+                }
+            }
+            uint8_t* gb = base + 2 * A_BYTES;
+#pragma unroll
+            for (int i = 0; i < ((c_dbg & 2) ? 0 : G_TILE / 16 / 128); ++i) {
+                const int off = (t + 128 * i) * 16;
+                if (((off & 4095) >> 7) < valid) {
+                    split_lo16(gb + off, gb + G_TILE + off);
+                } else {
+                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                    *reinterpret_cast<float4*>(gb + off) = z;
+                    *reinterpret_cast<float4*>(gb + G_TILE + off) = z;
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&splt[st]);
+        }
+        // ---- epilogue: partial rows k of this K tile (TMEM lane = k - kt*128)
+        mbar_wait(&done, 0u);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int gk = kt * 128 + q * 32 + lane;
+        float* P = partial + ((int64_t)src * n_chunks + chunk) * (int64_t)K * N;
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            tmem_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+            tmem_wait_ld();
+            if (gk < K && c0 < N) {
+                float* prow = P + (int64_t)gk * N + c0;
+                const int lim = N - c0;
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    if (jj < lim) prow[jj] = __uint_as_float(r[jj]);
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, NCOLS);
+    }
+}
+
+// Fixed-order reduction of the active chunks' partials (chunk order, then the
+// 8 warp sums in order): deterministic for a given M.
+__global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restrict__ partial, int KN, int n_chunks,
+                                                          const int* __restrict__ d_M, int M_cap,
+                                                          float* __restrict__ out1, float* __restrict__ out2) {
+    __shared__ float s_part[8][33];
+    const int M = hg_load_count(d_M, M_cap);
+    const int rpc = M > 0 ? wg_rows_per_chunk(M, n_chunks) : 1;
+    const int chunks = M > 0 ? (M + rpc - 1) / rpc : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int per_src = (KN + 31) / 32;
+    const int s = blockIdx.x / per_src;
+    const int e = (blockIdx.x - s * per_src) * 32 + lane;
+    float acc = 0.f;
+    if (e < KN) {
+        const float* p = partial + (int64_t)s * n_chunks * KN + e;
+        for (int c = w; c < chunks; c += 8) acc += p[(int64_t)c * KN];
+    }
+    s_part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && e < KN) {
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += s_part[k][lane];
+        (s ? out2 : out1)[e] = t;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host: tensor maps through the driver entry point (no libcuda link needed)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// fp32 matrix [rows x cols] with row stride ld (elements); box = box_cols x box_rows
+int make_map(CUtensorMap* m, const float* base, int cols, int rows, int ld, int box_cols, int box_rows,
+             CUtensorMapSwizzle sw) {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) {
+        hg_set_error("gemm_tma: cuTensorMapEncodeTiled unavailable");
+        return HG_ECUDA;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)(rows > 0 ? rows : 1)};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        hg_set_error("gemm_tma: cuTensorMapEncodeTiled failed (%d): cols %d rows %d ld %d", (int)r, cols, rows, ld);
+        return HG_ECUDA;
+    }
+    return HG_OK;
+}
+
+template <int BN>
+int launch_fwd(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, int nk1, int nk2,
+               const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
+    const int smem = fwd_stages<BN>() * fwd_stage_bytes<BN>() + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gemm_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    int gx = hg_ceil_div(M_cap, 128);
+    gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
+    k_gemm_tma<BN><<<dim3(gx, n_nt), FWD_THREADS, smem, s>>>(m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
+    return hg_check_launch("gemm_tma");
+}
+
+template <int BN>
+int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, int nk1,
+                  int nk2, const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
+    const int smem = ts_stages<BN>() * ts_stage_bytes<BN>() + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    int gx = hg_ceil_div(M_cap, 128);
+    gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
+    k_gemm_tma_ts<BN><<<dim3(gx, n_nt), FWD_THREADS, smem, s>>>(m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
+    return hg_check_launch("gemm_tma_ts");
+}
+
+int g_fwd_form = 1;  // 1: TS form for BN <= 128 (hg_set_tuning key 3), 0: SS form everywhere
+
+template <int BN>
+int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, const CUtensorMap& mg, int K,
+              int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo) {
+    const int smem = wg_stages<BN>() * wg_stage_bytes<BN>() + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_wgrad_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_wgrad_tma<BN><<<grid, WG_THREADS, smem, s>>>(m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial, lbo, sbo);
+    return hg_check_launch("wgrad_tma");
+}
+
+}  // namespace
+
+void hg_tma_set_fwd_form(int v) { g_fwd_form = v; }
+void hg_tma_set_dbg(int v) { cudaMemcpyToSymbol(c_dbg, &v, sizeof(int)); }
+
+int hg_tma_gemm_bn(int N) {
+    const int Nr = (N + 15) & ~15;
+    return Nr <= 32 ? 32 : Nr <= 64 ? 64 : Nr <= 128 ? 128 : 256;
+}
+
+int hg_gemm_tma_launch(const float* A1, int lda1, int K1, const float* A2, int lda2, int K2, const uint8_t* bimg,
+                       float* C, int ldc, int N, const int* d_M, int M_cap, int act, cudaStream_t s) {
+    CUtensorMap m1, m2;
+    int rc = make_map(&m1, A1, K1, M_cap, lda1, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    if (A2 && K2 > 0) {
+        rc = make_map(&m2, A2, K2, M_cap, lda2, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (rc) return rc;
+    } else {
+        m2 = m1;
+    }
+    const int nk1 = hg_ceil_div(K1, 32), nk2 = (A2 && K2 > 0) ? hg_ceil_div(K2, 32) : 0;
+    const int bn = hg_tma_gemm_bn(N);
+    const int n_nt = hg_ceil_div(N, bn);
+    if (g_fwd_form == 1 && bn <= 128) {
+        switch (bn) {
+            case 32: return launch_fwd_ts<32>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+            case 64: return launch_fwd_ts<64>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+            default: return launch_fwd_ts<128>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+        }
+    }
+    switch (bn) {
+        case 32: return launch_fwd<32>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+        case 64: return launch_fwd<64>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+        case 128: return launch_fwd<128>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+        default: return launch_fwd<256>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+    }
+}
+
+int hg_wgrad_tma_chunks(int K, int n_src) {
+    const int units = hg_ceil_div(K > 0 ? K : 1, 128) * n_src;
+    const int c = HG_NUM_SMS / units;
+    return c < 1 ? 1 : c;
+}
+
+int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, int K, const float* G, int ldg, int N,
+                        const int* d_M, int M_cap, float* out1, float* out2, float* ws, uint32_t lbo, uint32_t sbo,
+                        cudaStream_t s) {
+    const int n_src = A2 ? 2 : 1;
+    const int ktiles = hg_ceil_div(K, 128);
+    const int n_chunks = hg_wgrad_tma_chunks(K, n_src);
+    if (M_cap > 0) {
+        CUtensorMap m1, m2, mg;
+        const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+        int rc = make_map(&m1, A1, K, M_cap, lda1, 32, 32, sw);
+        if (!rc && A2) rc = make_map(&m2, A2, K, M_cap, lda2, 32, 32, sw);
+        if (!A2) m2 = m1;
+        if (!rc) rc = make_map(&mg, G, N, M_cap, ldg, 32, 32, sw);
+        if (rc) return rc;
+        const int Nr = (N + 15) & ~15;
+        dim3 grid(ktiles * n_src, n_chunks);
+        if (Nr <= 32) rc = launch_wg<32>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
+        else if (Nr <= 64) rc = launch_wg<64>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
+        else if (Nr <= 128) rc = launch_wg<128>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
+        else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
+        if (rc) return rc;
+    }
+    k_wgrad_tma_reduce<<<n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s>>>(ws, K * N, n_chunks, d_M, M_cap,
+                                                                                out1, out2);
+    return hg_check_launch("wgrad_tma_reduce");
+}

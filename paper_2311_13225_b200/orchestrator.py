@@ -159,7 +159,6 @@ class HotProducer:
         self.emb = zf(self.cap, e.ld[1])
         self.snaps = zf(max(n_snaps, 1), e.params.bottom_numel)
         self.img = dense.BImage(e.dims[0], e.dims[0] if e.sage else 0, e.dims[1], 1, dev)
-        self.d_n = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def snapshot(self, j: int):
         """_ParamCell.publish (orchestrator.py:281-284): copy W0 at this version."""

@@ -102,6 +102,10 @@ class SampledBlockStack:
         return sum(b.n_edges for b in self.blocks)
 
 
+def _as_stream(stream, device):
+    return stream if stream is not None else torch.cuda.current_stream(device)
+
+
 class LayerSampler:
     """Workspace + launches for one layer's block (draw -> dedup -> order).
 
@@ -145,11 +149,23 @@ class LayerSampler:
         side stream, off the forward critical path)."""
         cap = self.cap_dst if cap_dst is None else int(cap_dst)
         assert cap <= self.cap_dst
+        if cap != self.cap_dst:
+            # the dedup workspace (decoupled look-back status + generation counter)
+            # is laid out for the sampler's static capacity: a smaller call keeps
+            # that layout and passes its size as a device count instead
+            if d_n_dst is not None:
+                raise ValueError("cap_dst override needs d_n_dst=None (the count is the override)")
+            if not hasattr(self, "_n_override"):
+                self._n_override = torch.zeros(1, dtype=torch.int32, device=self.dg.device)
+            with torch.cuda.stream(_as_stream(stream, self.dg.device)):
+                self._n_override.fill_(cap)
+            d_n_dst, cap = self._n_override, self.cap_dst
         cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
         s = stream_ptr(stream)
         g = self.dg
         if self.outdeg is not None:
-            self.outdeg.zero_()
+            with torch.cuda.stream(_as_stream(stream, self.dg.device)):
+                self.outdeg.zero_()
         _lib.call("hg_sample_layer", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
                   ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos.table),
                   ptr(self.minpos.tag), ptr(self.scratch), s)

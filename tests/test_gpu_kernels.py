@@ -131,3 +131,27 @@ def test_sampler_errors(S, ggraphs):
         S.sample_one_hop_hot(g, np.array([1, 1]), 2, 1)
     with pytest.raises(S.SamplerError):
         S.Fanouts(())
+
+
+def test_layer_sampler_varying_chunk_sizes(S):
+    """One LayerSampler reused with growing and shrinking size overrides (the
+    hot producer's queue chunks, orchestrator.py:259-271): every block equals the
+    oracle's sample_one_hop_hot block on the same graph bytes."""
+    import torch
+    from oracle import oracle as O
+    from paper_2311_13225_b200.datagen import make_dataset
+    from paper_2311_13225_b200.device import DeviceGraph, u64_tensor
+    ds = make_dataset("c2", scale=0.1)
+    dg = DeviceGraph.from_dataset(ds)
+    og = O.Graph(ds.offsets, ds.targets.astype(np.int64))
+    smp = S.LayerSampler(dg, 60000, 15, minpos=dg.minpos.like())
+    rng = np.random.default_rng(5)
+    for c in (60000, 1200, 45000, 7, 60000, 31000):
+        ids = rng.choice(ds.num_vertices, size=c, replace=False)
+        seed = int(rng.integers(1 << 62))
+        smp.run(torch.as_tensor(ids.astype(np.int32), device="cuda"), None, u64_tensor(seed, "cuda"), 0, cap_dst=c)
+        got = smp.to_block(ids)
+        ref = O.sample_one_hop_hot(og, ids, 15, seed)
+        assert np.array_equal(got.src_vertices, ref.src_vertices), c
+        assert np.array_equal(got.edge_src, ref.edge_src), c
+        assert np.array_equal(got.edge_dst, ref.edge_dst), c
