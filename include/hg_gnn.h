@@ -148,7 +148,8 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
                void* stream);
 /* process-wide tuning knobs for the tensor-core kernels (key 1: MN-major descriptor offsets;
  * key 2: 1 = legacy cp.async GEMM kernels instead of the warp-specialised TMA pipelines;
- * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem) */
+ * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem;
+ * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always) */
 int hg_set_tuning(int32_t key, int32_t value);
 /* out_s[K x N] = A_s^T G (s = 1, 2; A2 may be NULL), deterministic split-M. */
 int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int32_t n_src);

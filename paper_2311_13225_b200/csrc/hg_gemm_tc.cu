@@ -28,6 +28,7 @@ namespace {
 using namespace hgtc;
 
 int g_mn_swap = 0;  // tuning knob (hg_set_tuning key 1): MN-major descriptor offset assignment
+int g_skinny = 0;   // tuning knob (hg_set_tuning key 4): SIMT latency path for small M (hg_gemm_skinny.cu; measured slower than the TMA pipelines on B200, kept selectable)
 int g_legacy = 0;   // tuning knob (hg_set_tuning key 2): 1 = the cp.async kernels below instead of hg_gemm_tma.cu
 
 constexpr int TC_THREADS = 256;    // wgrad CTAs
@@ -530,6 +531,8 @@ extern "C" int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float
     cudaStream_t s = (cudaStream_t)stream;
     const int bn = gemm_bn(N);
     const uint8_t* b = (const uint8_t*)bimg;
+    if (g_skinny && hg_skinny_gemm_ok(M_cap, K1, A2 ? K2 : 0, N))
+        return hg_gemm_skinny_launch(A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act, s);
     if (!g_legacy) return hg_gemm_tma_launch(A1, lda1, K1, A2, lda2, K2, b, C, ldc, N, d_M, M_cap, act, s);
     dim3 g(hg_ceil_div(M_cap, 128), hg_ceil_div(N, bn));
     switch (bn) {
@@ -545,6 +548,7 @@ extern "C" int hg_set_tuning(int32_t key, int32_t value) {
     if (key == 1) { g_mn_swap = value ? 1 : 0; return HG_OK; }
     if (key == 2) { g_legacy = value ? 1 : 0; return HG_OK; }
     if (key == 3) { hg_tma_set_fwd_form(value ? 1 : 0); return HG_OK; }
+    if (key == 4) { g_skinny = value ? 1 : 0; return HG_OK; }
     if (key == 9) { hg_tma_set_dbg(value); return HG_OK; }
     hg_set_error("set_tuning: unknown key %d", key);
     return HG_EINVAL;
@@ -555,7 +559,9 @@ extern "C" int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int3
     const int rpc = wgrad_rows_per_chunk(M_cap > 0 ? M_cap : 1, kt, n_src);
     const int chunks = hg_ceil_div(M_cap > 0 ? M_cap : 1, rpc);
     const int tchunks = hg_wgrad_tma_chunks(K, n_src);
-    return (int64_t)n_src * (chunks > tchunks ? chunks : tchunks) * K * N;
+    const int64_t tc = (int64_t)n_src * (chunks > tchunks ? chunks : tchunks) * K * N;
+    const int64_t sk = hg_wgrad_skinny_ws_floats(K, N, M_cap, n_src);
+    return tc > sk ? tc : sk;
 }
 
 // out_s[K x N] = A_s[M x K]^T G[M x N] for s = 1 (A1) and, if A2, s = 2.
@@ -571,6 +577,10 @@ extern "C" int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32
         return HG_EINVAL;
     }
     const uint32_t lbo = g_mn_swap ? 512u : 4096u, sbo = g_mn_swap ? 4096u : 512u;
+    const bool al16 = ((reinterpret_cast<uintptr_t>(A1) | reinterpret_cast<uintptr_t>(A2) |
+                        reinterpret_cast<uintptr_t>(G)) & 15) == 0;
+    if (g_skinny && al16 && hg_skinny_wgrad_ok(M_cap, K, N))
+        return hg_wgrad_skinny_launch(A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, out1, out2, ws, s);
     if (!g_legacy) return hg_wgrad_tma_launch(A1, lda1, A2, lda2, K, G, ldg, N, d_M, M_cap, out1, out2, ws, lbo, sbo, s);
     const int n_src = A2 ? 2 : 1;
     const int kt = hg_ceil_div(K, 128);

@@ -23,3 +23,13 @@ int hg_wgrad_tma_chunks(int K, int n_src);
 int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, int K, const float* G, int ldg, int N,
                         const int* d_M, int M_cap, float* out1, float* out2, float* ws, uint32_t lbo, uint32_t sbo,
                         cudaStream_t s);
+
+// fp32 SIMT latency path for the small upper-layer transforms (hg_gemm_skinny.cu)
+#define HG_SKINNY_MAX_M 16384
+bool hg_skinny_gemm_ok(int M_cap, int K1, int K2, int N);
+bool hg_skinny_wgrad_ok(int M_cap, int K, int N);
+int hg_gemm_skinny_launch(const float* A1, int lda1, int K1, const float* A2, int lda2, int K2, const uint8_t* img,
+                          float* C, int ldc, int N, const int* d_M, int M_cap, int act, cudaStream_t s);
+int64_t hg_wgrad_skinny_ws_floats(int K, int N, int M_cap, int n_src);
+int hg_wgrad_skinny_launch(const float* A1, int lda1, const float* A2, int lda2, int K, const float* G, int ldg, int N,
+                           const int* d_M, int M_cap, float* out1, float* out2, float* ws, cudaStream_t s);

@@ -22,12 +22,24 @@ def _ld(k):
     return (k + 3) // 4 * 4
 
 
+@pytest.fixture(params=["tc", "skinny"])
+def path(request):
+    """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores only (default), or the
+    optional SIMT latency kernels for small M (hg_set_tuning key 4)."""
+    from paper_2311_13225_b200 import _lib
+    lib = _lib.load()
+    lib.hg_set_tuning(4, 1 if request.param == "skinny" else 0)
+    yield request.param
+    lib.hg_set_tuning(4, 0)
+
+
 @pytest.mark.parametrize("fn", ["hg_gemm_tc", "hg_gemm_f32"])
 @pytest.mark.parametrize("M,K1,K2,N,trans,act", [
     (300, 100, 100, 64, 1, 1), (1000, 64, 64, 47, 1, 0), (129, 32, 0, 16, 1, 0), (5000, 47, 0, 64, 0, 0),
     (777, 602, 0, 256, 1, 1), (1024, 128, 0, 172, 1, 0), (1, 3, 5, 9, 1, 0), (200, 64, 0, 300, 0, 0),
+    (5700, 64, 64, 64, 1, 1), (1024, 64, 0, 128, 0, 0), (3000, 128, 128, 128, 1, 0), (6000, 47, 0, 64, 0, 0),
 ])
-def test_gemm(fn, M, K1, K2, N, trans, act):
+def test_gemm(fn, M, K1, K2, N, trans, act, path):
     import torch
     from paper_2311_13225_b200 import _lib
     from paper_2311_13225_b200.device import ptr
@@ -77,8 +89,10 @@ def test_gemm(fn, M, K1, K2, N, trans, act):
 
 
 @pytest.mark.parametrize("M,K,N,two", [(51000, 100, 64, True), (1000, 64, 47, False), (37, 602, 256, False),
-                                       (5, 3, 7, True), (70000, 64, 64, True), (0, 16, 16, False)])
-def test_wgrad_tc(M, K, N, two):
+                                       (5, 3, 7, True), (70000, 64, 64, True), (0, 16, 16, False),
+                                       (5700, 64, 64, True), (1024, 64, 47, True), (3000, 128, 128, False),
+                                       (100, 47, 128, True)])
+def test_wgrad_tc(M, K, N, two, path):
     import torch
     from paper_2311_13225_b200 import _lib
     from paper_2311_13225_b200.device import ptr

@@ -36,8 +36,10 @@ def timeit(fn, reps=24):
 
 def main():
     lib = _lib.load()
-    M, K, N = int(sys.argv[1]) if len(sys.argv) > 1 else 51000, 100, 64
-    LD = int(sys.argv[2]) if len(sys.argv) > 2 else K  # row stride of the activations (elements)
+    M = int(sys.argv[1]) if len(sys.argv) > 1 else 51000
+    K = int(sys.argv[2]) if len(sys.argv) > 2 else 100  # per source
+    N = 64
+    LD = int(sys.argv[3]) if len(sys.argv) > 3 else K  # row stride of the activations (elements)
     print(f"M={M} K={K}+{K} N={N} ld={LD}")
     R = 6  # rotate 6 input sets (> L2 in total)
     A1 = [torch.randn(M, LD, device="cuda")[:, :K] for _ in range(R)]
@@ -54,7 +56,9 @@ def main():
     ref = None
     fwd_bytes = M * 2 * K * 4 + M * N * 4
     wg_bytes = M * 2 * K * 4 + M * N * 4
-    for name, legacy, form in (("legacy cp.async", 1, 1), ("tma SS", 0, 0), ("tma TS", 0, 1)):
+    for name, legacy, form, sk in (("legacy cp.async", 1, 1, 0), ("tma SS", 0, 0, 0), ("tma TS", 0, 1, 0),
+                                   ("skinny simt", 0, 1, 1)):
+        lib.hg_set_tuning(4, sk)
         lib.hg_set_tuning(2, legacy)
         lib.hg_set_tuning(3, form)
         f = lambda r: _lib.call("hg_gemm_tc", ptr(A1[r % R]), LD, K, ptr(A2[r % R]), LD, K, ptr(img), ptr(C), N, N,  # noqa
@@ -76,12 +80,23 @@ def main():
               f"wgrad {us_w:7.2f} us ({wg_bytes / us_w / 1e3:6.0f} GB/s, max err {werr:.2e})")
     lib.hg_set_tuning(2, 0)
     lib.hg_set_tuning(3, 1)
+    lib.hg_set_tuning(4, 0)
+    wsf = torch.zeros(int(lib.hg_wgrad_ws_size(K, N, M)), device="cuda")
+    cs = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+    f = lambda r: _lib.call("hg_gemm_f32", ptr(A1[r % R]), LD, K, ptr(W), N, ptr(A2[r % R]), LD, K,  # noqa: E731
+                            W[K:].data_ptr(), N, 0, ptr(C), N, N, ptr(dM), M, 1, cs())
+    g = lambda r: (_lib.call("hg_wgrad_f32", ptr(A1[r % R]), LD, K, ptr(G[r % R]), N, N, ptr(dM), M, ptr(o1), 1.0,  # noqa
+                             ptr(wsf), cs()),
+                   _lib.call("hg_wgrad_f32", ptr(A2[r % R]), LD, K, ptr(G[r % R]), N, N, ptr(dM), M, ptr(o2), 1.0,
+                             ptr(wsf), cs()))
+    print(f"{'simt fp32':16s} fwd {timeit(f):7.2f} us   wgrad {timeit(g):7.2f} us")
     for dbg, what in ((1, "no MMA"), (2, "no split"), (3, "loads only")):
         lib.hg_set_tuning(9, dbg)
         g = lambda r: _lib.call("hg_wgrad_tc", ptr(A1[r % R]), LD, ptr(A2[r % R]), LD, K, ptr(G[r % R]), N, N,  # noqa
                                 ptr(dM), M, ptr(o1), ptr(o2), ptr(ws), torch.cuda.current_stream().cuda_stream)
         print(f"wgrad tma {what:12s} {timeit(g):7.2f} us")
     lib.hg_set_tuning(9, 0)
+    lib.hg_set_tuning(4, 0)
 
 
 if __name__ == "__main__":
