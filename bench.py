@@ -222,7 +222,7 @@ def main():
     from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer
 
     dist_ctx = None
-    if world > 1:
+    if world > 1 or os.environ.get("HG_FORCE_DIST"):  # HG_FORCE_DIST: exercise the NCCL path at N=1
         torch.cuda.set_device(_env_int("LOCAL_RANK", 0))
         from paper_2311_13225_b200.parallel import DistContext
         dist_ctx = DistContext("nccl")

@@ -151,6 +151,12 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
  * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem;
  * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always) */
 int hg_set_tuning(int32_t key, int32_t value);
+/* L2 residency: feature-gathering kernels launched after this call attach an
+ * access-policy window [base, base+bytes) with persisting hits (hit_ratio of the
+ * window's lines), and the device's persisting-L2 carve-out is set to bytes
+ * (clamped to hg_l2_persist_max()).  base NULL / bytes 0 turns it off. */
+int64_t hg_l2_persist_max(void);
+int hg_set_l2_persist(const void* base, int64_t bytes, float hit_ratio);
 /* out_s[K x N] = A_s^T G (s = 1, 2; A2 may be NULL), deterministic split-M. */
 int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int32_t n_src);
 int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32_t lda2, int32_t K, const float* G,

@@ -279,12 +279,21 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
                const int* d_n, int cap, int f, const int* counts, const int* slot_g, const int* slot_local,
                const int* nself, const int* outdeg, const uint8_t* inj, float* self_out, int ld_self,
                float* agg_out, int ld_agg) {
-#define HG_FWD(L, V)                                                                                       \
-    if (LPR == L && NV == V) {                                                                             \
-        k_agg_fwd<L, V, MODE><<<g, 256, 0, s>>>(hin, ld_in, F4, frontier, d_n, cap, f, counts, slot_g,     \
-                                                slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, \
-                                                ld_agg);                                                   \
-        return HG_OK;                                                                                      \
+    // bottom layer (rows by global id): persisting L2 window over the hot feature rows
+    cudaLaunchAttribute attr[1];
+    const bool win = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL) && hg_l2_window_attr(&attr[0]);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cfg.attrs = win ? attr : nullptr;
+    cfg.numAttrs = win ? 1 : 0;
+#define HG_FWD(L, V)                                                                                      \
+    if (LPR == L && NV == V) {                                                                            \
+        cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE>, hin, ld_in, F4, frontier, d_n, cap, f, counts,    \
+                           slot_g, slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, ld_agg);   \
+        return HG_OK;                                                                                     \
     }
     HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 8)
 #undef HG_FWD

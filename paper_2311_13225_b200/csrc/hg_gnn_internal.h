@@ -33,3 +33,6 @@ int hg_gemm_skinny_launch(const float* A1, int lda1, int K1, const float* A2, in
 int64_t hg_wgrad_skinny_ws_floats(int K, int N, int M_cap, int n_src);
 int hg_wgrad_skinny_launch(const float* A1, int lda1, const float* A2, int lda2, int K, const float* G, int ldg, int N,
                            const int* d_M, int M_cap, float* out1, float* out2, float* ws, cudaStream_t s);
+
+// access-policy window of the persisting feature rows (hg_util.cu); false if unset
+bool hg_l2_window_attr(cudaLaunchAttribute* a);

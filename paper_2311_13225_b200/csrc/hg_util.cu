@@ -299,3 +299,51 @@ size_t hg_radix_ws_ints(long long n) {
 }
 
 extern "C" int64_t hg_radix_ws_size(int64_t n) { return (int64_t)hg_radix_ws_ints(n); }
+
+// ---------------------------------------------------------------------------
+// L2 residency for the hot rows of the feature table (process-wide): kernels
+// that gather feature rows attach an access-policy window so accesses inside it
+// persist in L2 across batches (hub rows are re-read by most batches).
+// ---------------------------------------------------------------------------
+namespace {
+const void* g_l2_base = nullptr;
+size_t g_l2_bytes = 0;
+float g_l2_hit = 0.f;
+}  // namespace
+
+bool hg_l2_window_attr(cudaLaunchAttribute* a) {
+    if (!g_l2_base || !g_l2_bytes) return false;
+    a->id = cudaLaunchAttributeAccessPolicyWindow;
+    a->val.accessPolicyWindow.base_ptr = const_cast<void*>(g_l2_base);
+    a->val.accessPolicyWindow.num_bytes = g_l2_bytes;
+    a->val.accessPolicyWindow.hitRatio = g_l2_hit;
+    a->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    a->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    return true;
+}
+
+extern "C" int64_t hg_l2_persist_max(void) {
+    int dev = 0, a = 0, b = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&a, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&b, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    return (int64_t)(a < b ? a : b);
+}
+
+extern "C" int hg_set_l2_persist(const void* base, int64_t bytes, float hit_ratio) {
+    if (!base || bytes <= 0) {
+        g_l2_base = nullptr;
+        g_l2_bytes = 0;
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        return hg_check_launch("set_l2_persist(off)");
+    }
+    const int64_t mx = hg_l2_persist_max();
+    if (mx <= 0) { hg_set_error("set_l2_persist: device has no persisting L2"); return HG_EUNSUPPORTED; }
+    if (bytes > mx) bytes = mx;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)bytes) != cudaSuccess)
+        return hg_check_launch("set_l2_persist");
+    g_l2_base = base;
+    g_l2_bytes = (size_t)bytes;
+    g_l2_hit = hit_ratio < 0.f ? 0.f : (hit_ratio > 1.f ? 1.f : hit_ratio);
+    return HG_OK;
+}

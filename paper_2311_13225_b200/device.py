@@ -6,6 +6,8 @@ these buffers is one of the library's sm_100a kernels.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -98,6 +100,33 @@ class DeviceGraph:
         self.labels = None if labels is None else i32(labels, self.device)
         # first-occurrence table for the dedup kernel (shared by sequential users)
         self.minpos = FirstOccurrenceTable(self.num_vertices, self.device)
+
+    def persist_hot_rows(self, max_bytes: int | None = None, hit_ratio: float = 1.0) -> int:
+        """Pin the hottest contiguous block of feature rows in L2 (persisting
+        access-policy window on the feature-gathering kernels).  Rows are chosen
+        as the window of consecutive ids with the largest degree sum (sampled
+        neighbours are drawn roughly in proportion to degree; the generators put
+        hubs at low ids, graph.py:357).  Size: ``max_bytes`` or env
+        HG_L2_PERSIST_MB (default 32 MB), clamped to the device's persisting-L2
+        limit; 0 disables.  Returns the window size in bytes."""
+        from . import _lib
+        lib = _lib.load()
+        if self.features is None:
+            return 0
+        if max_bytes is None:
+            max_bytes = int(float(os.environ.get("HG_L2_PERSIST_MB", "32")) * 2**20)
+        row = self.feat_ld * 4
+        nbytes = min(int(max_bytes), int(lib.hg_l2_persist_max()), self.num_vertices * row)
+        rows = nbytes // row
+        if rows <= 0:
+            _lib.call("hg_set_l2_persist", None, 0, 0.0)
+            return 0
+        deg = torch.diff(self.offsets)
+        cs = torch.cumsum(torch.nn.functional.pad(deg, (1, 0)), 0)
+        start = int(torch.argmax(cs[rows:] - cs[:-rows]).item()) if rows < self.num_vertices else 0
+        self.l2_window = (start, rows)
+        _lib.call("hg_set_l2_persist", self.features[start].data_ptr(), rows * row, float(hit_ratio))
+        return rows * row
 
     @classmethod
     def from_dataset(cls, ds, device=None):

@@ -196,6 +196,8 @@ class Trainer:
         self.cfg = config
         self.ds = ds
         self.dg = ds if isinstance(ds, DeviceGraph) else DeviceGraph.from_dataset(ds, device=device)
+        if not hasattr(self.dg, "l2_window"):
+            self.dg.persist_hot_rows()
         self.train_ids = np.nonzero(np.asarray(ds.train_mask))[0].astype(np.int64)
         self.fan = tuple(int(f) for f in config.fanouts)
         C = int(np.asarray(ds.labels).max()) + 1
