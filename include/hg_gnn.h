@@ -119,6 +119,20 @@ int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const fl
                      const int32_t* d_n_src, int32_t cap_src, const float* hmask, int32_t ld_hmask,
                      const uint8_t* inj_mask, float* dx, int32_t ld_dx, const int32_t* csc_dst,
                      const float* csc_w, void* stream);
+/* Transposed aggregation by deterministic fixed-point scatter (default path for
+ * layers >= 1): dx[s] = mask(dself[s] (s < n_dst) + sum_e w_e dagg[dst_e]) with
+ * the sum accumulated as int64 at scale 2^40 (order-independent, bit-exact
+ * across runs) in acc_ws (int64 [cap_src x F], zero on first use, left zeroed);
+ * outdeg (required): sampled edges per local source (hg_dedup_relabel's outdeg);
+ * sources s >= n_dst with outdeg 1 get their final row stored directly;
+ * d_flags[0] |= 1 if a contribution is >= 2^20 or non-finite. */
+int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself,
+                             int32_t ld_dself, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
+                             int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                             const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg,
+                             const int32_t* d_n_src, int32_t cap_src, const float* hmask, int32_t ld_hmask,
+                             const uint8_t* inj_mask, int64_t* acc_ws, float* dx, int32_t ld_dx, int32_t* d_flags,
+                             void* stream);
 /* per sorted transposed edge: (dst, weight), dst = -1 for empty slots / SAGE self edges;
  * optional input of hg_aggregate_bwd (csc_dst/csc_w NULL => derived on the fly) */
 int hg_csc_weights(int32_t model, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,

@@ -454,3 +454,197 @@ extern "C" int hg_segment_weighted_rows_f64(const int64_t* edge_src, const int64
     k_swr_rows<<<hg_grid((long long)n_out * 32, 256, 8), 256, 0, s>>>(edge_src, w, rows, d, sv, beg, end, n_out, out);
     return hg_check_launch("segment_weighted_rows_f64");
 }
+
+// ---------------------------------------------------------------------------
+// Transposed aggregation by deterministic scatter (layers >= 1; replaces the
+// CSC gather above on the default path).  The reference scatters
+// segment_weighted_rows(ed, es, w, dz W^T) over the edges (gnnmath.py:140,199);
+// here every destination row of dagg is read once (coalesced, in the slot
+// form the forward uses) and its weighted copies are added into a FIXED-POINT
+// int64 accumulator per (src, column) with integer atomics.  Integer addition
+// is associative, so the result is bit-identical for any execution order
+// (eager = graph replay = pipelined) with no sort and no src-major view: the
+// whole per-layer CSC build (radix sort + scans + bounds + weights, ~10
+// kernels) leaves the sampling graph.  Scale 2^40: resolution 9.1e-13, |sum| <
+// 2^23; a contribution >= 2^20 in magnitude (or non-finite) sets d_flags[0]
+// (checked by the host like the reference's non-finite guard,
+// gnnmath.py:100-102).  The finish pass converts, adds the SAGE self term,
+// applies the lower layer's ReLU' / injected-row masks, writes dx, and clears
+// the accumulator for the next step.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr double FX_SCALE = 1099511627776.0;  // 2^40
+constexpr float FX_GUARD = 1048576.0f;        // 2^20
+
+__device__ __forceinline__ void fx_add(unsigned long long* p, float v, bool& bad) {
+    if (!(fabsf(v) < FX_GUARD)) bad = true;
+    const long long q = __double2ll_rn((double)v * FX_SCALE);
+    atomicAdd(p, (unsigned long long)q);
+}
+
+// Sources s >= n_dst with exactly one incoming transposed edge (outdeg[s] == 1;
+// most of them: ~1.15 edges per source at C2) take the single-contribution fast
+// path: the final dx row (ReLU' and injected-row masks applied) is stored
+// directly, with no accumulator round trip.  Everything else accumulates in
+// fixed point and is finished by k_bwd_finish.
+__device__ __forceinline__ float4 bwd_mask(float4 a, const float* __restrict__ hmask, int ld_hmask, int s, int c,
+                                           bool zero_row) {
+    if (hmask) {  // ReLU' of the layer below: z > 0  <=>  relu(z) > 0
+        const float4 h = __ldg(reinterpret_cast<const float4*>(hmask + (int64_t)s * ld_hmask) + c);
+        a.x = h.x > 0.f ? a.x : 0.f; a.y = h.y > 0.f ? a.y : 0.f;
+        a.z = h.z > 0.f ? a.z : 0.f; a.w = h.w > 0.f ? a.w : 0.f;
+    }
+    if (zero_row) a = make_float4(0.f, 0.f, 0.f, 0.f);
+    return a;
+}
+
+template <int LPR, int NV, bool GCN>
+__global__ void __launch_bounds__(256) k_bwd_scatter(
+    const float* __restrict__ dagg, int ld_dagg, int F4, const int* __restrict__ frontier, const int* d_n_dst,
+    int cap_dst, int f, const int* __restrict__ counts, const int* __restrict__ slot_g,
+    const int* __restrict__ slot_local, const int* __restrict__ nself, const int* __restrict__ outdeg,
+    unsigned long long* __restrict__ acc, int* __restrict__ d_flags, const float* __restrict__ hmask, int ld_hmask,
+    const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx) {
+    const int n = hg_load_count(d_n_dst, cap_dst);
+    const int lane = threadIdx.x & 31;
+    const int lr = lane & (LPR - 1);
+    const int groups_per_block = blockDim.x / LPR;
+    const int F = F4 * 4;
+    bool bad = false;
+    for (int d0 = blockIdx.x * groups_per_block; d0 < n; d0 += gridDim.x * groups_per_block) {
+        const int d = d0 + threadIdx.x / LPR;
+        if (d >= n) continue;
+        const int cnt = counts[d];
+        float4 x[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lr + k * LPR;
+            x[k] = c < F4 ? __ldg(reinterpret_cast<const float4*>(dagg + (int64_t)d * ld_dagg) + c)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const int v = GCN ? 0 : frontier[d];
+        const float wd = GCN ? 0.f : (nself[d] > 0 ? 1.0f / (float)nself[d] : 0.f);
+        const int64_t sbase = (int64_t)d * f;
+        for (int j = 0; j < cnt; ++j) {
+            const int s = slot_local[sbase + j];
+            const int od = outdeg[s];
+            float w;
+            if (GCN) {
+                w = gcn_w(od, cnt);
+            } else {
+                if (slot_g[sbase + j] == v) continue;  // SAGE drops self edges (gnnmath.py:148)
+                w = wd;
+            }
+            if (s >= n && od == 1) {  // single contribution: final row, no accumulator
+                const bool zero_row = inj && inj[s];
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int c = lr + k * LPR;
+                    if (c < F4) {
+                        float4 a = make_float4(w * x[k].x, w * x[k].y, w * x[k].z, w * x[k].w);
+                        if (!(fabsf(a.x) < FX_GUARD && fabsf(a.y) < FX_GUARD && fabsf(a.z) < FX_GUARD &&
+                              fabsf(a.w) < FX_GUARD))
+                            bad = true;
+                        reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx)[c] = bwd_mask(a, hmask, ld_hmask, s, c, zero_row);
+                    }
+                }
+                continue;
+            }
+            unsigned long long* row = acc + (int64_t)s * F;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int c = lr + k * LPR;
+                if (c < F4) {
+                    fx_add(row + 4 * c + 0, w * x[k].x, bad);
+                    fx_add(row + 4 * c + 1, w * x[k].y, bad);
+                    fx_add(row + 4 * c + 2, w * x[k].z, bad);
+                    fx_add(row + 4 * c + 3, w * x[k].w, bad);
+                }
+            }
+        }
+    }
+    if (bad && d_flags) atomicOr(d_flags, 1);
+}
+
+template <int LPR, int NV>
+__global__ void __launch_bounds__(256) k_bwd_finish(
+    unsigned long long* __restrict__ acc, int F4, const float* __restrict__ dself, int ld_dself, const int* d_n_dst,
+    int cap_dst, const int* d_n_src, int cap_src, const int* __restrict__ outdeg, const float* __restrict__ hmask,
+    int ld_hmask, const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx) {
+    const int n_src = hg_load_count(d_n_src, cap_src);
+    const int n_dst = hg_load_count(d_n_dst, cap_dst);
+    const int lane = threadIdx.x & 31;
+    const int lr = lane & (LPR - 1);
+    const int groups_per_block = blockDim.x / LPR;
+    const int F = F4 * 4;
+    for (int s0 = blockIdx.x * groups_per_block; s0 < n_src; s0 += gridDim.x * groups_per_block) {
+        const int s = s0 + threadIdx.x / LPR;
+        if (s >= n_src) continue;
+        if (s >= n_dst && outdeg[s] == 1) continue;  // written by the scatter's fast path
+        const bool zero_row = inj && inj[s];
+        ulonglong4* arow = reinterpret_cast<ulonglong4*>(acc + (int64_t)s * F);
+        float4* out = reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lr + k * LPR;
+            if (c >= F4) continue;
+            const ulonglong4 q = arow[c];
+            arow[c] = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+            float4 a = make_float4((float)((double)(long long)q.x / FX_SCALE), (float)((double)(long long)q.y / FX_SCALE),
+                                   (float)((double)(long long)q.z / FX_SCALE), (float)((double)(long long)q.w / FX_SCALE));
+            if (dself && s < n_dst) {  // dx[:n_dst] = dz W_self^T + scatter (gnnmath.py:195-199)
+                const float4 ds = __ldg(reinterpret_cast<const float4*>(dself + (int64_t)s * ld_dself) + c);
+                a.x = ds.x + a.x; a.y = ds.y + a.y; a.z = ds.z + a.z; a.w = ds.w + a.w;
+            }
+            out[c] = bwd_mask(a, hmask, ld_hmask, s, c, zero_row);
+        }
+    }
+}
+
+template <bool GCN>
+int launch_scatter(int LPR, int NV, dim3 g, dim3 g2, cudaStream_t s, const float* dagg, int ld_dagg,
+                   const float* dself, int ld_dself, int F4, const int* frontier, const int* d_n_dst, int cap_dst,
+                   int f, const int* counts, const int* slot_g, const int* slot_local, const int* nself,
+                   const int* outdeg, const int* d_n_src, int cap_src, const float* hmask, int ld_hmask,
+                   const uint8_t* inj, unsigned long long* acc, float* dx, int ld_dx, int* d_flags) {
+#define HG_SC(L, V)                                                                                            \
+    if (LPR == L && NV == V) {                                                                                 \
+        k_bwd_scatter<L, V, GCN><<<g, 256, 0, s>>>(dagg, ld_dagg, F4, frontier, d_n_dst, cap_dst, f, counts,   \
+                                                   slot_g, slot_local, nself, outdeg, acc, d_flags, hmask,     \
+                                                   ld_hmask, inj, dx, ld_dx);                                  \
+        k_bwd_finish<L, V><<<g2, 256, 0, s>>>(acc, F4, dself, ld_dself, d_n_dst, cap_dst, d_n_src, cap_src,    \
+                                              outdeg, hmask, ld_hmask, inj, dx, ld_dx);                        \
+        return HG_OK;                                                                                          \
+    }
+    HG_SC(8, 1) HG_SC(16, 1) HG_SC(32, 1) HG_SC(32, 2) HG_SC(32, 4) HG_SC(32, 8)
+#undef HG_SC
+    return HG_EUNSUPPORTED;
+}
+}  // namespace
+
+extern "C" int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself,
+                                        int32_t ld_dself, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
+                                        int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                                        const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg,
+                                        const int32_t* d_n_src, int32_t cap_src, const float* hmask,
+                                        int32_t ld_hmask, const uint8_t* inj_mask, int64_t* acc_ws, float* dx,
+                                        int32_t ld_dx, int32_t* d_flags, void* stream) {
+    if (F % 4 || ld_dagg % 4 || ld_dx % 4 || (dself && ld_dself % 4) || (hmask && ld_hmask % 4)) {
+        hg_set_error("aggregate_bwd_scatter: widths must be multiples of 4");
+        return HG_EINVAL;
+    }
+    if (F > 1024) { hg_set_error("aggregate_bwd_scatter: F > 1024 unsupported"); return HG_EUNSUPPORTED; }
+    if (cap_src == 0) return HG_OK;
+    if (!outdeg) { hg_set_error("aggregate_bwd_scatter: needs the per-source edge counts (outdeg)"); return HG_EINVAL; }
+    const int F4 = F / 4;
+    int LPR, NV;
+    pick_lanes(F4, LPR, NV);
+    dim3 g(hg_grid((long long)(cap_dst > 0 ? cap_dst : 1) * LPR, 256, 8));
+    dim3 g2(hg_grid((long long)cap_src * LPR, 256, 8));
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(acc_ws);
+    const int rc = model ? launch_scatter<true>(LPR, NV, g, g2, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, d_n_src, cap_src, hmask, ld_hmask, inj_mask, acc, dx, ld_dx, d_flags)
+                         : launch_scatter<false>(LPR, NV, g, g2, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, d_n_src, cap_src, hmask, ld_hmask, inj_mask, acc, dx, ld_dx, d_flags);
+    if (rc) { hg_set_error("aggregate_bwd_scatter: unsupported width"); return rc; }
+    return hg_check_launch("aggregate_bwd_scatter");
+}

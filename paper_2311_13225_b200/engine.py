@@ -26,6 +26,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -189,11 +191,17 @@ class TrainEngine:
         # bit-identical to the sequential order) ----
         z32 = lambda *s: torch.zeros(*s, dtype=torch.int32, device=dev)  # noqa: E731
         zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        # transposed aggregation of layers >= 1: deterministic fixed-point scatter
+        # (default) or the CSC gather over a stable src-major view (HG_BWD=csc)
+        self.bwd_scatter = os.environ.get("HG_BWD", "scatter").lower() != "csc"
         self.sets = []
         for k in range(n_sets):
             mp = None if k == 0 else dg.minpos.like()
-            smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage, need_outdeg=not self.sage,
-                                need_csc=l > 0, minpos=mp) for l in range(self.L)]
+            # outdeg: GCN norm; with the scatter backward also the per-source edge
+            # counts that select its single-contribution fast path
+            smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage,
+                                need_outdeg=(not self.sage) or (l > 0 and self.bwd_scatter),
+                                need_csc=l > 0 and not self.bwd_scatter, minpos=mp) for l in range(self.L)]
             self.sets.append(SampleSet(samplers=smp, seeds=z32(self.batch_cap), counts_in=z32(2),
                                        bp=torch.zeros(BP_SIZE, dtype=torch.int64, device=dev)))
         self.cur = 0
@@ -214,6 +222,9 @@ class TrainEngine:
         ws = max(dense.wgrad_ws_size(self.dims[l], self.dims[l + 1], self.cap_dst[l], 2 if self.sage else 1)
                  for l in range(self.L))
         self.wgrad_ws = zf(max(ws, 1))
+        self.fx_acc = [torch.zeros((self.cap_src[l], self.ld[l]), dtype=torch.int64, device=dev)
+                       if (l > 0 and self.bwd_scatter) else None for l in range(self.L)]
+        self.fx_flags = z32(1)
         self.d_loss = zf(1)
         self.row_loss = zf(self.batch_cap)
         self.d_maxdelta = z32(1)
@@ -295,10 +306,10 @@ class TrainEngine:
         for l in range(self.L - 1, -1, -1):
             fr, n = self.frontier(l)
             self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False)
-            if l > 0:
+            if l > 0 and not self.bwd_scatter:
                 sc.wait_stream(main)
                 self.samplers[l].build_csc(n, sc, frontier=fr)
-        if self.L > 1:
+        if self.L > 1 and not self.bwd_scatter:
             main.wait_stream(sc)
 
     def enqueue_train_part(self, stream=None, mark=None):
@@ -386,6 +397,13 @@ class TrainEngine:
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dagg[l]),
                          self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
                 dsp, dsl, dap, dal = None, 0, ptr(self.dagg[l]), self.ld[l]
+            if self.bwd_scatter:
+                _lib.call("hg_aggregate_bwd_scatter", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n),
+                          self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
+                          ptr(smp.nself), ptr(smp.outdeg), ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]),
+                          self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), ptr(self.dz[l - 1]),
+                          self.ld[l], ptr(self.fx_flags), s)
+                continue
             _lib.call("hg_aggregate_bwd", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n), self.cap_dst[l],
                       self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.nself), ptr(smp.outdeg),
                       ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end), ptr(smp.n_src), self.cap_src[l],
@@ -483,6 +501,13 @@ class TrainEngine:
         torch.cuda.synchronize(self.device)
         return gs, segs
 
+    def check_numerics(self):
+        """Raise like the reference's non-finite guard (gnnmath.py:100-102) if a
+        backward scatter saw a non-finite or out-of-range (>= 2^20) value."""
+        if int(self.fx_flags.item()):
+            self.fx_flags.zero_()
+            raise FloatingPointError("non-finite or out-of-range gradient in the transposed aggregation")
+
     def _save_state(self):
         st = {"flat": self.params.flat.clone(), "md": self.d_maxdelta.clone(),
               "loss": self.loss_arr.clone(), "mdarr": self.md_arr.clone()}
@@ -497,6 +522,7 @@ class TrainEngine:
     def _restore_state(self, st):
         """The warm-up pass ran one real update; undo it so capture is side-effect free."""
         self.params.flat.copy_(st["flat"])
+        self.fx_flags.zero_()  # the warm-up ran on unfed (empty) sample sets
         self.d_maxdelta.copy_(st["md"])
         self.loss_arr.copy_(st["loss"])
         self.md_arr.copy_(st["mdarr"])

@@ -378,6 +378,7 @@ class Trainer:
         if state["prod_done"] is not None:
             main.wait_event(state["prod_done"])
         torch.cuda.synchronize(dev)
+        e.check_numerics()
         rep.losses = e.loss_arr[:nb].double().cpu().tolist()
         rep.max_weight_deltas = e.md_arr[:nb].double().cpu().tolist()
         hits = hot.batch_hits[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)

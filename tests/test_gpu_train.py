@@ -116,3 +116,44 @@ def test_hot_ratio_zero_equals_baseline(golden_meta, ggraphs):
     b, _ = _run(ggraphs, "sbm_sage_hot", meta, hot_ratio=0.0, strategy="case1")
     for ra, rb in zip(a, b):
         assert ra.losses == rb.losses
+
+
+@pytest.mark.parametrize("name", ["sbm_sage_hot", "pl_gcn_adam"])
+def test_bwd_scatter_matches_csc_gather(golden_meta, ggraphs, monkeypatch, name):
+    """The fixed-point scatter backward (default) and the CSC-gather backward
+    (HG_BWD=csc) compute the same transposed aggregation: per-batch losses agree
+    to fp32 rounding over a whole run."""
+    meta = golden_meta["runs"][name]
+    monkeypatch.setenv("HG_BWD", "csc")
+    a, _ = _run(ggraphs, name, meta)
+    monkeypatch.setenv("HG_BWD", "scatter")
+    b, _ = _run(ggraphs, name, meta)
+    for ra, rb in zip(a, b):
+        np.testing.assert_allclose(ra.losses, rb.losses, rtol=1e-5)
+
+
+def test_bwd_scatter_flags_nonfinite():
+    """A non-finite gradient entering the scatter raises FloatingPointError
+    (the reference's non-finite guard, gnnmath.py:100-102)."""
+    import torch
+    from paper_2311_13225_b200 import _lib
+    from paper_2311_13225_b200.device import ptr
+    F, n_dst, f = 8, 3, 2
+    dagg = torch.zeros((n_dst, F), device="cuda")
+    dagg[1, 3] = float("inf")
+    counts = torch.tensor([2, 2, 1], dtype=torch.int32, device="cuda")
+    slot_local = torch.tensor([3, 4, 0, 5, 1, 0], dtype=torch.int32, device="cuda")
+    slot_g = torch.tensor([13, 14, 10, 15, 11, 0], dtype=torch.int32, device="cuda")
+    frontier = torch.tensor([10, 11, 12], dtype=torch.int32, device="cuda")
+    nself = torch.tensor([2, 2, 1], dtype=torch.int32, device="cuda")
+    n_src = torch.tensor([6], dtype=torch.int32, device="cuda")
+    outdeg = torch.tensor([1, 1, 0, 1, 1, 1], dtype=torch.int32, device="cuda")
+    acc = torch.zeros((6, F), dtype=torch.int64, device="cuda")
+    dx = torch.zeros((6, F), device="cuda")
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("hg_aggregate_bwd_scatter", 0, ptr(dagg), F, None, 0, F, ptr(frontier), None, n_dst, f, ptr(counts),
+              ptr(slot_g), ptr(slot_local), ptr(nself), ptr(outdeg), ptr(n_src), 6, None, 0, None, ptr(acc), ptr(dx), F,
+              ptr(flags), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert int(flags.item()) == 1
+    assert int(acc.abs().sum().item()) == 0  # accumulator left cleared
