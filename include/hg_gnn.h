@@ -65,7 +65,7 @@ int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream);
  *      Produces src_vertices (first-occurrence order, dst prefix first),
  *      *d_n_src, slots re-ordered by local src id with slot_local, per-dst
  *      non-self counts `nself` (gnnmath.py:145-154; nullable) and block
- *      out-degrees `outdeg` (gnnmath.py:96; nullable, zeroed by caller), and
+ *      out-degrees `outdeg` (gnnmath.py:96; nullable; entries [0, n_src) are reset by the call), and
  *      bumps *tag_ctr so the next use of minpos starts clean. */
 int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout);
 int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
@@ -180,7 +180,8 @@ int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32_t lda2, in
 /* ---- K9/K10 loss and updates (gnnmath.py:263-312; orchestrator.py:246-255) */
 /* dlogits = (softmax - onehot) / *d_div (d_div NULL: / n); *d_loss = mean CE over
  * the n = min(*d_n, cap) rows; labels indexed by seeds[r] (seeds NULL: by r).
- * row_ws: cap floats (per-row losses, reduced in a fixed order). */
+ * row_ws: cap + 1 floats, zero-filled once and then kept (per-row losses, reduced
+ * in a fixed order by the last block to finish; row_ws[cap] is its ticket). */
 int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const int32_t* d_n, int32_t cap,
                     const int32_t* labels, const int32_t* seeds, const int32_t* d_div, float* dlogits,
                     int32_t ldd, float* d_loss, float* row_ws, void* stream);
@@ -188,6 +189,13 @@ int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const int32_t* d
 int hg_record_batch(const int64_t* bp, const float* d_loss, uint32_t* d_maxdelta, float* loss_arr,
                     float* md_arr, void* stream);
 int hg_sgd(float* w, const float* g, int64_t n, float lr, uint32_t* d_maxdelta, void* stream);
+/* hg_sgd + hg_gemm_tc_prep_b_many + hg_record_batch in ONE launch: the tensor-core
+ * B images (host_desc: n_img <= 8 rows of int64 {B, ldb, trans_b, K1, K2, N, img},
+ * every B inside w, images fully built once before) are rewritten from the updated
+ * weights in the same pass; the last block records loss / max |dw| of the batch.
+ * ctl: 2 uint32 zero at rest (max |dw| bits, last-block ticket). */
+int hg_sgd_fused(float* w, const float* g, int64_t n, float lr, int32_t n_img, const int64_t* host_desc,
+                 uint32_t* ctl, const int64_t* bp, const float* d_loss, float* loss_arr, float* md_arr, void* stream);
 int hg_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
             int32_t* d_t, uint32_t* d_maxdelta, void* stream);
 

@@ -74,6 +74,73 @@ __global__ void k_prep_b_many(const __grid_constant__ PrepBatch pb) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// One launch at the end of a training step: SGD on the flat parameter buffer
+// (gnnmath.py:277-283) + max |w_new - w_old| (orchestrator.py:246-255), the
+// tensor-core B images of the UPDATED weights written in the same pass (each
+// weight lands at its swizzled hi/lo positions of every image built from it;
+// padding positions were zeroed by the initial full build and never change),
+// and — by the last block to finish — the per-batch record (loss, max delta
+// into the epoch arrays, orchestrator.py:527-544).  Replaces hg_sgd +
+// hg_gemm_tc_prep_b_many + hg_record_batch (three dependent launches).
+__device__ __forceinline__ void img_put(const PrepDesc& d, int64_t e, float v) {
+    const int64_t rows_ld = (int64_t)d.ldb;
+    const int row = (int)(e / rows_ld), col = (int)(e - (int64_t)row * rows_ld);
+    int k, n;
+    if (d.trans_b) { k = row; n = col; } else { n = row; k = col; }
+    if (n >= d.N || k >= d.K1 + d.K2) return;
+    int kt, kk;
+    if (k < d.K1) { kt = k >> 5; kk = k & 31; }
+    else { const int k2 = k - d.K1; kt = d.nk1 + (k2 >> 5); kk = k2 & 31; }
+    const int nt = n / d.bn, nn = n - nt * d.bn;
+    uint8_t* base = d.img + ((int64_t)nt * d.nk + kt) * (2 * d.bn * 128);
+    const uint32_t off = off_k(nn, kk >> 2) + (kk & 3) * 4;
+    *reinterpret_cast<float*>(base + off) = v;
+    *reinterpret_cast<float*>(base + d.bn * 128 + off) = tf32_lo(v);
+}
+
+struct FusedImages {
+    PrepDesc d[MAX_PREP];
+    int64_t lo[MAX_PREP], hi[MAX_PREP];  // [lo, hi): flat weight indices each image is built from
+};
+
+__global__ void __launch_bounds__(256) k_sgd_fused(const __grid_constant__ FusedImages pb, int n_img,
+                                                   float* __restrict__ w, const float* __restrict__ g, long long n,
+                                                   float lr, unsigned* __restrict__ ctl, const int64_t* __restrict__ bp,
+                                                   const float* __restrict__ d_loss, float* __restrict__ loss_arr,
+                                                   float* __restrict__ md_arr) {
+    __shared__ float s_m[8];
+    __shared__ bool s_last;
+    float md = 0.f;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float old = w[i];
+        const float nw = old - lr * g[i];
+        w[i] = nw;
+        md = fmaxf(md, fabsf(nw - old));
+        for (int j = 0; j < n_img; ++j)
+            if (i >= pb.lo[j] && i < pb.hi[j]) img_put(pb.d[j], i - pb.lo[j], nw);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o));
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = md;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.f;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmaxf(m, s_m[k]);
+        atomicMax(&ctl[0], __float_as_uint(m));  // non-negative floats order like their bits
+        __threadfence();
+        s_last = atomicAdd(&ctl[1], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        const int bi = (int)bp[3];  // BP_BATCH_IN_EPOCH
+        loss_arr[bi] = *d_loss;
+        md_arr[bi] = __uint_as_float(atomicExch(&ctl[0], 0u));
+        ctl[1] = 0u;
+    }
+}
+
 // B image: for every (N tile, K tile) the exact swizzled smem bytes of the
 // operand tile, hi then lo (2 * BN * 128 bytes), so CTAs stage B with plain
 // 16-byte cp.async copies.  Built once per weight update by k_prep_b.
@@ -600,4 +667,39 @@ extern "C" int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32
     k_wgrad_tc_reduce<<<n_src * hg_ceil_div(K * N, 32), 256, 0, s>>>(ws, K * N, n_src, chunks, rpc, d_M, M_cap, out1,
                                                                      out2);
     return hg_check_launch("wgrad_tc_reduce");
+}
+
+// hg_sgd + hg_gemm_tc_prep_b_many + hg_record_batch in one launch (see
+// k_sgd_fused).  host_desc: n_img rows of int64 {B, ldb, trans_b, K1, K2, N, img}
+// whose B lie inside w; ctl: 2 uint32 (max |dw| bits, last-block ticket), zero
+// at rest; bp/d_loss/loss_arr/md_arr as hg_record_batch.
+extern "C" int hg_sgd_fused(float* w, const float* g, int64_t n, float lr, int32_t n_img, const int64_t* host_desc,
+                            uint32_t* ctl, const int64_t* bp, const float* d_loss, float* loss_arr, float* md_arr,
+                            void* stream) {
+    if (n <= 0) return HG_OK;
+    if (n_img < 0 || n_img > MAX_PREP) { hg_set_error("sgd_fused: at most %d images", MAX_PREP); return HG_EINVAL; }
+    FusedImages pb{};
+    for (int i = 0; i < n_img; ++i) {
+        const int64_t* r = host_desc + 7 * i;
+        PrepDesc& d = pb.d[i];
+        d.B = reinterpret_cast<const float*>(r[0]);
+        d.ldb = (int)r[1];
+        d.trans_b = (int)r[2];
+        d.K1 = (int)r[3];
+        d.K2 = (int)r[4];
+        d.N = (int)r[5];
+        d.img = reinterpret_cast<uint8_t*>(r[6]);
+        d.bn = gemm_bn(d.N);
+        d.nk1 = hg_ceil_div(d.K1, 32);
+        d.nk = d.nk1 + (d.K2 > 0 ? hg_ceil_div(d.K2, 32) : 0);
+        d.nnt = hg_ceil_div(d.N, d.bn);
+        const int64_t off = (reinterpret_cast<const char*>(d.B) - reinterpret_cast<const char*>(w)) / 4;
+        const int64_t rows = d.trans_b ? (int64_t)(d.K1 + d.K2) : (int64_t)d.N;
+        if (off < 0 || off + rows * d.ldb > n) { hg_set_error("sgd_fused: image source outside w"); return HG_EINVAL; }
+        pb.lo[i] = off;
+        pb.hi[i] = off + rows * d.ldb;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    k_sgd_fused<<<hg_grid(n, 256, 4), 256, 0, s>>>(pb, n_img, w, g, n, lr, ctl, bp, d_loss, loss_arr, md_arr);
+    return hg_check_launch("sgd_fused");
 }

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
                                                          const int* __restrict__ tag_ctr, int* __restrict__ rank,
                                                          int* __restrict__ src_vertices, int* __restrict__ d_n_src,
                                                          unsigned long long* __restrict__ status,
-                                                         const int* __restrict__ d_gen) {
+                                                         const int* __restrict__ d_gen, int* __restrict__ outdeg) {
     __shared__ int s_warp[MS_THREADS / 32];
     __shared__ int s_prefix;
     const int n = hg_load_count(d_n, cap);
@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
         if (flags & (1u << k)) {
             rank[my0 + k] = local;
             src_vertices[local] = u[k];
+            if (outdeg) outdeg[local] = 0;  // counted by the relabel kernel that follows
             ++local;
         }
     }
@@ -475,8 +476,8 @@ extern "C" int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream) {
 
 // Dedup + relabel + per-dst sort (kernels.py:166-180, sampler.py:106-118).
 // ws: >= hg_dedup_ws_size(cap_dst, fanout) ints.  Produces src_vertices[0..n_src),
-// *d_n_src, sorted slots / slot_local, nself (nullable), outdeg (nullable; must be
-// zeroed over cap_src by the caller), and retires the first-occurrence tag.
+// *d_n_src, sorted slots / slot_local, nself (nullable), outdeg (nullable; entries
+// [0, n_src) reset by the mark/scan pass), and retires the first-occurrence tag.
 // ws layout (ints): rank[P] | pad | status (uint64)[tiles] | generation counter.
 // The workspace must be zero-filled once when allocated and then kept.
 extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
@@ -498,7 +499,7 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
     int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
     k_markscan<<<(unsigned)tiles, MS_THREADS, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
                                                       (const unsigned long long*)minpos, tag_ctr, flags, src_vertices,
-                                                      d_n_src, status, d_gen);
+                                                      d_n_src, status, d_gen, outdeg);
     if (fanout <= 32) {
         const int W = seg_width(fanout);
         const int grid = hg_grid((long long)cap_dst * W, 256, 8);

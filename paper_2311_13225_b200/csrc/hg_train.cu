@@ -26,10 +26,15 @@ namespace {
 // *d_div (the global batch size; == n on one GPU, gnnmath.py:273)
 // one warp per row; per-row losses land in row_loss, reduced in fixed order by
 // k_xent_reduce (deterministic, no float atomics)
+// One launch: per-row warps write dlogits and the row losses; the last block
+// to finish (threadfence + ticket in row_ws[cap]) reduces the row losses in a
+// fixed order (fp64), so the batch loss is deterministic, and re-arms the ticket.
 __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, int ld, int C, const int* d_n,
                                               int cap, const int* __restrict__ labels, const int* __restrict__ seeds,
                                               const int* __restrict__ d_div, float* __restrict__ dlogits, int ldd,
-                                              float* __restrict__ row_loss) {
+                                              float* __restrict__ row_loss, float* __restrict__ d_loss) {
+    __shared__ double s_part[8];
+    __shared__ bool s_last;
     const int n = hg_load_count(d_n, cap);
     const float grad_scale = 1.0f / (float)(d_div ? *d_div : (n > 0 ? n : 1));
     const int lane = threadIdx.x & 31;
@@ -52,22 +57,25 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
         }
         if (lane == 0) row_loss[r] = logf(se) - (z[y] - mx);  // -log softmax_y
     }
-}
-
-__global__ void __launch_bounds__(1024) k_xent_reduce(const float* __restrict__ row_loss, const int* d_n, int cap,
-                                                      float* __restrict__ d_loss) {
-    __shared__ double s_part[32];
-    const int n = hg_load_count(d_n, cap);
+    // ---- last block: fixed-order mean of the row losses ----
+    unsigned* ticket = reinterpret_cast<unsigned*>(row_loss + cap);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     double part = 0.0;
-    for (int r = threadIdx.x; r < n; r += blockDim.x) part += (double)row_loss[r];
+    for (int r = threadIdx.x; r < n; r += blockDim.x) part += (double)__ldcg(row_loss + r);
 #pragma unroll
     for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = part;
+    if (lane == 0) s_part[threadIdx.x >> 5] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
         double tot = 0.0;
         for (int k = 0; k < (int)(blockDim.x >> 5); ++k) tot += s_part[k];
         *d_loss = n > 0 ? (float)(tot / (double)n) : 0.f;
+        *ticket = 0u;
     }
 }
 
@@ -324,8 +332,8 @@ extern "C" int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const
                                int32_t ldd, float* d_loss, float* row_ws, void* stream) {
     if (cap <= 0) { hg_set_error("softmax_xent: empty batch"); return HG_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
-    k_xent<<<hg_ceil_div(cap, 8), 256, 0, s>>>(logits, ld, C, d_n, cap, labels, seeds, d_div, dlogits, ldd, row_ws);
-    k_xent_reduce<<<1, 1024, 0, s>>>(row_ws, d_n, cap, d_loss);
+    k_xent<<<hg_ceil_div(cap, 8), 256, 0, s>>>(logits, ld, C, d_n, cap, labels, seeds, d_div, dlogits, ldd, row_ws,
+                                               d_loss);
     return hg_check_launch("softmax_xent");
 }
 

@@ -226,8 +226,8 @@ class TrainEngine:
                        if (l > 0 and self.bwd_scatter) else None for l in range(self.L)]
         self.fx_flags = z32(1)
         self.d_loss = zf(1)
-        self.row_loss = zf(self.batch_cap)
-        self.d_maxdelta = z32(1)
+        self.row_loss = zf(self.batch_cap + 1)  # + the loss kernel's last-block ticket
+        self.d_maxdelta = z32(2)  # max |dw| bits + the fused update's last-block ticket
         self.loss_arr = zf(max(max_batches, 1))
         self.md_arr = zf(max(max_batches, 1))
         self.side = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
@@ -252,21 +252,29 @@ class TrainEngine:
         self.g_train = None
         self.enqueue_weight_images()
 
-    def enqueue_weight_images(self, stream=None):
-        """Rebuild every tensor-core B image from the current weights (one launch)."""
-        s = stream_ptr(stream)
+    def _image_jobs(self):
+        """(image, source weight pointer) of every tensor-core B image."""
         P = self.params
         jobs = []
         for l in range(self.L):
             jobs.append((self.img_fwd[l], ptr(P.view(l, 0))))
             for m, img in enumerate(self.img_dx[l]):
                 jobs.append((img, ptr(P.view(l, m))))
+        return jobs
+
+    def _image_desc(self, jobs):
+        return np.array([[w, self._ldb_of(img), img.trans_b, img.K1, img.K2, img.N, img.buf.data_ptr()]
+                         for img, w in jobs], dtype=np.int64)
+
+    def enqueue_weight_images(self, stream=None):
+        """Rebuild every tensor-core B image from the current weights (one launch)."""
+        s = stream_ptr(stream)
+        jobs = self._image_jobs()
         if dense.BACKEND == "simt":
             return
         for i in range(0, len(jobs), 8):
             part = jobs[i:i + 8]
-            desc = np.array([[w, self._ldb_of(img), img.trans_b, img.K1, img.K2, img.N, img.buf.data_ptr()]
-                             for img, w in part], dtype=np.int64)
+            desc = self._image_desc(part)
             _lib.call("hg_gemm_tc_prep_b_many", len(part), desc.ctypes.data, s)
 
     def _ldb_of(self, img):
@@ -414,6 +422,13 @@ class TrainEngine:
         mark("update")
         if self.allreduce is not None:
             self.allreduce(P.grad)
+        jobs = self._image_jobs()
+        if self.optimizer == "sgd" and dense.BACKEND != "simt" and len(jobs) <= 8:
+            # SGD + B images of the updated weights + batch record: one launch
+            desc = self._image_desc(jobs)
+            _lib.call("hg_sgd_fused", ptr(P.flat), ptr(P.grad), P.numel, self.lr, len(jobs), desc.ctypes.data,
+                      ptr(self.d_maxdelta), ptr(self.bp), ptr(self.d_loss), ptr(self.loss_arr), ptr(self.md_arr), s)
+            return
         if self.optimizer == "sgd":
             _lib.call("hg_sgd", ptr(P.flat), ptr(P.grad), P.numel, self.lr, ptr(self.d_maxdelta), s)
         else:

@@ -276,7 +276,7 @@ def loss_and_grad(logits, labels):
     lab = torch.as_tensor(np.asarray(labels, np.int32), device=dev)
     dl = torch.zeros_like(z)
     loss = torch.zeros(1, dtype=torch.float32, device=dev)
-    rows = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+    rows = torch.zeros(max(n, 1) + 1, dtype=torch.float32, device=dev)
     _lib.call("hg_softmax_xent", ptr(z), z.shape[1], C, None, n, ptr(lab), None, None, ptr(dl), z.shape[1], ptr(loss),
               ptr(rows), stream_ptr())
     return float(loss.item()), dl[:n, :C].double().cpu().numpy()

@@ -163,9 +163,6 @@ class LayerSampler:
         cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
         s = stream_ptr(stream)
         g = self.dg
-        if self.outdeg is not None:
-            with torch.cuda.stream(_as_stream(stream, self.dg.device)):
-                self.outdeg.zero_()
         _lib.call("hg_sample_layer", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
                   ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos.table),
                   ptr(self.minpos.tag), ptr(self.scratch), s)
