@@ -163,7 +163,8 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
 /* process-wide tuning knobs for the tensor-core kernels (key 1: MN-major descriptor offsets;
  * key 2: 1 = legacy cp.async GEMM kernels instead of the warp-specialised TMA pipelines;
  * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem;
- * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always) */
+ * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always;
+ * key 5: programmatic dependent launch of the step kernels, 1 (default; env HG_PDL=0 at load turns it off) / 0) */
 int hg_set_tuning(int32_t key, int32_t value);
 /* L2 residency: feature-gathering kernels launched after this call attach an
  * access-policy window [base, base+bytes) with persisting hits (hit_ratio of the

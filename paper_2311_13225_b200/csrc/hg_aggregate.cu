@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
     int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
     const int* __restrict__ nself, const int* __restrict__ outdeg, const uint8_t* __restrict__ inj,
     float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out, int ld_agg) {
+    hg_pdl_begin();
     constexpr bool GLOBAL = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL);
     constexpr bool GCN = (MODE == M_GCN_LOCAL || MODE == M_GCN_GLOBAL);
     const int n = hg_load_count(d_n, cap);
@@ -280,15 +281,21 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
                const int* nself, const int* outdeg, const uint8_t* inj, float* self_out, int ld_self,
                float* agg_out, int ld_agg) {
     // bottom layer (rows by global id): persisting L2 window over the hot feature rows
-    cudaLaunchAttribute attr[1];
-    const bool win = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL) && hg_l2_window_attr(&attr[0]);
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if ((MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL) && hg_l2_window_attr(&attr[na])) ++na;
+    if (hg_pdl_enabled()) {  // programmatic dependent launch (see hg_common.cuh)
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = g;
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
-    cfg.attrs = win ? attr : nullptr;
-    cfg.numAttrs = win ? 1 : 0;
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
 #define HG_FWD(L, V)                                                                                      \
     if (LPR == L && NV == V) {                                                                            \
         cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE>, hin, ld_in, F4, frontier, d_n, cap, f, counts,    \
@@ -505,6 +512,7 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
     const int* __restrict__ slot_local, const int* __restrict__ nself, const int* __restrict__ outdeg,
     unsigned long long* __restrict__ acc, int* __restrict__ d_flags, const float* __restrict__ hmask, int ld_hmask,
     const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n_dst, cap_dst);
     const int lane = threadIdx.x & 31;
     const int lr = lane & (LPR - 1);
@@ -571,6 +579,7 @@ __global__ void __launch_bounds__(256) k_bwd_finish(
     unsigned long long* __restrict__ acc, int F4, const float* __restrict__ dself, int ld_dself, const int* d_n_dst,
     int cap_dst, const int* d_n_src, int cap_src, const int* __restrict__ outdeg, const float* __restrict__ hmask,
     int ld_hmask, const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx) {
+    hg_pdl_begin();
     const int n_src = hg_load_count(d_n_src, cap_src);
     const int n_dst = hg_load_count(d_n_dst, cap_dst);
     const int lane = threadIdx.x & 31;
@@ -609,10 +618,10 @@ int launch_scatter(int LPR, int NV, dim3 g, dim3 g2, cudaStream_t s, const float
                    const uint8_t* inj, unsigned long long* acc, float* dx, int ld_dx, int* d_flags) {
 #define HG_SC(L, V)                                                                                            \
     if (LPR == L && NV == V) {                                                                                 \
-        k_bwd_scatter<L, V, GCN><<<g, 256, 0, s>>>(dagg, ld_dagg, F4, frontier, d_n_dst, cap_dst, f, counts,   \
+        hg_launch(k_bwd_scatter<L, V, GCN>, g, 256, 0, s, dagg, ld_dagg, F4, frontier, d_n_dst, cap_dst, f, counts,   \
                                                    slot_g, slot_local, nself, outdeg, acc, d_flags, hmask,     \
                                                    ld_hmask, inj, dx, ld_dx);                                  \
-        k_bwd_finish<L, V><<<g2, 256, 0, s>>>(acc, F4, dself, ld_dself, d_n_dst, cap_dst, d_n_src, cap_src,    \
+        hg_launch(k_bwd_finish<L, V>, g2, 256, 0, s, acc, F4, dself, ld_dself, d_n_dst, cap_dst, d_n_src, cap_src,    \
                                               outdeg, hmask, ld_hmask, inj, dx, ld_dx);                        \
         return HG_OK;                                                                                          \
     }

@@ -57,6 +57,39 @@ static inline int hg_grid(long long work, int per_block, int max_blocks_per_sm =
     return (int)g;
 }
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): step kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization (programmatic edges once
+// captured into a graph), so a kernel's CTAs are scheduled while its
+// predecessor drains.  Every such kernel calls hg_pdl_begin() first:
+// griddepcontrol.wait blocks until the predecessor grid has completed and its
+// writes are visible (so correctness never depends on the trigger), then
+// launch_dependents lets the next kernel start launching.  No-ops when the
+// kernel was launched without the attribute.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void hg_pdl_begin() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+bool hg_pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t hg_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = hg_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // set by every entry point; read through hg_last_error()
 void hg_set_error(const char* fmt, ...);
 int hg_check_launch(const char* what);

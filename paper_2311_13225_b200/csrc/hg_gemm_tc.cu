@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(256) k_sgd_fused(const __grid_constant__ Fused
                                                    float lr, unsigned* __restrict__ ctl, const int64_t* __restrict__ bp,
                                                    const float* __restrict__ d_loss, float* __restrict__ loss_arr,
                                                    float* __restrict__ md_arr) {
+    hg_pdl_begin();
     __shared__ float s_m[8];
     __shared__ bool s_last;
     float md = 0.f;
@@ -616,6 +617,7 @@ extern "C" int hg_set_tuning(int32_t key, int32_t value) {
     if (key == 2) { g_legacy = value ? 1 : 0; return HG_OK; }
     if (key == 3) { hg_tma_set_fwd_form(value ? 1 : 0); return HG_OK; }
     if (key == 4) { g_skinny = value ? 1 : 0; return HG_OK; }
+    if (key == 5) { hg_set_pdl(value); return HG_OK; }
     if (key == 9) { hg_tma_set_dbg(value); return HG_OK; }
     hg_set_error("set_tuning: unknown key %d", key);
     return HG_EINVAL;
@@ -700,6 +702,6 @@ extern "C" int hg_sgd_fused(float* w, const float* g, int64_t n, float lr, int32
         pb.hi[i] = off + rows * d.ldb;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    k_sgd_fused<<<hg_grid(n, 256, 4), 256, 0, s>>>(pb, n_img, w, g, n, lr, ctl, bp, d_loss, loss_arr, md_arr);
+    hg_launch(k_sgd_fused, hg_grid(n, 256, 4), 256, 0, s, pb, n_img, w, g, n, lr, ctl, bp, d_loss, loss_arr, md_arr);
     return hg_check_launch("sgd_fused");
 }

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
            const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
            int M_cap, int act) {
+    hg_pdl_begin();
     constexpr int S = fwd_stages<BN>();
     constexpr int STAGE = fwd_stage_bytes<BN>();
     constexpr int B_BYTES = 2 * BN * 128;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
               const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
               int M_cap, int act) {
+    hg_pdl_begin();
     constexpr int S = ts_stages<BN>();
     constexpr int STAGE = ts_stage_bytes<BN>();
     constexpr int B_BYTES = 2 * BN * 128;
@@ -413,6 +415,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
             int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
+    hg_pdl_begin();
     constexpr int S = wg_stages<BN>();
     constexpr int STAGE = wg_stage_bytes<BN>();
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
@@ -555,6 +558,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
 __global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restrict__ partial, int KN, int n_chunks,
                                                           const int* __restrict__ d_M, int M_cap,
                                                           float* __restrict__ out1, float* __restrict__ out2) {
+    hg_pdl_begin();
     __shared__ float s_part[8][33];
     const int M = hg_load_count(d_M, M_cap);
     const int rpc = M > 0 ? wg_rows_per_chunk(M, n_chunks) : 1;
@@ -629,7 +633,7 @@ int launch_fwd(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
-    k_gemm_tma<BN><<<dim3(gx, n_nt), FWD_THREADS, smem, s>>>(m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
+    hg_launch(k_gemm_tma<BN>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
     return hg_check_launch("gemm_tma");
 }
 
@@ -644,7 +648,7 @@ int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, co
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
-    k_gemm_tma_ts<BN><<<dim3(gx, n_nt), FWD_THREADS, smem, s>>>(m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
+    hg_launch(k_gemm_tma_ts<BN>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
     return hg_check_launch("gemm_tma_ts");
 }
 
@@ -659,7 +663,7 @@ int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMa
         cudaFuncSetAttribute(k_wgrad_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    k_wgrad_tma<BN><<<grid, WG_THREADS, smem, s>>>(m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial, lbo, sbo);
+    hg_launch(k_wgrad_tma<BN>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial, lbo, sbo);
     return hg_check_launch("wgrad_tma");
 }
 
@@ -730,7 +734,7 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
         else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
         if (rc) return rc;
     }
-    k_wgrad_tma_reduce<<<n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s>>>(ws, K * N, n_chunks, d_M, M_cap,
+    hg_launch(k_wgrad_tma_reduce, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K * N, n_chunks, d_M, M_cap,
                                                                                 out1, out2);
     return hg_check_launch("wgrad_tma_reduce");
 }

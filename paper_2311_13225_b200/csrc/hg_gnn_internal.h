@@ -36,3 +36,5 @@ int hg_wgrad_skinny_launch(const float* A1, int lda1, const float* A2, int lda2,
 
 // access-policy window of the persisting feature rows (hg_util.cu); false if unset
 bool hg_l2_window_attr(cudaLaunchAttribute* a);
+
+void hg_set_pdl(int v);

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // K1-K3: bit-exact k-hop block sampling on an HBM-resident CSR.
 //
 // Replaces the reference's per-layer block construction
@@ -31,6 +32,19 @@
 
 namespace {
 
+// CTAs per SM for the draw / relabel grids (env HG_SAMPLE_CTAS_PER_SM, default 8):
+// fewer leaves SM room for the training stream's kernels that run concurrently
+int hg_sample_ctas_per_sm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HG_SAMPLE_CTAS_PER_SM");
+        v = e ? atoi(e) : 8;
+        if (v < 1) v = 1;
+        if (v > 8) v = 8;
+    }
+    return v;
+}
+
 __device__ __forceinline__ uint32_t fo_tag(const int* ctr) { return 0xFFFFFFFEu - (uint32_t)(*ctr); }
 __device__ __forceinline__ unsigned long long fo_key(uint32_t tag, long long pos) {
     return ((unsigned long long)tag << 32) | (unsigned long long)(uint32_t)pos;
@@ -47,6 +61,7 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
                                                     int layer, int* __restrict__ counts,
                                                     int* __restrict__ slots, unsigned long long* __restrict__ minpos,
                                                     const int* __restrict__ tag_ctr) {
+    hg_pdl_begin();
     __shared__ int s_last[256];
     const int n = hg_load_count(d_n, cap);
     const uint32_t tag = fo_tag(tag_ctr);
@@ -112,6 +127,7 @@ __global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __r
                              const uint64_t* __restrict__ d_seed, int layer, int* __restrict__ counts,
                              int* __restrict__ slots, unsigned long long* __restrict__ minpos,
                              const int* __restrict__ tag_ctr, int* __restrict__ scratch) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     const uint32_t tag = fo_tag(tag_ctr);
     const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
@@ -197,6 +213,7 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
                                                          int* __restrict__ src_vertices, int* __restrict__ d_n_src,
                                                          unsigned long long* __restrict__ status,
                                                          const int* __restrict__ d_gen, int* __restrict__ outdeg) {
+    hg_pdl_begin();
     __shared__ int s_warp[MS_THREADS / 32];
     __shared__ int s_prefix;
     const int n = hg_load_count(d_n, cap);
@@ -302,6 +319,7 @@ __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict_
                                                           const int* __restrict__ rank,
                                                           int* __restrict__ nself, int* __restrict__ outdeg,
                                                           int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // retire this use of the table and of the scan status
         *tag_ctr += 1;
@@ -343,6 +361,7 @@ __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* 
                                    int* __restrict__ slot_local, const unsigned long long* __restrict__ minpos,
                                    const int* __restrict__ rank, int* __restrict__ nself,
                                    int* __restrict__ outdeg, int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *tag_ctr += 1;
@@ -452,16 +471,16 @@ extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, c
     if (cap_dst == 0) return HG_OK;
     if (fanout <= 32) {
         const int W = seg_width(fanout);
-        const int grid = hg_grid((long long)cap_dst * W, 256, 8);
+        const int grid = hg_grid((long long)cap_dst * W, 256, hg_sample_ctas_per_sm());
         switch (W) {
-            case 4: k_sample_seg<4><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
-            case 8: k_sample_seg<8><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
-            case 16: k_sample_seg<16><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
-            default: k_sample_seg<32><<<grid, 256, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            case 4: hg_launch(k_sample_seg<4>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            case 8: hg_launch(k_sample_seg<8>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            case 16: hg_launch(k_sample_seg<16>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            default: hg_launch(k_sample_seg<32>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
         }
     } else {
         if (!scratch) { hg_set_error("sample_layer: fanout > 32 needs scratch"); return HG_EINVAL; }
-        k_sample_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(offsets, targets, frontier, d_n_dst, cap_dst, fanout,
+        hg_launch(k_sample_seq, hg_grid(cap_dst, 128, 8), 128, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout,
                                                               d_seed, layer, counts, slots, (unsigned long long*)minpos,
                                                               tag_ctr, scratch);
     }
@@ -497,20 +516,20 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
     int* flags = ws;  // rank of each first-occurrence position
     unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + ((P + 1) & ~1LL));
     int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
-    k_markscan<<<(unsigned)tiles, MS_THREADS, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
+    hg_launch(k_markscan, (unsigned)tiles, MS_THREADS, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots,
                                                       (const unsigned long long*)minpos, tag_ctr, flags, src_vertices,
                                                       d_n_src, status, d_gen, outdeg);
     if (fanout <= 32) {
         const int W = seg_width(fanout);
-        const int grid = hg_grid((long long)cap_dst * W, 256, 8);
+        const int grid = hg_grid((long long)cap_dst * W, 256, hg_sample_ctas_per_sm());
         switch (W) {
-            case 4: k_relabel_sort_seg<4><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
-            case 8: k_relabel_sort_seg<8><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
-            case 16: k_relabel_sort_seg<16><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
-            default: k_relabel_sort_seg<32><<<grid, 256, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            case 4: hg_launch(k_relabel_sort_seg<4>, grid, 256, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            case 8: hg_launch(k_relabel_sort_seg<8>, grid, 256, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            case 16: hg_launch(k_relabel_sort_seg<16>, grid, 256, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
+            default: hg_launch(k_relabel_sort_seg<32>, grid, 256, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, (const unsigned long long*)minpos, flags, nself, outdeg, tag_ctr, d_gen); break;
         }
     } else {
-        k_relabel_sort_seq<<<hg_grid(cap_dst, 128, 8), 128, 0, s>>>(frontier, d_n_dst, cap_dst, fanout, counts, slots,
+        hg_launch(k_relabel_sort_seq, hg_grid(cap_dst, 128, 8), 128, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots,
                                                                     slot_local, (const unsigned long long*)minpos,
                                                                     flags, nself, outdeg, tag_ctr, d_gen);
     }

@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(256) k_xent(const float* __restrict__ logits, 
                                               int cap, const int* __restrict__ labels, const int* __restrict__ seeds,
                                               const int* __restrict__ d_div, float* __restrict__ dlogits, int ldd,
                                               float* __restrict__ row_loss, float* __restrict__ d_loss) {
+    hg_pdl_begin();
     __shared__ double s_part[8];
     __shared__ bool s_last;
     const int n = hg_load_count(d_n, cap);
@@ -151,6 +152,7 @@ __global__ void k_store_put(const int* __restrict__ ids, const int* d_n, int cap
                             int ld_emb, int H, const int* __restrict__ slot_of, float* __restrict__ tab,
                             int* __restrict__ ver, int* __restrict__ stamp, int version, int stamp_val,
                             int* __restrict__ d_puts) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -177,6 +179,7 @@ __global__ void k_store_lookup(const int* __restrict__ dst, const int* d_n, int 
                                uint8_t* __restrict__ inj_mask, int* __restrict__ inj_slot,
                                int* __restrict__ batch_hits, int* __restrict__ batch_miss,
                                int* __restrict__ batch_warm, unsigned long long* __restrict__ stats) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     const int cpu_tag = (int)bp[BP_CPU_TAG];
     const int sel = (int)bp[BP_TABLE_SEL];
@@ -233,6 +236,7 @@ __global__ void k_store_lookup(const int* __restrict__ dst, const int* d_n, int 
 __global__ void k_inject(const uint8_t* __restrict__ inj_mask, const int* __restrict__ inj_slot, const int* d_n,
                          int cap, const int64_t* __restrict__ bp, const float* __restrict__ tab0,
                          const float* __restrict__ tab1, int H, float* __restrict__ h, int ldh) {
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     const float* tab = bp[BP_TABLE_SEL] ? tab1 : tab0;
     const int lane = threadIdx.x & 31;
@@ -332,7 +336,7 @@ extern "C" int hg_softmax_xent(const float* logits, int32_t ld, int32_t C, const
                                int32_t ldd, float* d_loss, float* row_ws, void* stream) {
     if (cap <= 0) { hg_set_error("softmax_xent: empty batch"); return HG_EINVAL; }
     cudaStream_t s = (cudaStream_t)stream;
-    k_xent<<<hg_ceil_div(cap, 8), 256, 0, s>>>(logits, ld, C, d_n, cap, labels, seeds, d_div, dlogits, ldd, row_ws,
+    hg_launch(k_xent, hg_ceil_div(cap, 8), 256, 0, s, logits, ld, C, d_n, cap, labels, seeds, d_div, dlogits, ldd, row_ws,
                                                d_loss);
     return hg_check_launch("softmax_xent");
 }
@@ -362,7 +366,7 @@ extern "C" int hg_store_put(const int32_t* ids, const int32_t* d_n, int32_t cap,
                             int32_t H, const int32_t* slot_of, float* tab, int32_t* ver, int32_t* stamp,
                             int32_t version, int32_t stamp_val, int32_t* d_puts, void* stream) {
     if (cap <= 0) return HG_OK;
-    k_store_put<<<hg_grid((long long)cap * 32, 256, 8), 256, 0, (cudaStream_t)stream>>>(
+    hg_launch(k_store_put, hg_grid((long long)cap * 32, 256, 8), 256, 0, (cudaStream_t)stream, 
         ids, d_n, cap, emb, ld_emb, H, slot_of, tab, ver, stamp, version, stamp_val, d_puts);
     return hg_check_launch("store_put");
 }
@@ -373,7 +377,7 @@ extern "C" int hg_store_lookup(const int32_t* dst, const int32_t* d_n, int32_t c
                                uint8_t* inj_mask, int32_t* inj_slot, int32_t* batch_hits, int32_t* batch_miss,
                                int32_t* batch_warm, uint64_t* stats, void* stream) {
     if (cap <= 0) return HG_OK;
-    k_store_lookup<<<hg_grid(cap, 256, 8), 256, 0, (cudaStream_t)stream>>>(
+    hg_launch(k_store_lookup, hg_grid(cap, 256, 8), 256, 0, (cudaStream_t)stream, 
         dst, d_n, cap, bp, cpu_tag_of, slot_of, ver0, ver1, stamp0, stamp1, gap_bound, inj_mask, inj_slot, batch_hits,
         batch_miss, batch_warm, (unsigned long long*)stats);
     return hg_check_launch("store_lookup");
@@ -383,7 +387,7 @@ extern "C" int hg_inject_rows(const uint8_t* inj_mask, const int32_t* inj_slot, 
                               const int64_t* bp, const float* tab0, const float* tab1, int32_t H, float* h,
                               int32_t ldh, void* stream) {
     if (cap <= 0) return HG_OK;
-    k_inject<<<hg_grid((long long)cap * 32, 256, 8), 256, 0, (cudaStream_t)stream>>>(inj_mask, inj_slot, d_n, cap, bp,
+    hg_launch(k_inject, hg_grid((long long)cap * 32, 256, 8), 256, 0, (cudaStream_t)stream, inj_mask, inj_slot, d_n, cap, bp,
                                                                                      tab0, tab1, H, h, ldh);
     return hg_check_launch("inject_rows");
 }

@@ -347,3 +347,16 @@ extern "C" int hg_set_l2_persist(const void* base, int64_t bytes, float hit_rati
     g_l2_hit = hit_ratio < 0.f ? 0.f : (hit_ratio > 1.f ? 1.f : hit_ratio);
     return HG_OK;
 }
+
+// PDL switch (hg_set_tuning key 5; env HG_PDL=0 turns it off at load)
+namespace {
+int g_pdl = -1;
+}
+bool hg_pdl_enabled() {
+    if (g_pdl < 0) {
+        const char* e = getenv("HG_PDL");
+        g_pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_pdl == 1;
+}
+void hg_set_pdl(int v) { g_pdl = v ? 1 : 0; }
