@@ -176,7 +176,7 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
                 tmem_ld16_nowait(ta, r0);
                 tmem_ld16_nowait(ta + 16, r1);
                 tmem_wait_ld();
-                if (gm < M && n0 + c0 < N) {
+                if (gm < M && n0 + c0 < N && !(c_dbg & 4)) {
                     float* crow = C + (int64_t)gm * ldc + n0 + c0;
                     const int lim = N - (n0 + c0);
                     if (vec && lim >= 32) {
@@ -224,26 +224,33 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
 // written, A read by 8 of 12 MMAs, lo written) to ~72 KB, which is what bounds
 // the SS form at N = 64.  TMEM: 2 accumulators (2*BN columns) + S A stages of
 // 64 columns (hi 32 | lo 32).
+// RESB: the whole B image (nk tiles) stays resident in shared memory, loaded
+// once per CTA, and the ring holds A tiles only (B was re-streamed from L2 for
+// every K tile of every output tile, doubling the SM's ingress).
 template <int BN>
 __host__ __device__ constexpr int ts_stages() { return BN <= 64 ? 6 : 4; }
-template <int BN>
-__host__ __device__ constexpr int ts_stage_bytes() { return A_BYTES + 2 * BN * 128; }
+template <int BN, bool RESB>
+__host__ __device__ constexpr int ts_stage_bytes() { return RESB ? A_BYTES : A_BYTES + 2 * BN * 128; }
+constexpr int RESB_MAX_BYTES = 128 * 1024;
 
-template <int BN>
+template <int BN, bool RESB>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
 k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
               const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
               int M_cap, int act) {
     hg_pdl_begin();
     constexpr int S = ts_stages<BN>();
-    constexpr int STAGE = ts_stage_bytes<BN>();
+    constexpr int STAGE = ts_stage_bytes<BN, RESB>();
     constexpr int B_BYTES = 2 * BN * 128;
     constexpr int B_TILE = BN * 128;
     constexpr uint32_t A_COL0 = 2 * BN;  // first TMEM column of the A stages
     static_assert(2 * BN + S * 64 <= 512, "TMEM budget");
     constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t full[S], splt[S], empty[S], tfull[2], tempty[2];
+    // RESB: afree[st] (split warps done reading smem stage st) releases the A
+    // ring to the producer independently of the MMAs; empty[st] then only
+    // guards the TMEM A stage the split warps write next
+    __shared__ uint64_t full[S], splt[S], empty[S], afree[S], tfull[2], tempty[2], bfull;
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int M = hg_load_count(d_M, M_cap);
@@ -267,6 +274,9 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
+        mbar_init(&bfull, 1);
+#pragma unroll
+        for (int i = 0; i < S; ++i) mbar_init(&afree[i], 4);
         mbar_init_fence();
         tma_prefetch_desc(&tmA1);
         if (nk2) tma_prefetch_desc(&tmA2);
@@ -280,20 +290,26 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
             const uint8_t* bimg = Bimg + (int64_t)blockIdx.y * nk * B_BYTES;
+            if (RESB) {  // whole B image once, behind the A ring
+                mbar_expect_tx(&bfull, (uint32_t)(nk * B_BYTES));
+                for (int kt = 0; kt < nk; ++kt)
+                    bulk_load(smem_u32(smem + S * STAGE + kt * B_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &bfull);
+            }
             for (int it = 0; it < iters; ++it) {
                 const int st = it % S;
-                if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
+                if (it >= S) mbar_wait(RESB ? &afree[st] : &empty[st], (uint32_t)(((it / S) - 1) & 1));
                 const int tile = it / nk, kt = it - tile * nk;
                 const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
                 uint8_t* base = smem + st * STAGE;
-                mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
+                mbar_expect_tx(&full[st], RESB ? A_BYTES : A_BYTES + B_BYTES);
                 if (kt < nk1) tma_load_2d(smem_u32(base), &tmA1, kt * 32, m0, &full[st]);
                 else tma_load_2d(smem_u32(base), &tmA2, (kt - nk1) * 32, m0, &full[st]);
-                bulk_load(smem_u32(base + A_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &full[st]);
+                if (!RESB) bulk_load(smem_u32(base + A_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &full[st]);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer (A from TMEM)
+            if (RESB) mbar_wait(&bfull, 0u);
             int it = 0;
             for (int tile = 0; tile < n_my; ++tile) {
                 const int acc = tile & 1;
@@ -305,9 +321,12 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
                     mbar_wait(&splt[st], (uint32_t)((it / S) & 1));
                     tc_fence_after();
                     const uint32_t ta = tmem + A_COL0 + (uint32_t)(st * 64);
-                    const uint32_t b_hi = smem_u32(smem + st * STAGE + A_BYTES), b_lo = b_hi + B_TILE;
+                    const uint32_t b_hi = RESB ? smem_u32(smem + S * STAGE + kt * B_BYTES)
+                                               : smem_u32(smem + st * STAGE + A_BYTES);
+                    const uint32_t b_lo = b_hi + B_TILE;
 #pragma unroll
                     for (int s = 0; s < 4; ++s) {
+                        if (c_dbg & 1) break;
                         const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
                         mma_tf32_ts(d, ta + s * 8, dbh, IDESC, (kt | s) ? 1u : 0u);
                         mma_tf32_ts(d, ta + s * 8, dbl, IDESC, 1u);
@@ -325,6 +344,15 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             const int st = it % S;
             mbar_wait(&full[st], (uint32_t)((it / S) & 1));
             const uint8_t* base = smem + st * STAGE;
+            if (c_dbg & 2) {  // profiling: no split work (same hand-offs)
+                __syncwarp();
+                if (RESB) {
+                    if (lane == 0) mbar_arrive(&afree[st]);
+                    if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
+                }
+                if (lane == 0) mbar_arrive(&splt[st]);
+                continue;
+            }
             uint32_t hi[32], lo[32];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -336,6 +364,15 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             }
 #pragma unroll
             for (int k = 0; k < 32; ++k) lo[k] = __float_as_uint(tf32_lo(__uint_as_float(hi[k])));
+            if (RESB) {  // smem stage consumed: hand it back to the producer (generic-proxy
+                // reads before the next async-proxy TMA write), then wait for the MMAs
+                // still reading this TMEM stage's previous contents
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&afree[st]);
+                if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
+                tc_fence_after();
+            }
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(st * 64);
             tmem_st32(ta, hi);
             tmem_st32(ta + 32, lo);
@@ -360,7 +397,7 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
                 tmem_ld16_nowait(ta, r0);
                 tmem_ld16_nowait(ta + 16, r1);
                 tmem_wait_ld();
-                if (gm < M && n0 + c0 < N) {
+                if (gm < M && n0 + c0 < N && !(c_dbg & 4)) {
                     float* crow = C + (int64_t)gm * ldc + n0 + c0;
                     const int lim = N - (n0 + c0);
                     if (vec && lim >= 32) {
@@ -637,18 +674,31 @@ int launch_fwd(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const
     return hg_check_launch("gemm_tma");
 }
 
+int g_resb = 0;  // resident-B TS form when the image fits (hg_set_tuning key 6; measured no faster, off)
+
 template <int BN>
 int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, int nk1,
                   int nk2, const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
-    const int smem = ts_stages<BN>() * ts_stage_bytes<BN>() + 1024;
+    const int nk = nk1 + nk2;
+    const bool resb = g_resb && nk * 2 * BN * 128 <= RESB_MAX_BYTES;
+    const int smem = resb ? ts_stages<BN>() * ts_stage_bytes<BN, true>() + nk * 2 * BN * 128 + 1024
+                          : ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const int mx = ts_stages<BN>() * ts_stage_bytes<BN, true>() + RESB_MAX_BYTES + 1024;
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024);
         attr = true;
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
-    hg_launch(k_gemm_tma_ts<BN>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
+    if (resb)
+        hg_launch(k_gemm_tma_ts<BN, true>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M,
+                  M_cap, act);
+    else
+        hg_launch(k_gemm_tma_ts<BN, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N,
+                  d_M, M_cap, act);
     return hg_check_launch("gemm_tma_ts");
 }
 
@@ -670,6 +720,7 @@ int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMa
 }  // namespace
 
 void hg_tma_set_fwd_form(int v) { g_fwd_form = v; }
+void hg_tma_set_resb(int v) { g_resb = v ? 1 : 0; }
 void hg_tma_set_dbg(int v) { cudaMemcpyToSymbol(c_dbg, &v, sizeof(int)); }
 
 int hg_tma_gemm_bn(int N) {

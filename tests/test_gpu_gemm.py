@@ -22,15 +22,18 @@ def _ld(k):
     return (k + 3) // 4 * 4
 
 
-@pytest.fixture(params=["tc", "skinny"])
+@pytest.fixture(params=["tc", "tc_resb", "skinny"])
 def path(request):
-    """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores only (default), or the
-    optional SIMT latency kernels for small M (hg_set_tuning key 4)."""
+    """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores (default), the resident-B
+    TS form (hg_set_tuning key 6), or the optional SIMT latency kernels for
+    small M (key 4)."""
     from paper_2311_13225_b200 import _lib
     lib = _lib.load()
     lib.hg_set_tuning(4, 1 if request.param == "skinny" else 0)
+    lib.hg_set_tuning(6, 1 if request.param == "tc_resb" else 0)
     yield request.param
     lib.hg_set_tuning(4, 0)
+    lib.hg_set_tuning(6, 0)
 
 
 @pytest.mark.parametrize("fn", ["hg_gemm_tc", "hg_gemm_f32"])

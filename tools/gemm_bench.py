@@ -56,8 +56,10 @@ def main():
     ref = None
     fwd_bytes = M * 2 * K * 4 + M * N * 4
     wg_bytes = M * 2 * K * 4 + M * N * 4
-    for name, legacy, form, sk in (("legacy cp.async", 1, 1, 0), ("tma SS", 0, 0, 0), ("tma TS", 0, 1, 0),
-                                   ("skinny simt", 0, 1, 1)):
+    for name, legacy, form, sk, resb in (("legacy cp.async", 1, 1, 0, 0), ("tma SS", 0, 0, 0, 0),
+                                         ("tma TS", 0, 1, 0, 0), ("tma TS resident B", 0, 1, 0, 1),
+                                         ("skinny simt", 0, 1, 1, 1)):
+        lib.hg_set_tuning(6, resb)
         lib.hg_set_tuning(4, sk)
         lib.hg_set_tuning(2, legacy)
         lib.hg_set_tuning(3, form)
@@ -90,6 +92,11 @@ def main():
                    _lib.call("hg_wgrad_f32", ptr(A2[r % R]), LD, K, ptr(G[r % R]), N, N, ptr(dM), M, ptr(o2), 1.0,
                              ptr(wsf), cs()))
     print(f"{'simt fp32':16s} fwd {timeit(f):7.2f} us   wgrad {timeit(g):7.2f} us")
+    for dbg, what in ((1, "no MMA"), (2, "no split"), (3, "loads only"), (4, "no stores"), (7, "loads, no st")):
+        lib.hg_set_tuning(9, dbg)
+        f = lambda r: _lib.call("hg_gemm_tc", ptr(A1[r % R]), LD, K, ptr(A2[r % R]), LD, K, ptr(img), ptr(C), N, N,  # noqa
+                                ptr(dM), M, 1, torch.cuda.current_stream().cuda_stream)
+        print(f"fwd TS resB {what:12s} {timeit(f):7.2f} us")
     for dbg, what in ((1, "no MMA"), (2, "no split"), (3, "loads only")):
         lib.hg_set_tuning(9, dbg)
         g = lambda r: _lib.call("hg_wgrad_tc", ptr(A1[r % R]), LD, ptr(A2[r % R]), LD, K, ptr(G[r % R]), N, N,  # noqa
