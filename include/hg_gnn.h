@@ -66,10 +66,11 @@ int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream);
  *      *d_n_src, slots re-ordered by local src id with slot_local, per-dst
  *      non-self counts `nself` (gnnmath.py:145-154; nullable) and block
  *      out-degrees `outdeg` (gnnmath.py:96; nullable; entries [0, n_src) are reset by the call), and
- *      bumps *tag_ctr so the next use of minpos starts clean. */
+ *      bumps *tag_ctr so the next use of minpos starts clean (first-occurrence
+ *      entries are left holding their local id under the reserved tag 0xFFFFFFFF). */
 int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout);
 int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                     const int32_t* counts, int32_t* slots, int32_t* slot_local, const uint64_t* minpos,
+                     const int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
                      int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
                      int32_t* outdeg, int32_t* ws, void* stream);
 

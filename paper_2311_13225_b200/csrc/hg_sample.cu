@@ -45,6 +45,8 @@ int hg_sample_ctas_per_sm() {
     return v;
 }
 
+constexpr unsigned long long FO_RANKED = 0xFFFFFFFF00000000ull;  // tag of rewritten (ranked) entries
+
 __device__ __forceinline__ uint32_t fo_tag(const int* ctr) { return 0xFFFFFFFEu - (uint32_t)(*ctr); }
 __device__ __forceinline__ unsigned long long fo_key(uint32_t tag, long long pos) {
     return ((unsigned long long)tag << 32) | (unsigned long long)(uint32_t)pos;
@@ -208,7 +210,7 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__ frontier, const int* d_n, int cap,
                                                          int f, const int* __restrict__ counts,
                                                          const int* __restrict__ slots,
-                                                         const unsigned long long* __restrict__ minpos,
+                                                         unsigned long long* __restrict__ minpos,
                                                          const int* __restrict__ tag_ctr, int* __restrict__ rank,
                                                          int* __restrict__ src_vertices, int* __restrict__ d_n_src,
                                                          unsigned long long* __restrict__ status,
@@ -298,7 +300,12 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
 #pragma unroll
     for (int k = 0; k < MS_ITEMS; ++k) {
         if (flags & (1u << k)) {
-            rank[my0 + k] = local;
+            // the first occurrence's table entry becomes its local id under the
+            // reserved tag 0xFFFFFFFF: larger than every live key (tags count down),
+            // so later atomicMin's always win, never equal to a position key that
+            // another tile compares against, and the relabel pass reads local ids
+            // with one load instead of minpos -> rank
+            minpos[u[k]] = FO_RANKED | (unsigned)local;
             src_vertices[local] = u[k];
             if (outdeg) outdeg[local] = 0;  // counted by the relabel kernel that follows
             ++local;
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict_
         int u = -1, loc = HG_INT_MAX;
         if (sub < cnt) {
             u = slots[(int64_t)i * f + sub];
-            loc = rank[(uint32_t)minpos[u]];
+            loc = (int)(uint32_t)minpos[u];  // local id (rewritten by k_markscan)
         }
         int r = 0;
         for (int k = 0; k < cnt; ++k) {
@@ -374,7 +381,7 @@ __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* 
         int* lp = slot_local + (int64_t)i * f;
         int ns = 0;
         for (int j = 0; j < cnt; ++j) {
-            lp[j] = rank[(uint32_t)minpos[sp[j]]];
+            lp[j] = (int)(uint32_t)minpos[sp[j]];
             ns += sp[j] != v;
         }
         for (int j = 1; j < cnt; ++j) {  // stable insertion sort by local id
@@ -506,7 +513,7 @@ extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
 }
 
 extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                                const int32_t* counts, int32_t* slots, int32_t* slot_local, const uint64_t* minpos,
+                                const int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
                                 int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
                                 int32_t* outdeg, int32_t* ws, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
@@ -517,7 +524,7 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
     unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + ((P + 1) & ~1LL));
     int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
     hg_launch(k_markscan, (unsigned)tiles, MS_THREADS, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots,
-                                                      (const unsigned long long*)minpos, tag_ctr, flags, src_vertices,
+                                                      (unsigned long long*)minpos, tag_ctr, flags, src_vertices,
                                                       d_n_src, status, d_gen, outdeg);
     if (fanout <= 32) {
         const int W = seg_width(fanout);

@@ -93,7 +93,10 @@ class DeviceGraph:
             feats = np.asarray(features)
             V, F = feats.shape
             self.feat_dim = F
-            self.feat_ld = pad4(F)
+            # row stride: multiple of HG_FEAT_ALIGN floats (default 4 = 16-byte rows
+            # for float4 loads); 8 / 32 align rows to 32-byte sectors / 128-byte lines
+            align = max(4, int(os.environ.get("HG_FEAT_ALIGN", "4")))
+            self.feat_ld = (F + align - 1) // align * align
             x = torch.zeros((V, self.feat_ld), dtype=torch.float32, device=self.device)
             x[:, :F] = torch.as_tensor(np.ascontiguousarray(feats, dtype=np.float32), device=self.device)
             self.features = x
