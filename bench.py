@@ -342,7 +342,7 @@ def main():
         e.seeds.copy_(d_seeds[W + i])
         e.bp.copy_(d_bp[W + i])
         e.counts_in.copy_(d_counts)
-        parts[0][0].replay()
+        e.enqueue_sample()  # full dedup of every layer (the step itself skips it for SAGE's bottom block)
         torch.cuda.synchronize()
         n_dst0 = int(e.samplers[1].n_src.item())
         n_src0 = int(e.samplers[0].n_src.item())

@@ -55,6 +55,14 @@ int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_
                     const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
                     int32_t layer, int32_t* counts, int32_t* slots, uint64_t* minpos, int32_t* tag_ctr,
                     int32_t* scratch, void* stream);
+/* Draws only (same draws, counts and slot contents as hg_sample_layer) for a
+ * block consumed by global source ids (the SAGE bottom layer of the training
+ * step): no first-occurrence marks, no dedup pass; nself (nullable) receives the
+ * per-destination non-self counts (gnnmath.py:145-154). */
+int hg_sample_layer_draws(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                          const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                          int32_t layer, int32_t* counts, int32_t* slots, int32_t* nself, int32_t* scratch,
+                          void* stream);
 
 /* Retires the current first-occurrence tag after a draw that is not followed
  * by hg_dedup_relabel (which retires it itself). */

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
                 float my_w = 0.f;
                 if (j0 + lr < cnt) {
                     const int sg = slot_g[sbase + j0 + lr];
-                    const int sl = slot_local[sbase + j0 + lr];
+                    const int sl = (GLOBAL && !GCN) ? 0 : slot_local[sbase + j0 + lr];  // SAGE bottom: global ids only
                     if (GCN) { my_row = GLOBAL ? sg : sl; my_w = gcn_w(outdeg[sl], cnt); }
                     else if (sg != v) { my_row = GLOBAL ? sg : sl; my_w = wd; }  // non-self edge
                 }

@@ -62,11 +62,11 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
                                                     int cap, int f, const uint64_t* __restrict__ d_seed,
                                                     int layer, int* __restrict__ counts,
                                                     int* __restrict__ slots, unsigned long long* __restrict__ minpos,
-                                                    const int* __restrict__ tag_ctr) {
+                                                    const int* __restrict__ tag_ctr, int* __restrict__ nself) {
     hg_pdl_begin();
     __shared__ int s_last[256];
     const int n = hg_load_count(d_n, cap);
-    const uint32_t tag = fo_tag(tag_ctr);
+    const uint32_t tag = minpos ? fo_tag(tag_ctr) : 0u;
     const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
     const uint64_t base = hg_mix64(stream + HG_GOLDEN);  // kernels.py:153
     const int lane = threadIdx.x & 31;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
         const int i = i0 + threadIdx.x / W;
         if (i >= n) continue;  // segment-uniform
         const int v = frontier[i];
-        if (sub == 0) atomicMin(&minpos[v], fo_key(tag, i));  // frontier position i
+        if (sub == 0 && minpos) atomicMin(&minpos[v], fo_key(tag, i));  // frontier position i
         const int64_t off = offsets[v];
         const int64_t deg = offsets[v + 1] - off;
         const int cnt = deg < f ? (int)deg : f;
@@ -115,7 +115,11 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
         }
         if (sub < cnt) {
             slots[(int64_t)i * f + sub] = u;
-            atomicMin(&minpos[u], fo_key(tag, (long long)n + (long long)i * f + sub));
+            if (minpos) atomicMin(&minpos[u], fo_key(tag, (long long)n + (long long)i * f + sub));
+        }
+        if (nself) {  // SAGE non-self count (gnnmath.py:145-154) when no relabel pass follows
+            const unsigned ns = __ballot_sync(segmask, sub < cnt && u != v);
+            if (sub == 0) nself[i] = __popc(ns);
         }
     }
 }
@@ -128,15 +132,15 @@ __global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __r
                              const int* __restrict__ frontier, const int* d_n, int cap, int f,
                              const uint64_t* __restrict__ d_seed, int layer, int* __restrict__ counts,
                              int* __restrict__ slots, unsigned long long* __restrict__ minpos,
-                             const int* __restrict__ tag_ctr, int* __restrict__ scratch) {
+                             const int* __restrict__ tag_ctr, int* __restrict__ scratch, int* __restrict__ nself) {
     hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
-    const uint32_t tag = fo_tag(tag_ctr);
+    const uint32_t tag = minpos ? fo_tag(tag_ctr) : 0u;
     const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
     const uint64_t base = hg_mix64(stream + HG_GOLDEN);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int v = frontier[i];
-        atomicMin(&minpos[v], fo_key(tag, i));
+        if (minpos) atomicMin(&minpos[v], fo_key(tag, i));
         const int64_t off = offsets[v];
         const int64_t deg = offsets[v + 1] - off;
         const int cnt = deg < f ? (int)deg : f;
@@ -166,7 +170,13 @@ __global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __r
                 sp[j] = targets[off + vp];
             }
         }
-        for (int j = 0; j < cnt; ++j) atomicMin(&minpos[sp[j]], fo_key(tag, (long long)n + (long long)i * f + j));
+        if (minpos)
+            for (int j = 0; j < cnt; ++j) atomicMin(&minpos[sp[j]], fo_key(tag, (long long)n + (long long)i * f + j));
+        if (nself) {
+            int ns = 0;
+            for (int j = 0; j < cnt; ++j) ns += sp[j] != v;
+            nself[i] = ns;
+        }
     }
 }
 
@@ -468,30 +478,57 @@ int seg_width(int f) { return f <= 4 ? 4 : f <= 8 ? 8 : f <= 16 ? 16 : 32; }
 // layer >= 0 (stream = derive_seed(seed, 0x5A, layer), sampler.py:143), else the
 // stream seed itself (kernels.sample_layer).  scratch: cap*2*fanout ints, only
 // touched when fanout > 32.
-extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
-                               const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                               const uint64_t* d_seed, int32_t layer, int32_t* counts, int32_t* slots,
-                               uint64_t* minpos, int32_t* tag_ctr, int32_t* scratch, void* stream) {
-    cudaStream_t s = (cudaStream_t)stream;
+static int sample_layer_impl(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                             const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                             int32_t layer, int32_t* counts, int32_t* slots, uint64_t* minpos, int32_t* tag_ctr,
+                             int32_t* scratch, int32_t* nself, cudaStream_t s) {
     if (fanout < 1 || cap_dst < 0) { hg_set_error("sample_layer: bad fanout/cap"); return HG_EINVAL; }
     if ((long long)cap_dst * (fanout + 1) >= 0x7fffffffLL) { hg_set_error("sample_layer: cap too large"); return HG_EINVAL; }
     if (cap_dst == 0) return HG_OK;
+    unsigned long long* mp = (unsigned long long*)minpos;
     if (fanout <= 32) {
         const int W = seg_width(fanout);
         const int grid = hg_grid((long long)cap_dst * W, 256, hg_sample_ctas_per_sm());
         switch (W) {
-            case 4: hg_launch(k_sample_seg<4>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
-            case 8: hg_launch(k_sample_seg<8>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
-            case 16: hg_launch(k_sample_seg<16>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
-            default: hg_launch(k_sample_seg<32>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, (unsigned long long*)minpos, tag_ctr); break;
+            case 4: hg_launch(k_sample_seg<4>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, mp, tag_ctr, nself); break;
+            case 8: hg_launch(k_sample_seg<8>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, mp, tag_ctr, nself); break;
+            case 16: hg_launch(k_sample_seg<16>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, mp, tag_ctr, nself); break;
+            default: hg_launch(k_sample_seg<32>, grid, 256, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, mp, tag_ctr, nself); break;
         }
     } else {
         if (!scratch) { hg_set_error("sample_layer: fanout > 32 needs scratch"); return HG_EINVAL; }
-        hg_launch(k_sample_seq, hg_grid(cap_dst, 128, 8), 128, 0, s, offsets, targets, frontier, d_n_dst, cap_dst, fanout,
-                                                              d_seed, layer, counts, slots, (unsigned long long*)minpos,
-                                                              tag_ctr, scratch);
+        hg_launch(k_sample_seq, hg_grid(cap_dst, 128, 8), 128, 0, s, offsets, targets, frontier, d_n_dst, cap_dst,
+                  fanout, d_seed, layer, counts, slots, mp, tag_ctr, scratch, nself);
     }
     return hg_check_launch("sample_layer");
+}
+
+// Draw step of one layer (kernels.py:77-118).  d_seed: the batch rng seed when
+// layer >= 0 (stream = derive_seed(seed, 0x5A, layer), sampler.py:143), else the
+// stream seed itself (kernels.sample_layer).  scratch: cap*2*fanout ints, only
+// touched when fanout > 32.
+extern "C" int hg_sample_layer(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                               const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                               const uint64_t* d_seed, int32_t layer, int32_t* counts, int32_t* slots,
+                               uint64_t* minpos, int32_t* tag_ctr, int32_t* scratch, void* stream) {
+    if (fanout >= 1 && cap_dst > 0 && !minpos) {
+        hg_set_error("sample_layer: minpos required (see hg_sample_layer_draws)");
+        return HG_EINVAL;
+    }
+    return sample_layer_impl(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots,
+                             minpos, tag_ctr, scratch, nullptr, (cudaStream_t)stream);
+}
+
+// Draws only, for a block whose sources are consumed by GLOBAL id (the SAGE
+// bottom layer: the fused gather reads feature rows directly, and no backward
+// transposed aggregation exists below it): no first-occurrence marks and no
+// dedup/relabel pass; per-destination non-self counts come from the draw kernel.
+extern "C" int hg_sample_layer_draws(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                                     const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                                     int32_t layer, int32_t* counts, int32_t* slots, int32_t* nself,
+                                     int32_t* scratch, void* stream) {
+    return sample_layer_impl(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots,
+                             nullptr, nullptr, scratch, nself, (cudaStream_t)stream);
 }
 
 // Retire a first-occurrence tag without a dedup pass (a bare draw).

@@ -313,7 +313,7 @@ class TrainEngine:
         sc = self.side[1]
         for l in range(self.L - 1, -1, -1):
             fr, n = self.frontier(l)
-            self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False)
+            self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False, dedup=not self._bottom_draws_only(l))
             if l > 0 and not self.bwd_scatter:
                 sc.wait_stream(main)
                 self.samplers[l].build_csc(n, sc, frontier=fr)
@@ -515,6 +515,13 @@ class TrainEngine:
                     pass
         torch.cuda.synchronize(self.device)
         return gs, segs
+
+    def _bottom_draws_only(self, l: int) -> bool:
+        """SAGE's bottom block is consumed by global source id only (fused gather
+        of feature rows; no transposed aggregation below layer 0, gnnmath.py:256),
+        so the training step skips its dedup/relabel pass (HG_BOTTOM_DEDUP=1 keeps
+        it).  GCN needs the block-local out-degrees (gnnmath.py:96)."""
+        return l == 0 and self.sage and os.environ.get("HG_BOTTOM_DEDUP", "0") != "1"
 
     def check_numerics(self):
         """Raise like the reference's non-finite guard (gnnmath.py:100-102) if a

@@ -143,7 +143,7 @@ class LayerSampler:
             self.csc_w = torch.zeros(max(cap_dst * self.f, 1), dtype=torch.float32, device=dev)
 
     def run(self, frontier, d_n_dst, d_seed, layer: int, stream=None, cap_dst: int | None = None,
-            with_csc: bool = True):
+            with_csc: bool = True, dedup: bool = True):
         """Enqueue the block build for `frontier` (device int32, count *d_n_dst).
         ``with_csc=False`` defers the transposed view to ``build_csc`` (e.g. on a
         side stream, off the forward critical path)."""
@@ -163,6 +163,11 @@ class LayerSampler:
         cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
         s = stream_ptr(stream)
         g = self.dg
+        if not dedup:  # draws + non-self counts only (sources consumed by global id)
+            _lib.call("hg_sample_layer_draws", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap,
+                      self.f, ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.nself),
+                      ptr(self.scratch), s)
+            return self
         _lib.call("hg_sample_layer", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
                   ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos.table),
                   ptr(self.minpos.tag), ptr(self.scratch), s)
