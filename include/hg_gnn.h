@@ -174,8 +174,12 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
  * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem;
  * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always;
  * key 5: programmatic dependent launch of the step kernels, 1 (default; env HG_PDL=0 at load turns it off) / 0;
- * key 6: TS-form GEMM keeps the whole B image resident in smem when it fits, A ring released by the split warps (1) / streams B per stage (0, default)) */
+ * key 6: TS-form GEMM keeps the whole B image resident in smem when it fits, A ring released by the split warps (1) / streams B per stage (0, default);
+ * key 7: paired hi|lo MMAs (N = 2*BN operand, two instructions per K slice instead of three) for BN <= 64 (1, default) / 0) */
 int hg_set_tuning(int32_t key, int32_t value);
+/* profiling aid: the 8 x 64 globaltimer stamps (ns) of the tensor-core GEMM's
+ * pipeline timeline probe (hg_set_tuning key 9, bit 3) */
+int hg_debug_timeline(uint64_t* out);
 /* L2 residency: feature-gathering kernels launched after this call attach an
  * access-policy window [base, base+bytes) with persisting hits (hit_ratio of the
  * window's lines), and the device's persisting-L2 carve-out is set to bytes

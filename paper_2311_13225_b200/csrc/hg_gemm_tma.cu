@@ -51,6 +51,14 @@ __host__ __device__ constexpr uint32_t tmem_cols() { return C <= 32 ? 32 : C <= 
 // profiling knob (hg_set_tuning key 9): bit 0 skips the MMAs, bit 1 the split
 // work (pipelines still run; results are wrong) — isolates the bound stage
 __constant__ int c_dbg;
+// timeline probe (c_dbg bit 3): globaltimer stamps of CTA 0's first 64 iterations
+__device__ unsigned long long g_tl[8][64];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(ev, it) do { if ((c_dbg & 8) && blockIdx.x == 0 && blockIdx.y == 0 && (it) < 64) g_tl[ev][it] = gtime(); } while (0)
 
 __device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
@@ -58,7 +66,7 @@ __device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier
 // forward / dX: persistent CTAs over 128-row M tiles (blockIdx.y = BN-wide N tile)
 template <int BN>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
-k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
+k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2, int ls1, int ls2,
            const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
            int M_cap, int act) {
     hg_pdl_begin();
@@ -132,8 +140,11 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
                     tc_fence_after();
                     const uint32_t a_hi = smem_u32(smem + st * STAGE), a_lo = a_hi + A_BYTES;
                     const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_TILE;
+                    // 8-wide K slices past the source's K hold TMA zero fill: skipped
+                    const int ns = kt == nk1 - 1 ? ls1 : (kt == nk1 + nk2 - 1 ? ls2 : 4);
 #pragma unroll
                     for (int s = 0; s < 4; ++s) {
+                        if (s >= ns) break;
                         const uint64_t dah = sdesc(a_hi + s * 32, 16, 1024), dal = sdesc(a_lo + s * 32, 16, 1024);
                         const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
                         mma_tf32(d, dah, dbh, IDESC, (kt | s) ? 1u : 0u);
@@ -233,19 +244,32 @@ template <int BN, bool RESB>
 __host__ __device__ constexpr int ts_stage_bytes() { return RESB ? A_BYTES : A_BYTES + 2 * BN * 128; }
 constexpr int RESB_MAX_BYTES = 128 * 1024;
 
-template <int BN, bool RESB>
+// PAIR: the B image's hi and lo tiles are adjacent 64-row blocks of one K-major
+// tile, i.e. one N = 2*BN operand [B_hi ; B_lo]: per K slice the MMAs become
+// A_hi x [B_hi ; B_lo] (N = 2*BN, into two accumulator halves) + A_lo x B_hi
+// (N = BN), two instructions instead of three, and the epilogue adds the halves.
+// (The tensor pipe, not memory, bounds the three-MMA form at N = 64.)
+template <int BN, bool PAIR>
+__host__ __device__ constexpr int ts_acc_cols() { return PAIR ? 2 * BN : BN; }
+template <int BN, bool PAIR>
+__host__ __device__ constexpr int ts_nstages() { return PAIR ? (512 - 2 * ts_acc_cols<BN, PAIR>()) / 64 : ts_stages<BN>(); }
+
+template <int BN, bool RESB, bool PAIR>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
-k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2,
+k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2, int ls1, int ls2,
               const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
               int M_cap, int act) {
     hg_pdl_begin();
-    constexpr int S = ts_stages<BN>();
+    constexpr int S = ts_nstages<BN, PAIR>();
     constexpr int STAGE = ts_stage_bytes<BN, RESB>();
     constexpr int B_BYTES = 2 * BN * 128;
     constexpr int B_TILE = BN * 128;
-    constexpr uint32_t A_COL0 = 2 * BN;  // first TMEM column of the A stages
-    static_assert(2 * BN + S * 64 <= 512, "TMEM budget");
+    constexpr int ACC = ts_acc_cols<BN, PAIR>();  // accumulator columns per output tile
+    constexpr uint32_t A_COL0 = 2 * ACC;           // first TMEM column of the A stages
+    static_assert(2 * ACC + S * 64 <= 512, "TMEM budget");
+    static_assert(S >= 2, "stages");
     constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
+    constexpr uint32_t IDESC2 = idesc_tf32(128, 2 * BN, 0, 0);
     extern __shared__ uint8_t smem_raw[];
     // RESB: afree[st] (split warps done reading smem stage st) releases the A
     // ring to the producer independently of the MMAs; empty[st] then only
@@ -298,6 +322,7 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             for (int it = 0; it < iters; ++it) {
                 const int st = it % S;
                 if (it >= S) mbar_wait(RESB ? &afree[st] : &empty[st], (uint32_t)(((it / S) - 1) & 1));
+                TL(0, it);
                 const int tile = it / nk, kt = it - tile * nk;
                 const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
                 uint8_t* base = smem + st * STAGE;
@@ -315,24 +340,33 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
                 const int acc = tile & 1;
                 if (tile >= 2) mbar_wait(&tempty[acc], (uint32_t)(((tile >> 1) - 1) & 1));
                 tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                const uint32_t d = tmem + (uint32_t)(acc * ACC);
                 for (int kt = 0; kt < nk; ++kt, ++it) {
                     const int st = it % S;
                     mbar_wait(&splt[st], (uint32_t)((it / S) & 1));
+                    TL(3, it);
                     tc_fence_after();
                     const uint32_t ta = tmem + A_COL0 + (uint32_t)(st * 64);
                     const uint32_t b_hi = RESB ? smem_u32(smem + S * STAGE + kt * B_BYTES)
                                                : smem_u32(smem + st * STAGE + A_BYTES);
                     const uint32_t b_lo = b_hi + B_TILE;
+                    // 8-wide K slices past the source's K hold TMA zero fill: skipped
+                    const int ns = kt == nk1 - 1 ? ls1 : (kt == nk1 + nk2 - 1 ? ls2 : 4);
 #pragma unroll
                     for (int s = 0; s < 4; ++s) {
-                        if (c_dbg & 1) break;
+                        if ((c_dbg & 1) || s >= ns) break;
                         const uint64_t dbh = sdesc(b_hi + s * 32, 16, 1024), dbl = sdesc(b_lo + s * 32, 16, 1024);
-                        mma_tf32_ts(d, ta + s * 8, dbh, IDESC, (kt | s) ? 1u : 0u);
-                        mma_tf32_ts(d, ta + s * 8, dbl, IDESC, 1u);
-                        mma_tf32_ts(d, ta + 32 + s * 8, dbh, IDESC, 1u);
+                        if (PAIR) {  // [B_hi ; B_lo] is one N = 2*BN operand starting at b_hi
+                            mma_tf32_ts(d, ta + s * 8, dbh, IDESC2, (kt | s) ? 1u : 0u);
+                            mma_tf32_ts(d, ta + 32 + s * 8, dbh, IDESC, 1u);
+                        } else {
+                            mma_tf32_ts(d, ta + s * 8, dbh, IDESC, (kt | s) ? 1u : 0u);
+                            mma_tf32_ts(d, ta + s * 8, dbl, IDESC, 1u);
+                            mma_tf32_ts(d, ta + 32 + s * 8, dbh, IDESC, 1u);
+                        }
                     }
                     mma_commit(&empty[st]);
+                    TL(4, it);
                 }
                 mma_commit(&tfull[acc]);
             }
@@ -343,6 +377,7 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
         for (int it = 0; it < iters; ++it) {
             const int st = it % S;
             mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+            if (warp == 2 && lane == 0) TL(1, it);
             const uint8_t* base = smem + st * STAGE;
             if (c_dbg & 2) {  // profiling: no split work (same hand-offs)
                 __syncwarp();
@@ -380,6 +415,7 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&splt[st]);
+            if (warp == 2 && lane == 0) TL(2, it);
         }
     } else {  // ---- epilogue warps: TMEM lane quarter = warp % 4
         const int q = warp & 3;
@@ -393,9 +429,20 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t r0[16], r1[16];
-                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * ACC + c0);
                 tmem_ld16_nowait(ta, r0);
                 tmem_ld16_nowait(ta + 16, r1);
+                if (PAIR) {  // + the A_hi x B_lo half
+                    uint32_t p0[16], p1[16];
+                    tmem_ld16_nowait(ta + BN, p0);
+                    tmem_ld16_nowait(ta + BN + 16, p1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        r0[j] = __float_as_uint(__uint_as_float(r0[j]) + __uint_as_float(p0[j]));
+                        r1[j] = __float_as_uint(__uint_as_float(r1[j]) + __uint_as_float(p1[j]));
+                    }
+                }
                 tmem_wait_ld();
                 if (gm < M && n0 + c0 < N && !(c_dbg & 4)) {
                     float* crow = C + (int64_t)gm * ldc + n0 + c0;
@@ -447,7 +494,10 @@ __device__ __forceinline__ int wg_rows_per_chunk(int M, int n_chunks) {
     return ((r + 31) / 32) * 32;
 }
 
-template <int BN>
+// PAIR (BN <= 64): the G hi and lo tiles are consecutive MN groups of one
+// MN-major operand [G_hi | G_lo] (N = 2*BN): A_hi x [G_hi | G_lo] + A_lo x G_hi,
+// two MMAs per K slice instead of three; the epilogue adds the halves.
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(WG_THREADS, 1)
 k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
@@ -457,8 +507,9 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
     constexpr int STAGE = wg_stage_bytes<BN>();
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
     constexpr int NG = BN / 32;       // G boxes (32 columns each) per stage
-    constexpr uint32_t NCOLS = tmem_cols<BN>();
+    constexpr uint32_t NCOLS = tmem_cols<PAIR ? 2 * BN : BN>();
     constexpr uint32_t IDESC = idesc_tf32(128, BN, 1, 1);
+    constexpr uint32_t IDESC2 = idesc_tf32(128, 2 * BN, 1, 1);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[S], splt[S], empty[S], done;
     __shared__ uint32_t s_tmem;
@@ -520,9 +571,14 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                     if (c_dbg & 1) break;
                     const uint64_t dah = sdesc(a_hi + s * 1024, lbo, sbo, 1), dal = sdesc(a_lo + s * 1024, lbo, sbo, 1);
                     const uint64_t dgh = sdesc(g_hi + s * 1024, lbo, sbo, 1), dgl = sdesc(g_lo + s * 1024, lbo, sbo, 1);
-                    mma_tf32(tmem, dah, dgh, IDESC, (j | s) ? 1u : 0u);
-                    mma_tf32(tmem, dah, dgl, IDESC, 1u);
-                    mma_tf32(tmem, dal, dgh, IDESC, 1u);
+                    if (PAIR) {
+                        mma_tf32(tmem, dah, dgh, IDESC2, (j | s) ? 1u : 0u);
+                        mma_tf32(tmem, dal, dgh, IDESC, 1u);
+                    } else {
+                        mma_tf32(tmem, dah, dgh, IDESC, (j | s) ? 1u : 0u);
+                        mma_tf32(tmem, dah, dgl, IDESC, 1u);
+                        mma_tf32(tmem, dal, dgh, IDESC, 1u);
+                    }
                 }
                 mma_commit(&empty[st]);
             }
@@ -572,6 +628,13 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
         for (int c0 = 0; c0 < BN; c0 += 16) {
             uint32_t r[16];
             tmem_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+            if (PAIR) {  // + the A_hi x G_lo half
+                uint32_t p[16];
+                tmem_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(BN + c0), p);
+                tmem_wait_ld();
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __uint_as_float(p[jj]));
+            }
             tmem_wait_ld();
             if (gk < K && c0 < N) {
                 float* prow = P + (int64_t)gk * N + c0;
@@ -619,6 +682,8 @@ __global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restric
     }
 }
 
+int g_pair = 1;  // paired hi|lo MMA form for BN <= 64, fwd and wgrad (hg_set_tuning key 7)
+
 // ---------------------------------------------------------------------------
 // host: tensor maps through the driver entry point (no libcuda link needed)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -661,6 +726,7 @@ int make_map(CUtensorMap* m, const float* base, int cols, int rows, int ld, int 
 
 template <int BN>
 int launch_fwd(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, int nk1, int nk2,
+               int ls1, int ls2,
                const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
     const int smem = fwd_stages<BN>() * fwd_stage_bytes<BN>() + 1024;
     static bool attr = false;
@@ -670,7 +736,7 @@ int launch_fwd(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
-    hg_launch(k_gemm_tma<BN>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, M_cap, act);
+    hg_launch(k_gemm_tma<BN>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, M_cap, act);
     return hg_check_launch("gemm_tma");
 }
 
@@ -678,27 +744,34 @@ int g_resb = 0;  // resident-B TS form when the image fits (hg_set_tuning key 6;
 
 template <int BN>
 int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, int nk1,
-                  int nk2, const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
+                  int nk2, int ls1, int ls2, const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
     const int nk = nk1 + nk2;
     const bool resb = g_resb && nk * 2 * BN * 128 <= RESB_MAX_BYTES;
     const int smem = resb ? ts_stages<BN>() * ts_stage_bytes<BN, true>() + nk * 2 * BN * 128 + 1024
                           : ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024;
+    const bool pair = g_pair && BN <= 64 && !resb;
+    constexpr bool PB = BN <= 64;
+    const int smem_pair = ts_nstages<BN, PB>() * ts_stage_bytes<BN, false>() + 1024;
     static bool attr = false;
     if (!attr) {
         const int mx = ts_stages<BN>() * ts_stage_bytes<BN, true>() + RESB_MAX_BYTES + 1024;
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024);
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair);
         attr = true;
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
     if (resb)
-        hg_launch(k_gemm_tma_ts<BN, true>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M,
-                  M_cap, act);
+        hg_launch(k_gemm_tma_ts<BN, true, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc,
+                  N, d_M, M_cap, act);
+    else if (pair)
+        hg_launch(k_gemm_tma_ts<BN, false, (BN <= 64)>, dim3(gx, n_nt), FWD_THREADS, smem_pair, s, m1, m2, nk1, nk2, ls1, ls2,
+                  bimg, C, ldc, N, d_M, M_cap, act);
     else
-        hg_launch(k_gemm_tma_ts<BN, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, bimg, C, ldc, N,
-                  d_M, M_cap, act);
+        hg_launch(k_gemm_tma_ts<BN, false, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc,
+                  N, d_M, M_cap, act);
     return hg_check_launch("gemm_tma_ts");
 }
 
@@ -708,12 +781,19 @@ template <int BN>
 int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, const CUtensorMap& mg, int K,
               int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo) {
     const int smem = wg_stages<BN>() * wg_stage_bytes<BN>() + 1024;
+    constexpr bool PB = BN <= 64;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_wgrad_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    hg_launch(k_wgrad_tma<BN>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial, lbo, sbo);
+    if (g_pair && PB)
+        hg_launch(k_wgrad_tma<BN, PB>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial,
+                  lbo, sbo);
+    else
+        hg_launch(k_wgrad_tma<BN, false>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks,
+                  partial, lbo, sbo);
     return hg_check_launch("wgrad_tma");
 }
 
@@ -721,7 +801,12 @@ int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMa
 
 void hg_tma_set_fwd_form(int v) { g_fwd_form = v; }
 void hg_tma_set_resb(int v) { g_resb = v ? 1 : 0; }
+void hg_tma_set_pair(int v) { g_pair = v ? 1 : 0; }
 void hg_tma_set_dbg(int v) { cudaMemcpyToSymbol(c_dbg, &v, sizeof(int)); }
+// timeline probe read-back: 8 x 64 globaltimer stamps (ns)
+extern "C" int hg_debug_timeline(uint64_t* out) {
+    return cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl)) == cudaSuccess ? HG_OK : HG_ECUDA;
+}
 
 int hg_tma_gemm_bn(int N) {
     const int Nr = (N + 15) & ~15;
@@ -740,20 +825,21 @@ int hg_gemm_tma_launch(const float* A1, int lda1, int K1, const float* A2, int l
         m2 = m1;
     }
     const int nk1 = hg_ceil_div(K1, 32), nk2 = (A2 && K2 > 0) ? hg_ceil_div(K2, 32) : 0;
+    const int ls1 = (K1 - 1) % 32 / 8 + 1, ls2 = nk2 ? (K2 - 1) % 32 / 8 + 1 : 4;  // live 8-wide slices of each last tile
     const int bn = hg_tma_gemm_bn(N);
     const int n_nt = hg_ceil_div(N, bn);
     if (g_fwd_form == 1 && bn <= 128) {
         switch (bn) {
-            case 32: return launch_fwd_ts<32>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
-            case 64: return launch_fwd_ts<64>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
-            default: return launch_fwd_ts<128>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+            case 32: return launch_fwd_ts<32>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
+            case 64: return launch_fwd_ts<64>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
+            default: return launch_fwd_ts<128>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
         }
     }
     switch (bn) {
-        case 32: return launch_fwd<32>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
-        case 64: return launch_fwd<64>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
-        case 128: return launch_fwd<128>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
-        default: return launch_fwd<256>(M_cap, n_nt, s, m1, m2, nk1, nk2, bimg, C, ldc, N, d_M, act);
+        case 32: return launch_fwd<32>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
+        case 64: return launch_fwd<64>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
+        case 128: return launch_fwd<128>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
+        default: return launch_fwd<256>(M_cap, n_nt, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc, N, d_M, act);
     }
 }
 

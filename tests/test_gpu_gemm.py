@@ -22,7 +22,7 @@ def _ld(k):
     return (k + 3) // 4 * 4
 
 
-@pytest.fixture(params=["tc", "tc_resb", "skinny"])
+@pytest.fixture(params=["tc", "tc_resb", "tc_unpaired", "skinny"])
 def path(request):
     """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores (default), the resident-B
     TS form (hg_set_tuning key 6), or the optional SIMT latency kernels for
@@ -31,9 +31,11 @@ def path(request):
     lib = _lib.load()
     lib.hg_set_tuning(4, 1 if request.param == "skinny" else 0)
     lib.hg_set_tuning(6, 1 if request.param == "tc_resb" else 0)
+    lib.hg_set_tuning(7, 0 if request.param == "tc_unpaired" else 1)
     yield request.param
     lib.hg_set_tuning(4, 0)
     lib.hg_set_tuning(6, 0)
+    lib.hg_set_tuning(7, 1)
 
 
 @pytest.mark.parametrize("fn", ["hg_gemm_tc", "hg_gemm_f32"])
