@@ -519,10 +519,27 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
     const int groups_per_block = blockDim.x / LPR;
     const int F = F4 * 4;
     bool bad = false;
-    for (int d0 = blockIdx.x * groups_per_block; d0 < n; d0 += gridDim.x * groups_per_block) {
-        const int d = d0 + threadIdx.x / LPR;
-        if (d >= n) continue;
+    // one lane group per SLOT (edge), not per destination: the ~f dependent
+    // loads of a destination's edge loop (slot -> outdeg / mask -> store) run in
+    // parallel across groups; the destination's dagg row is re-read per edge
+    // from L2.
+    const long long Q = (long long)n * f;
+    for (long long q0 = (long long)blockIdx.x * groups_per_block; q0 < Q; q0 += (long long)gridDim.x * groups_per_block) {
+        const long long q = q0 + threadIdx.x / LPR;
+        if (q >= Q) continue;
+        const int d = (int)(q / f), j = (int)(q - (long long)d * f);
         const int cnt = counts[d];
+        if (j >= cnt) continue;
+        const int s = slot_local[q];
+        float w;
+        if (GCN) {
+            w = gcn_w(outdeg[s], cnt);
+        } else {
+            if (slot_g[q] == frontier[d]) continue;  // SAGE drops self edges (gnnmath.py:148)
+            const int ns = nself[d];
+            w = ns > 0 ? 1.0f / (float)ns : 0.f;
+        }
+        const int od = outdeg[s];
         float4 x[NV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -530,44 +547,30 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
             x[k] = c < F4 ? __ldg(reinterpret_cast<const float4*>(dagg + (int64_t)d * ld_dagg) + c)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        const int v = GCN ? 0 : frontier[d];
-        const float wd = GCN ? 0.f : (nself[d] > 0 ? 1.0f / (float)nself[d] : 0.f);
-        const int64_t sbase = (int64_t)d * f;
-        for (int j = 0; j < cnt; ++j) {
-            const int s = slot_local[sbase + j];
-            const int od = outdeg[s];
-            float w;
-            if (GCN) {
-                w = gcn_w(od, cnt);
-            } else {
-                if (slot_g[sbase + j] == v) continue;  // SAGE drops self edges (gnnmath.py:148)
-                w = wd;
-            }
-            if (s >= n && od == 1) {  // single contribution: final row, no accumulator
-                const bool zero_row = inj && inj[s];
-#pragma unroll
-                for (int k = 0; k < NV; ++k) {
-                    const int c = lr + k * LPR;
-                    if (c < F4) {
-                        float4 a = make_float4(w * x[k].x, w * x[k].y, w * x[k].z, w * x[k].w);
-                        if (!(fabsf(a.x) < FX_GUARD && fabsf(a.y) < FX_GUARD && fabsf(a.z) < FX_GUARD &&
-                              fabsf(a.w) < FX_GUARD))
-                            bad = true;
-                        reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx)[c] = bwd_mask(a, hmask, ld_hmask, s, c, zero_row);
-                    }
-                }
-                continue;
-            }
-            unsigned long long* row = acc + (int64_t)s * F;
+        if (s >= n && od == 1) {  // single contribution: final row, no accumulator
+            const bool zero_row = inj && inj[s];
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 const int c = lr + k * LPR;
                 if (c < F4) {
-                    fx_add(row + 4 * c + 0, w * x[k].x, bad);
-                    fx_add(row + 4 * c + 1, w * x[k].y, bad);
-                    fx_add(row + 4 * c + 2, w * x[k].z, bad);
-                    fx_add(row + 4 * c + 3, w * x[k].w, bad);
+                    float4 a = make_float4(w * x[k].x, w * x[k].y, w * x[k].z, w * x[k].w);
+                    if (!(fabsf(a.x) < FX_GUARD && fabsf(a.y) < FX_GUARD && fabsf(a.z) < FX_GUARD &&
+                          fabsf(a.w) < FX_GUARD))
+                        bad = true;
+                    reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx)[c] = bwd_mask(a, hmask, ld_hmask, s, c, zero_row);
                 }
+            }
+            continue;
+        }
+        unsigned long long* row = acc + (int64_t)s * F;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lr + k * LPR;
+            if (c < F4) {
+                fx_add(row + 4 * c + 0, w * x[k].x, bad);
+                fx_add(row + 4 * c + 1, w * x[k].y, bad);
+                fx_add(row + 4 * c + 2, w * x[k].z, bad);
+                fx_add(row + 4 * c + 3, w * x[k].w, bad);
             }
         }
     }
@@ -648,7 +651,7 @@ extern "C" int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_
     const int F4 = F / 4;
     int LPR, NV;
     pick_lanes(F4, LPR, NV);
-    dim3 g(hg_grid((long long)(cap_dst > 0 ? cap_dst : 1) * LPR, 256, 8));
+    dim3 g(hg_grid((long long)(cap_dst > 0 ? cap_dst : 1) * fanout * LPR, 256, 8));  // one group per slot
     dim3 g2(hg_grid((long long)cap_src * LPR, 256, 8));
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* acc = reinterpret_cast<unsigned long long*>(acc_ws);

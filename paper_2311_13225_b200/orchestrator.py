@@ -169,7 +169,8 @@ class HotProducer:
         e, hot = self.e, self.e.hot
         s = stream_ptr(stream)
         d0, d1 = e.dims[0], e.dims[1]
-        self.smp.run(ids, None, seed_dev, 0, stream, cap_dst=c)
+        # SAGE reads the chunk's neighbour rows by global id: draws only, no dedup
+        self.smp.run(ids, None, seed_dev, 0, stream, cap_dst=c, dedup=not e.sage)
         model = 0 if e.sage else 1
         _lib.call("hg_aggregate_fwd", model, 1, ptr(e.dg.features), e.dg.feat_ld, e.ld[0], ptr(ids), None, c,
                   e.fan[0], ptr(self.smp.counts), ptr(self.smp.slots), ptr(self.smp.slot_local), ptr(self.smp.nself),

@@ -164,6 +164,8 @@ class LayerSampler:
         s = stream_ptr(stream)
         g = self.dg
         if not dedup:  # draws + non-self counts only (sources consumed by global id)
+            if self.nself is None:
+                raise ValueError("draws-only sampling produces SAGE non-self counts: need_nself=True")
             _lib.call("hg_sample_layer_draws", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap,
                       self.f, ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.nself),
                       ptr(self.scratch), s)
