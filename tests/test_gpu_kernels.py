@@ -155,3 +155,28 @@ def test_layer_sampler_varying_chunk_sizes(S):
         assert np.array_equal(got.src_vertices, ref.src_vertices), c
         assert np.array_equal(got.edge_src, ref.edge_src), c
         assert np.array_equal(got.edge_dst, ref.edge_dst), c
+
+
+def test_draws_only_matches_full_block(S):
+    """hg_sample_layer_draws (the SAGE bottom block of the training step) yields the
+    same per-destination draws and non-self counts as the full draw + dedup +
+    relabel pass (whose slots are the same draws re-ordered by local source id)."""
+    import torch
+    from paper_2311_13225_b200.datagen import make_dataset
+    from paper_2311_13225_b200.device import DeviceGraph, u64_tensor
+    ds = make_dataset("c2", scale=0.1)
+    dg = DeviceGraph.from_dataset(ds)
+    rng = np.random.default_rng(11)
+    ids = torch.as_tensor(rng.choice(ds.num_vertices, size=20000, replace=False).astype(np.int32), device="cuda")
+    seed = u64_tensor(0xABCDEF, "cuda")
+    full = S.LayerSampler(dg, 20000, 15, need_nself=True, minpos=dg.minpos.like()).run(ids, None, seed, 0)
+    draws = S.LayerSampler(dg, 20000, 15, need_nself=True).run(ids, None, seed, 0, dedup=False)
+    torch.cuda.synchronize()
+    assert torch.equal(full.counts, draws.counts)
+    assert torch.equal(full.nself, draws.nself)
+    f = 15
+    a = full.slots.view(-1, f).cpu().numpy()
+    b = draws.slots.view(-1, f).cpu().numpy()
+    cnt = full.counts.cpu().numpy()
+    for i in range(0, 20000, 97):
+        assert sorted(a[i, :cnt[i]].tolist()) == sorted(b[i, :cnt[i]].tolist()), i
