@@ -235,12 +235,18 @@ def main():
                       strategy="case1", hot_ratio=0.0, use_graph=True, seed=0)
     tr = Trainer(ds, cfg, dist=dist_ctx)
     e = tr.engine
-    # per sample set: the sample-half graph and the train half split around the
-    # dominant kernel (bottom fused gather+aggregate), so CUDA events bracket it
-    # (train half = [store lookup (none here) + bottom aggregate | rest])
-    parts = [e.capture_segments(split_at=("fwd0_gemm",), set_index=k) for k in range(len(e.sets))]
-    for _, segs in parts:
-        assert [n for n, _ in segs] == ["start", "fwd0_gemm"], [n for n, _ in segs]
+    # instrumented copies of every set's graphs, split so CUDA events bracket the
+    # dominant kernel (bottom fused gather+aggregate): it runs at the end of the
+    # SAMPLE half (early_agg0: no weights involved, overlaps the previous batch's
+    # training), else at the start of the train half
+    early = e.early_agg0()
+    parts = [e.capture_segments(split_at=("sample_agg0",) if early else ("fwd0_gemm",), set_index=k)
+             for k in range(len(e.sets))]
+    for ssegs, segs in parts:
+        if early:
+            assert [n for n, _ in ssegs] == ["start", "sample_agg0"], [n for n, _ in ssegs]
+        else:
+            assert [n for n, _ in segs] == ["start", "fwd0_gemm"], [n for n, _ in segs]
     K, W = args.steps, args.warmup
     batches, rseeds = epoch_batches(ds, W + K, rank=rank, world=world)
     # stage every step's inputs in HBM (value = device-resident inputs)
@@ -260,7 +266,7 @@ def main():
     ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
 
-    def sample(i):
+    def sample(i, timed_idx=None, split=False):
         k = i % nset
         if trained[k] is not None:
             ss.wait_event(trained[k])
@@ -269,14 +275,23 @@ def main():
             s.seeds.copy_(d_seeds[i], non_blocking=True)
             s.bp.copy_(d_bp[i], non_blocking=True)
             s.counts_in.copy_(d_counts, non_blocking=True)
-            parts[k][0].replay()
+            if split and early:  # instrumented: events bracket the bottom aggregation segment
+                ssegs = parts[k][0]
+                ssegs[0][1].replay()
+                if timed_idx is not None:
+                    ev_a[timed_idx].record(ss)
+                ssegs[1][1].replay()
+                if timed_idx is not None:
+                    ev_b[timed_idx].record(ss)
+            else:
+                e.g_sample[k].replay()
             sampled[k].record(ss)
 
     def train(i, timed_idx=None, split=False):
         k = i % nset
         st.wait_event(sampled[k])
         with torch.cuda.stream(st):
-            if split:  # instrumented: CUDA events bracket the dominant kernel's graph segment
+            if split and not early:  # instrumented: CUDA events bracket the dominant kernel's graph segment
                 segs = parts[k][1]
                 if timed_idx is not None:
                     ev_a[timed_idx].record(st)
@@ -294,10 +309,10 @@ def main():
         """Software pipeline: sample batch i+1 (stream ss) while batch i trains (st)."""
         ss.wait_stream(stream)
         st.wait_stream(stream)
-        sample(lo)
+        sample(lo, 0 if timed else None, split)
         for i in range(lo, hi):
             if i + 1 < hi:
-                sample(i + 1)
+                sample(i + 1, (i + 1 - lo) if timed else None, split)
             train(i, (i - lo) if timed else None, split)
         stream.wait_stream(ss)
         stream.wait_stream(st)
@@ -482,9 +497,14 @@ def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):
     """Per-phase device time (ms) of one step run SEQUENTIALLY (sample half, then
     the train half split at every mark; no cross-batch overlap)."""
     import torch
+    early = e.early_agg0()
     marks = tuple(m for m in e.MARKS if e.hot is not None or m != "fwd0_agg")  # no empty segments
+    if early:  # the bottom aggregation closes the sample half; the train half starts at its GEMM
+        marks = tuple(m for m in marks if m != "fwd0_gemm") + ("sample_agg0",)
     gs, segs = e.capture_segments(split_at=marks)
-    segs = [("sample", gs)] + [(("train_start" if n == "start" else n), g) for n, g in segs]
+    sample_segs = [("sample", gs)] if not isinstance(gs, list) else \
+        [("sample" if n == "start" else "bottom_agg", g) for n, g in gs]
+    segs = sample_segs + [(("train_start" if n == "start" else n), g) for n, g in segs]
     tot = {n: 0.0 for n, _ in segs}
     e.cur = 0
     for r in range(reps):

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // K4-K7: gather + mean/GCN aggregation forward, transposed aggregation backward.
 //
 // Forward replaces, for one sampled block,
@@ -326,6 +327,18 @@ int launch_bwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* dagg, int l
     return HG_EUNSUPPORTED;
 }
 
+// CTAs per SM of the bottom (global-id) aggregation grid: env HG_AGG_CTAS_PER_SM
+// (default 8); fewer leaves SM slots for the concurrently running training stream
+int agg_ctas_per_sm() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HG_AGG_CTAS_PER_SM");
+        v = e ? atoi(e) : 8;
+        v = v < 1 ? 1 : (v > 8 ? 8 : v);
+    }
+    return v;
+}
+
 void pick_lanes(int F4, int& LPR, int& NV) {
     if (F4 <= 8) { LPR = 8; NV = 1; }
     else if (F4 <= 16) { LPR = 16; NV = 1; }
@@ -355,7 +368,7 @@ extern "C" int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* 
     const int F4 = F / 4;
     int LPR, NV;
     pick_lanes(F4, LPR, NV);
-    dim3 g(hg_grid((long long)cap_dst * LPR, 256, 8));
+    dim3 g(hg_grid((long long)cap_dst * LPR, 256, global_src ? agg_ctas_per_sm() : 8));
     cudaStream_t s = (cudaStream_t)stream;
     int rc;
     const int mode = (model ? 2 : 0) + (global_src ? 1 : 0);

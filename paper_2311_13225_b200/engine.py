@@ -214,6 +214,12 @@ class TrainEngine:
         # ---- activations / gradients ----
         self.self_buf = zf(self.cap_dst[0], self.ld[0]) if self.sage else None
         self.agg = [zf(self.cap_dst[l], self.ld[l]) for l in range(self.L)]
+        # bottom aggregation outputs per sample set: the bottom gather+aggregate
+        # needs no weights, so (without hot-embedding injection) it runs in the
+        # SAMPLE half of batch k+1 while batch k trains (see early_agg0)
+        self._self_bufs = [self.self_buf] + [zf(self.cap_dst[0], self.ld[0]) if self.sage else None
+                                             for _ in range(n_sets - 1)]
+        self._agg0s = [self.agg[0]] + [zf(self.cap_dst[0], self.ld[0]) for _ in range(n_sets - 1)]
         self.out = [zf(self.cap_dst[l], self.ld[l + 1]) for l in range(self.L)]  # out[l] = H_{l+1}
         self.dz = [zf(self.cap_dst[l], self.ld[l + 1]) for l in range(self.L)]
         self.dagg = [zf(self.cap_dst[l], self.ld[l]) if l > 0 else None for l in range(self.L)]
@@ -306,10 +312,32 @@ class TrainEngine:
         self.enqueue_sample_part(main)
         self.enqueue_train_part(main, mark)
 
-    def enqueue_sample_part(self, stream=None):
-        """Blocks L-1..0 of the current set; the transposed (backward) views are
-        built on a side stream (a parallel graph branch) joined at the end."""
+    def early_agg0(self) -> bool:
+        """Bottom gather+aggregate in the sample half (no weights involved); kept
+        in the train half when hot embeddings are injected (its skip mask comes
+        from the store lookup) or with HG_EARLY_AGG=0."""
+        return self.hot is None and os.environ.get("HG_EARLY_AGG", "1") != "0"
+
+    def _bottom_bufs(self):
+        """(self rows, aggregate) buffers of the bottom layer for the current set."""
+        k = self.cur if self.early_agg0() else 0
+        return self._self_bufs[k], self._agg0s[k]
+
+    def _enqueue_agg0(self, s, inj=None):
+        smp = self.samplers[0]
+        fr, n = self.frontier(0)
+        sb, ag = self._bottom_bufs()
+        _lib.call("hg_aggregate_fwd", 0 if self.sage else 1, 1, ptr(self.dg.features), self.dg.feat_ld, self.ld[0],
+                  ptr(fr), ptr(n), self.cap_dst[0], self.fan[0], ptr(smp.counts), ptr(smp.slots),
+                  ptr(smp.slot_local), ptr(smp.nself), ptr(smp.outdeg), ptr(inj), ptr(sb if self.sage else None),
+                  self.ld[0], ptr(ag), self.ld[0], s)
+
+    def enqueue_sample_part(self, stream=None, mark=None):
+        """Blocks L-1..0 of the current set (+ the bottom aggregation when
+        early_agg0); the transposed (backward) views of the CSC path are built on
+        a side stream (a parallel graph branch) joined at the end."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
+        mark = mark or (lambda name: None)
         sc = self.side[1]
         for l in range(self.L - 1, -1, -1):
             fr, n = self.frontier(l)
@@ -319,6 +347,9 @@ class TrainEngine:
                 self.samplers[l].build_csc(n, sc, frontier=fr)
         if self.L > 1 and not self.bwd_scatter:
             main.wait_stream(sc)
+        if self.early_agg0():
+            mark("sample_agg0")
+            self._enqueue_agg0(main.cuda_stream)
 
     def enqueue_train_part(self, stream=None, mark=None):
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -345,20 +376,24 @@ class TrainEngine:
                 hin, ld_in, glob = g.features, g.feat_ld, 1
             else:
                 hin, ld_in, glob = self.out[l - 1], self.ld[l], 0
-            self_out = self.self_buf if (l == 0 and self.sage) else None
             mark("fwd0_agg" if l == 0 else "fwd_upper" if l == 1 else "")
-            _lib.call("hg_aggregate_fwd", model, glob, ptr(hin), ld_in, self.ld[l], ptr(fr), ptr(n),
-                      self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
-                      ptr(smp.nself), ptr(smp.outdeg), ptr(inj if l == 0 else None), ptr(self_out),
-                      self.ld[0], ptr(self.agg[l]), self.ld[l], s)
+            sb0, ag0 = self._bottom_bufs()
+            agg_l = ag0 if l == 0 else self.agg[l]
+            if l == 0:
+                if not self.early_agg0():
+                    self._enqueue_agg0(s, inj)
+            else:
+                _lib.call("hg_aggregate_fwd", model, glob, ptr(hin), ld_in, self.ld[l], ptr(fr), ptr(n),
+                          self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
+                          ptr(smp.nself), ptr(smp.outdeg), None, None, self.ld[0], ptr(agg_l), self.ld[l], s)
             act = 1 if l < L - 1 else 0
             mark("fwd0_gemm" if l == 0 else "")
             if self.sage:  # [h_self | mean] [W_self; W_neigh]
-                a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
-                dense.fwd(ptr(a1), lda1, ptr(self.agg[l]), self.ld[l], d_in, ptr(P.view(l, 0)), d_out,
+                a1, lda1 = (sb0, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
+                dense.fwd(ptr(a1), lda1, ptr(agg_l), self.ld[l], d_in, ptr(P.view(l, 0)), d_out,
                           ptr(self.out[l]), self.ld[l + 1], ptr(n), self.cap_dst[l], act, s, img=self.img_fwd[l])
             else:
-                dense.fwd(ptr(self.agg[l]), self.ld[l], None, 0, d_in, ptr(P.view(l, 0)), d_out, ptr(self.out[l]),
+                dense.fwd(ptr(agg_l), self.ld[l], None, 0, d_in, ptr(P.view(l, 0)), d_out, ptr(self.out[l]),
                           self.ld[l + 1], ptr(n), self.cap_dst[l], act, s, img=self.img_fwd[l])
             if l == 0 and inj is not None:
                 _lib.call("hg_inject_rows", ptr(hot.inj_mask), ptr(hot.inj_slot), ptr(n), self.cap_dst[0],
@@ -380,13 +415,15 @@ class TrainEngine:
             d_in, d_out = self.dims[l], self.dims[l + 1]
             sw.wait_stream(main)
             ws_ = sw.cuda_stream
+            sb0, ag0 = self._bottom_bufs()
+            agg_l = ag0 if l == 0 else self.agg[l]
             if self.sage:  # dW_self = h_self^T dz, dW_neigh = mean^T dz (gnnmath.py:190-191)
-                a1, lda1 = (self.self_buf, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
-                dense.wgrad(ptr(a1), lda1, ptr(self.agg[l]), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1],
+                a1, lda1 = (sb0, self.ld[0]) if l == 0 else (self.out[l - 1], self.ld[l])
+                dense.wgrad(ptr(a1), lda1, ptr(agg_l), self.ld[l], d_in, ptr(self.dz[l]), self.ld[l + 1],
                             d_out, ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), ptr(P.view(l, 1, P.grad)),
                             ptr(self.wgrad_ws), ws_)
             else:  # dW = agg^T dz (gnnmath.py:135)
-                dense.wgrad(ptr(self.agg[l]), self.ld[l], None, 0, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
+                dense.wgrad(ptr(agg_l), self.ld[l], None, 0, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
                             ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), ws_)
             if l == 0:
                 continue
@@ -478,19 +515,31 @@ class TrainEngine:
         return g
 
     def capture_segments(self, split_at=(), stream: torch.cuda.Stream | None = None, set_index: int = 0):
-        """Capture the TRAIN half of set ``set_index`` as consecutive graphs split
+        """Capture the halves of set ``set_index`` as consecutive graphs split
         before the marks in ``split_at`` (so a caller can record CUDA events between
-        segments, e.g. around the dominant kernel), plus its sample half.
-        Returns (sample_graph, [(first_mark, graph), ...])."""
+        segments, e.g. around the dominant kernel).  Returns (sample, [(first_mark,
+        graph), ...]) where sample is one graph, or a [(mark, graph), ...] list when
+        a mark split the sample half too."""
         stream = stream or torch.cuda.Stream(device=self.device)
         if self.g_sample is None:
             self._warmup(stream)
         self.cur = set_index
-        gs = _new_graph()
+        ssegs = []
+        scur = {"g": _new_graph(), "name": "start"}
+
+        def smark(name):
+            if name in split_at:
+                scur["g"].capture_end()
+                ssegs.append((scur["name"], scur["g"]))
+                scur["g"], scur["name"] = _new_graph(), name
+                scur["g"].capture_begin()
+
         with torch.cuda.stream(stream):
-            gs.capture_begin()
-            self.enqueue_sample_part()
-            gs.capture_end()
+            scur["g"].capture_begin()
+            self.enqueue_sample_part(mark=smark)
+            scur["g"].capture_end()
+            ssegs.append((scur["name"], scur["g"]))
+        gs = ssegs[0][1] if len(ssegs) == 1 else ssegs
         segs = []
         cur = {"g": _new_graph(), "name": "start"}
 
@@ -507,7 +556,7 @@ class TrainEngine:
             cur["g"].capture_end()
             segs.append((cur["name"], cur["g"]))
         self.cur = 0
-        for g in [gs] + [g for _, g in segs]:
+        for g in [g for _, g in ssegs] + [g for _, g in segs]:
             if hasattr(g, "instantiate"):
                 try:
                     g.instantiate()
