@@ -121,6 +121,23 @@ int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* hin, int32_
                      const int32_t* counts, const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself,
                      const int32_t* outdeg, const uint8_t* inj_mask, float* self_out, int32_t ld_self,
                      float* agg_out, int32_t ld_agg, void* stream);
+/* Bottom-layer hg_aggregate_fwd over a feature table row-sharded across devices
+ * (C4, features larger than one GPU): shard_ptrs is a HOST array of n_shards (<= 8)
+ * device pointers (NVLink peer pointers from hg_ipc_open_handle, or slices of one
+ * table), each holding rows_per_shard rows of stride ld_in; row v lives in shard
+ * v / rows_per_shard.  Outputs are bit-identical to the unsharded call. */
+int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard_ptrs, int32_t n_shards, int32_t rows_per_shard,
+                             int32_t ld_in, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
+                             int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                             const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg,
+                             const uint8_t* inj_mask, float* self_out, int32_t ld_self, float* agg_out,
+                             int32_t ld_agg, void* stream);
+/* CUDA IPC between the per-GPU processes (64-byte cudaIpcMemHandle_t blobs); the
+ * handle names dptr's whole allocation and *out_offset locates dptr inside it */
+int hg_ipc_get_handle(const void* dptr, uint8_t* out_handle64, int64_t* out_offset);
+int hg_ipc_open_handle(const uint8_t* handle64, void** out_ptr);
+int hg_ipc_close(void* ptr);
+int hg_enable_peer_access(int32_t peer_device);
 int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself, int32_t ld_dself,
                      int32_t F, const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
                      const int32_t* counts, const int32_t* slot_g, const int32_t* nself, const int32_t* outdeg,

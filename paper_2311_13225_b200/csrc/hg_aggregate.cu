@@ -42,13 +42,30 @@ __device__ __forceinline__ float gcn_w(int outdeg_s, int indeg_d) {
     return (float)(1.0 / sqrt((double)outdeg_s * (double)indeg_d));
 }
 
-template <int LPR, int NV, int MODE>
+// Feature table row-sharded over devices (C4: features larger than one GPU's
+// HBM): row v lives in shard v / rows_per_shard, at row v % rows_per_shard; the
+// bases are NVLink peer pointers (CUDA IPC) or slices of one local table.
+constexpr int HG_MAX_SHARDS = 8;
+struct FeatShards {
+    const float* base[HG_MAX_SHARDS];
+    int n;
+    int rows_per_shard;
+};
+
+template <int LPR, int NV, int MODE, bool SH = false>
 __global__ void __launch_bounds__(256) k_agg_fwd(
     const float* __restrict__ hin, int ld_in, int F4, const int* __restrict__ frontier, const int* d_n, int cap,
     int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
     const int* __restrict__ nself, const int* __restrict__ outdeg, const uint8_t* __restrict__ inj,
-    float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out, int ld_agg) {
+    float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out, int ld_agg, const FeatShards shards) {
     hg_pdl_begin();
+    auto rowp = [&](int v) -> const float4* {
+        if (SH) {
+            const int k = v / shards.rows_per_shard;
+            return reinterpret_cast<const float4*>(shards.base[k] + (int64_t)(v - k * shards.rows_per_shard) * ld_in);
+        }
+        return reinterpret_cast<const float4*>(hin + (int64_t)v * ld_in);
+    };
     constexpr bool GLOBAL = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL);
     constexpr bool GCN = (MODE == M_GCN_LOCAL || MODE == M_GCN_GLOBAL);
     const int n = hg_load_count(d_n, cap);
@@ -67,7 +84,7 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
         const int v = frontier[i];
         if (!skip) {
             if (GLOBAL && self_out) {  // self row gather (the SAGE/GCN-free "gather" part)
-                const float4* src = reinterpret_cast<const float4*>(hin + (int64_t)v * ld_in);
+                const float4* src = rowp(v);
                 float4* dst = reinterpret_cast<float4*>(self_out + (int64_t)i * ld_self);
 #pragma unroll
                 for (int k = 0; k < NV; ++k) {
@@ -105,7 +122,7 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
                     float4 x[U][NV];
 #pragma unroll
                     for (int t = 0; t < U; ++t) {
-                        const float4* rp = reinterpret_cast<const float4*>(hin + (int64_t)(r[t] < 0 ? 0 : r[t]) * ld_in);
+                        const float4* rp = rowp(r[t] < 0 ? 0 : r[t]);
 #pragma unroll
                         for (int k = 0; k < NV; ++k) {
                             const int c = lr + k * LPR;
@@ -276,11 +293,11 @@ __global__ void k_swr_rows(const int64_t* __restrict__ edge_src, const double* _
     }
 }
 
-template <int MODE>
+template <int MODE, bool SH = false>
 int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld_in, int F4, const int* frontier,
                const int* d_n, int cap, int f, const int* counts, const int* slot_g, const int* slot_local,
                const int* nself, const int* outdeg, const uint8_t* inj, float* self_out, int ld_self,
-               float* agg_out, int ld_agg) {
+               float* agg_out, int ld_agg, const FeatShards& shards = FeatShards{}) {
     // bottom layer (rows by global id): persisting L2 window over the hot feature rows
     cudaLaunchAttribute attr[2];
     int na = 0;
@@ -299,8 +316,9 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
     cfg.numAttrs = na;
 #define HG_FWD(L, V)                                                                                      \
     if (LPR == L && NV == V) {                                                                            \
-        cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE>, hin, ld_in, F4, frontier, d_n, cap, f, counts,    \
-                           slot_g, slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, ld_agg);   \
+        cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE, SH>, hin, ld_in, F4, frontier, d_n, cap, f, counts, \
+                           slot_g, slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, ld_agg,    \
+                           shards);                                                                        \
         return HG_OK;                                                                                     \
     }
     HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 8)
@@ -380,6 +398,48 @@ extern "C" int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* 
     }
     if (rc) { hg_set_error("aggregate_fwd: unsupported width"); return rc; }
     return hg_check_launch("aggregate_fwd");
+}
+
+// hg_aggregate_fwd for the bottom layer with the feature table row-sharded over
+// devices: shard_ptrs (host array of n_shards device pointers: peer pointers from
+// hg_ipc_open_handle, or slices of one table) each hold rows_per_shard rows of
+// stride ld_in.  Same outputs, bit for bit, as the unsharded call.
+extern "C" int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard_ptrs, int32_t n_shards,
+                                        int32_t rows_per_shard, int32_t ld_in, int32_t F, const int32_t* frontier,
+                                        const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                                        const int32_t* counts, const int32_t* slot_g, const int32_t* slot_local,
+                                        const int32_t* nself, const int32_t* outdeg, const uint8_t* inj_mask,
+                                        float* self_out, int32_t ld_self, float* agg_out, int32_t ld_agg,
+                                        void* stream) {
+    if (n_shards < 1 || n_shards > HG_MAX_SHARDS || rows_per_shard < 1) {
+        hg_set_error("aggregate_fwd_sharded: 1..%d shards with rows_per_shard >= 1", HG_MAX_SHARDS);
+        return HG_EINVAL;
+    }
+    if (F % 4 || ld_in % 4 || ld_agg % 4 || (self_out && ld_self % 4)) {
+        hg_set_error("aggregate_fwd_sharded: F and row strides must be multiples of 4");
+        return HG_EINVAL;
+    }
+    if (F > 1024) { hg_set_error("aggregate_fwd_sharded: F > 1024 unsupported"); return HG_EUNSUPPORTED; }
+    if (cap_dst == 0) return HG_OK;
+    FeatShards sh{};
+    for (int i = 0; i < n_shards; ++i) {
+        if (!shard_ptrs[i] || (reinterpret_cast<uintptr_t>(shard_ptrs[i]) & 15)) {
+            hg_set_error("aggregate_fwd_sharded: shard %d pointer null or not 16-byte aligned", i);
+            return HG_EINVAL;
+        }
+        sh.base[i] = shard_ptrs[i];
+    }
+    sh.n = n_shards;
+    sh.rows_per_shard = rows_per_shard;
+    const int F4 = F / 4;
+    int LPR, NV;
+    pick_lanes(F4, LPR, NV);
+    dim3 g(hg_grid((long long)cap_dst * LPR, 256, agg_ctas_per_sm()));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int rc = model ? launch_fwd<M_GCN_GLOBAL, true>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh)
+                         : launch_fwd<M_SAGE_GLOBAL, true>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh);
+    if (rc) { hg_set_error("aggregate_fwd_sharded: unsupported width"); return rc; }
+    return hg_check_launch("aggregate_fwd_sharded");
 }
 
 extern "C" int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself,

@@ -1,3 +1,4 @@
+#include <cuda.h>
 // Error plumbing, device-wide exclusive scan and stable LSD radix sort.
 //
 // Both primitives are deterministic (no float atomics; stable ordering) and
@@ -360,3 +361,52 @@ bool hg_pdl_enabled() {
     return g_pdl == 1;
 }
 void hg_set_pdl(int v) { g_pdl = v ? 1 : 0; }
+
+// ---------------------------------------------------------------------------
+// CUDA IPC: export / import device allocations between the per-GPU processes
+// (NVLink peer pointers for the row-sharded feature table)
+// ---------------------------------------------------------------------------
+// The handle names the whole allocation (a caching allocator may sub-allocate):
+// *out_offset = dptr - allocation base, to add to the importer's mapping.
+extern "C" int hg_ipc_get_handle(const void* dptr, uint8_t* out_handle64, int64_t* out_offset) {
+    typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range = nullptr;
+    if (!range) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            range = reinterpret_cast<RangeFn>(p);
+    }
+    if (!range) { hg_set_error("ipc_get_handle: cuMemGetAddressRange unavailable"); return HG_ECUDA; }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)dptr) != CUDA_SUCCESS) { hg_set_error("ipc_get_handle: address range"); return HG_ECUDA; }
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, (void*)base) != cudaSuccess) return hg_check_launch("ipc_get_handle");
+    memcpy(out_handle64, &h, sizeof(h));
+    *out_offset = (int64_t)((CUdeviceptr)dptr - base);
+    return HG_OK;
+}
+
+extern "C" int hg_ipc_open_handle(const uint8_t* handle64, void** out_ptr) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    if (cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return hg_check_launch("ipc_open_handle");
+    return HG_OK;
+}
+
+extern "C" int hg_ipc_close(void* ptr) {
+    if (cudaIpcCloseMemHandle(ptr) != cudaSuccess) return hg_check_launch("ipc_close");
+    return HG_OK;
+}
+
+extern "C" int hg_enable_peer_access(int32_t peer_device) {
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return HG_OK;
+    }
+    return hg_check_launch("enable_peer_access");
+}

@@ -327,6 +327,13 @@ class TrainEngine:
         smp = self.samplers[0]
         fr, n = self.frontier(0)
         sb, ag = self._bottom_bufs()
+        sh = getattr(self.dg, "shards", None)
+        if sh is not None:  # feature rows spread over the box's GPUs (parallel.ShardedFeatures)
+            _lib.call("hg_aggregate_fwd_sharded", 0 if self.sage else 1, sh.ptrs, sh.n_shards, sh.rows_per_shard,
+                      sh.ld, self.ld[0], ptr(fr), ptr(n), self.cap_dst[0], self.fan[0], ptr(smp.counts),
+                      ptr(smp.slots), ptr(smp.slot_local), ptr(smp.nself), ptr(smp.outdeg), ptr(inj),
+                      ptr(sb if self.sage else None), self.ld[0], ptr(ag), self.ld[0], s)
+            return
         _lib.call("hg_aggregate_fwd", 0 if self.sage else 1, 1, ptr(self.dg.features), self.dg.feat_ld, self.ld[0],
                   ptr(fr), ptr(n), self.cap_dst[0], self.fan[0], ptr(smp.counts), ptr(smp.slots),
                   ptr(smp.slot_local), ptr(smp.nself), ptr(smp.outdeg), ptr(inj), ptr(sb if self.sage else None),

@@ -196,7 +196,8 @@ class Trainer:
         config.validate()
         self.cfg = config
         self.ds = ds
-        self.dg = ds if isinstance(ds, DeviceGraph) else DeviceGraph.from_dataset(ds, device=device)
+        given = ds if isinstance(ds, DeviceGraph) else getattr(ds, "device_graph", None)
+        self.dg = given if given is not None else DeviceGraph.from_dataset(ds, device=device)
         if not hasattr(self.dg, "l2_window"):
             self.dg.persist_hot_rows()
         self.train_ids = np.nonzero(np.asarray(ds.train_mask))[0].astype(np.int64)
@@ -553,6 +554,8 @@ class _Merged:
     """(Graph, VertexData) viewed as one dataset object."""
 
     def __init__(self, graph, data):
+        # an already-resident DeviceGraph (e.g. with row-sharded features) is used as is
+        self.device_graph = graph if isinstance(graph, DeviceGraph) else None
         self.offsets, self.targets = graph.offsets, graph.targets
         self.features, self.labels = data.features, data.labels
         self.train_mask, self.val_mask, self.test_mask = data.train_mask, data.val_mask, data.test_mask

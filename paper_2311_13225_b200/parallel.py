@@ -65,3 +65,71 @@ class DistContext:
 
     def barrier(self):
         dist.barrier()
+
+
+class ShardedFeatures:
+    """Feature table row-sharded over the ranks of one box (SURVEY §8(e), C4:
+    features larger than one GPU's HBM).  Rank r keeps rows
+    [r*rows_per_shard, (r+1)*rows_per_shard) in its own HBM, exports the shard
+    through CUDA IPC, and opens every other rank's shard, so the bottom gather
+    (hg_aggregate_fwd_sharded) reads remote rows in place over NVLink — no
+    all-to-all exchange step.  ``all_gather`` is any list-gathering callable
+    (torch.distributed.all_gather_object over gloo or NCCL).
+
+    With world == 1 the shards may also be carved out of one local table
+    (``local_slices``) — the same kernel, used by the single-GPU tests."""
+
+    def __init__(self, features: np.ndarray, rank: int, world: int, all_gather=None, device=None,
+                 local_slices: int = 0):
+        import ctypes
+
+        from . import _lib
+        from .device import pad4
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        feats = np.asarray(features, dtype=np.float32)
+        V, F = feats.shape
+        self.num_vertices, self.feat_dim, self.ld = V, F, pad4(F)
+        n_shards = local_slices if local_slices else world
+        if not 1 <= n_shards <= 8:
+            raise ValueError("1..8 feature shards")
+        self.n_shards = n_shards
+        self.rows_per_shard = (V + n_shards - 1) // n_shards
+        self._opened = []
+        lib = _lib.load()
+        if local_slices:  # one table, n slices (single process)
+            x = torch.zeros((n_shards * self.rows_per_shard, self.ld), dtype=torch.float32, device=self.device)
+            x[:V, :F] = torch.as_tensor(feats, device=self.device)
+            self.local = x
+            ptrs = [x[k * self.rows_per_shard].data_ptr() for k in range(n_shards)]
+        else:
+            lo = rank * self.rows_per_shard
+            hi = min(V, lo + self.rows_per_shard)
+            x = torch.zeros((self.rows_per_shard, self.ld), dtype=torch.float32, device=self.device)
+            if hi > lo:
+                x[:hi - lo, :F] = torch.as_tensor(feats[lo:hi], device=self.device)
+            self.local = x
+            torch.cuda.synchronize(self.device)
+            handle = (ctypes.c_uint8 * 64)()
+            off = ctypes.c_int64(0)
+            _lib.call("hg_ipc_get_handle", x.data_ptr(), handle, ctypes.byref(off))
+            mine = (bytes(handle), int(off.value), int(self.device.index or 0))
+            allh = all_gather(mine) if world > 1 else [mine]
+            ptrs = []
+            for r, (h, o, dev) in enumerate(allh):
+                if r == rank:
+                    ptrs.append(x.data_ptr())
+                    continue
+                if dev != (self.device.index or 0):
+                    _lib.call("hg_enable_peer_access", dev)
+                p = ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+                _lib.call("hg_ipc_open_handle", buf, ctypes.byref(p))
+                self._opened.append(p.value)
+                ptrs.append(p.value + o)
+        self.ptrs = (ctypes.c_void_p * n_shards)(*ptrs)
+        self._lib = lib
+
+    def close(self):
+        for p in self._opened:
+            self._lib.hg_ipc_close(p)
+        self._opened = []
