@@ -231,8 +231,10 @@ def main():
         dist.all_reduce(t)  # NCCL warm-up outside capture
     dev = torch.device("cuda", torch.cuda.current_device())
     ds = make_dataset("c2", cache_dir=CACHE)
+    # report_transfers=False: the per-batch CSV bookkeeping (needed-row counting) is
+    # not part of training and no report is written here
     cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
-                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0)
+                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0, report_transfers=False)
     tr = Trainer(ds, cfg, dist=dist_ctx)
     e = tr.engine
     # instrumented copies of every set's graphs, split so CUDA events bracket the

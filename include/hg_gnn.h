@@ -209,6 +209,14 @@ int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32_t lda2, in
                 int32_t ldg, int32_t N, const int32_t* d_M, int32_t M_cap, float* out1, float* out2, float* ws,
                 void* stream);
 
+/* Per-batch needed bottom rows (transfer.py:59-73; the batch CSV's raw_rows): distinct
+ * sources of non-injected destinations + their self rows, added to
+ * out[bp[3]]; tag_of: int32[V] (any initial contents below 0 / never equal to a
+ * future reading_batch + 1), tag = bp[2] + 1. */
+int hg_count_needed_rows(const int32_t* frontier, const int32_t* d_n, int32_t cap, int32_t fanout,
+                         const int32_t* counts, const int32_t* slots, const uint8_t* inj_mask, const int64_t* bp,
+                         int32_t* tag_of, int32_t* out, void* stream);
+
 /* ---- K9/K10 loss and updates (gnnmath.py:263-312; orchestrator.py:246-255) */
 /* dlogits = (softmax - onehot) / *d_div (d_div NULL: / n); *d_loss = mean CE over
  * the n = min(*d_n, cap) rows; labels indexed by seeds[r] (seeds NULL: by r).

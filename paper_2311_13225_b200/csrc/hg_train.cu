@@ -435,3 +435,46 @@ extern "C" int hg_argmax_correct(const float* logits, int32_t ld, int32_t C, int
                                                                            (unsigned long long*)d_correct);
     return hg_check_launch("argmax_correct");
 }
+
+// --------------------------------------------------------------------------
+// Per-batch transfer accounting (transfer.py:59-73 needed_bottom_rows, reported
+// as the batch CSV's raw_rows, reporting.py:23-27): the number of distinct
+// bottom-block source vertices feeding a computed (non-injected) destination,
+// plus the computed destinations' own self rows.  First-writer counting on a
+// per-vertex tag table (atomicExch(tag_of[v], tag) != tag counts v once) gives
+// the exact distinct count in any order; tag = reading batch + 1, so the table
+// is never reset.  out[bp[BATCH_IN_EPOCH]] += count.
+// --------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(256) k_count_needed(const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                                                      const int* __restrict__ counts, const int* __restrict__ slots,
+                                                      const uint8_t* __restrict__ inj, const int64_t* __restrict__ bp,
+                                                      int* __restrict__ tag_of, int* __restrict__ out) {
+    hg_pdl_begin();
+    const int n = hg_load_count(d_n, cap);
+    const int tag = (int)bp[BP_READING_BATCH] + 1;
+    const long long Q = (long long)n * (f + 1);
+    int c = 0;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Q; q += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(q / (f + 1)), j = (int)(q - (long long)i * (f + 1));
+        if (inj && inj[i]) continue;  // injected destination: nothing of it is computed
+        int v;
+        if (j == f) v = frontier[i];  // the destination's own self row
+        else if (j < counts[i]) v = slots[(int64_t)i * f + j];
+        else continue;
+        if (atomicExch(&tag_of[v], tag) != tag) ++c;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&out[(int)bp[BP_BATCH_IN_EPOCH]], c);
+}
+}  // namespace
+
+extern "C" int hg_count_needed_rows(const int32_t* frontier, const int32_t* d_n, int32_t cap, int32_t fanout,
+                                    const int32_t* counts, const int32_t* slots, const uint8_t* inj_mask,
+                                    const int64_t* bp, int32_t* tag_of, int32_t* out, void* stream) {
+    if (cap <= 0) return HG_OK;
+    hg_launch(k_count_needed, hg_grid((long long)cap * (fanout + 1), 256, 8), 256, 0, (cudaStream_t)stream, frontier,
+              d_n, cap, fanout, counts, slots, inj_mask, bp, tag_of, out);
+    return hg_check_launch("count_needed_rows");
+}

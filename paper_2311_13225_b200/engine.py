@@ -236,6 +236,11 @@ class TrainEngine:
         self.d_maxdelta = z32(2)  # max |dw| bits + the fused update's last-block ticket
         self.loss_arr = zf(max(max_batches, 1))
         self.md_arr = zf(max(max_batches, 1))
+        # per-batch needed bottom rows (the reference's transfer accounting,
+        # transfer.py:59-73) on a side branch of the train half
+        self.raw_rows_arr = z32(max(max_batches, 1))
+        self.account_rows = True  # TrainConfig.report_transfers
+        self.need_tag = torch.full((max(V, 1),), -1, dtype=torch.int32, device=dev)
         self.side = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
         # tensor-core B operand images, rebuilt from the current weights each step
         self.img_fwd = [dense.BImage(self.dims[l], self.dims[l] if self.sage else 0, self.dims[l + 1], 1, dev)
@@ -462,6 +467,11 @@ class TrainEngine:
                       ptr(self.out[l - 1]), self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]),
                       self.ld[l], ptr(smp.csc_dst), ptr(smp.csc_w), s)
         main.wait_stream(sw)
+        if self.account_rows:  # the reference's per-batch transfer accounting (bookkeeping only)
+            fr0, n0 = self.frontier(0)
+            smp0 = self.samplers[0]
+            _lib.call("hg_count_needed_rows", ptr(fr0), ptr(n0), self.cap_dst[0], self.fan[0], ptr(smp0.counts),
+                      ptr(smp0.slots), ptr(inj), ptr(self.bp), ptr(self.need_tag), ptr(self.raw_rows_arr), s)
         # ---------------- update ----------------
         mark("update")
         if self.allreduce is not None:
@@ -601,6 +611,8 @@ class TrainEngine:
         """The warm-up pass ran one real update; undo it so capture is side-effect free."""
         self.params.flat.copy_(st["flat"])
         self.fx_flags.zero_()  # the warm-up ran on unfed (empty) sample sets
+        self.need_tag.fill_(-1)  # ... and tagged vertices for the row accounting
+        self.raw_rows_arr.zero_()
         self.d_maxdelta.copy_(st["md"])
         self.loss_arr.copy_(st["loss"])
         self.md_arr.copy_(st["mdarr"])

@@ -64,6 +64,7 @@ class TrainConfig:
     simulate_costs: bool = False  # accepted for compatibility; the simulator is out of scope
     preset: object = None
     use_graph: bool = True  # replay each step as one captured CUDA graph
+    report_transfers: bool = True  # per-batch needed-row accounting for the batch CSV (transfer.py:59-73)
 
     def validate(self) -> None:
         if self.model not in ("gcn", "sage"):
@@ -212,6 +213,7 @@ class Trainer:
         self.engine = TrainEngine(self.dg, config.model, self.dims, self.fan, config.batch_size, config.lr,
                                   optimizer=config.optimizer, weights=weights, max_batches=n_batches,
                                   allreduce=dist.allreduce if dist is not None else None)
+        self.engine.account_rows = bool(config.report_transfers)
         self.version = 0
         # ---- hot list (hotness.py:70-108 via orchestrator.py:692-702) ----
         if hot_list is None:
@@ -296,6 +298,7 @@ class Trainer:
         nb = len(plan.batches)
         if hot is not None:
             hot.reset_counters()
+        e.raw_rows_arr.zero_()
         if self.use_hot and self.producer is None:
             cap = max([plan.queue_sizes.get(g, 0) for g in plan.queue_sizes] + [1])
             cap = (cap + cfg.super_batch_n - 1) // cfg.super_batch_n
@@ -385,12 +388,20 @@ class Trainer:
         rep.max_weight_deltas = e.md_arr[:nb].double().cpu().tolist()
         hits = hot.batch_hits[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)
         miss = hot.batch_miss[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)
+        raw_rows = e.raw_rows_arr[:nb].cpu().numpy()
+        feat_dim = self.dg.feat_dim
+        # batch CSV transfer columns (orchestrator.py:505-543): raw features of the needed
+        # rows; embeddings / aux move per super-batch, not per batch; the bottom weights'
+        # gradient elements when the bottom layer is split off (layer-based, L > 1)
+        grad_elems = (self.engine.params.bottom_numel if (self.layer_based and cfg.layers > 1) else 0)
         for g, group in enumerate(plan.groups):
             rep.epsilon_trace.append(max(rep.max_weight_deltas[b] for b in group) * 2 * cfg.super_batch_n)
             for b in group:
                 rep.batch_rows.append({"epoch": plan.epoch, "batch": plan.first_global_batch + b, "super_batch": g,
                                        "loss": rep.losses[b], "reuse_hits": int(hits[b]), "fallbacks": int(miss[b]),
-                                       "max_weight_delta": rep.max_weight_deltas[b]})
+                                       "raw_rows": int(raw_rows[b]), "cache_hit_rows": 0,
+                                       "raw_elems": int(raw_rows[b]) * feat_dim, "emb_elems": 0, "aux_elems": 0,
+                                       "grad_elems": int(grad_elems), "max_weight_delta": rep.max_weight_deltas[b]})
         rep.reuse_hits, rep.fallbacks = int(hits.sum()), int(miss.sum())
         if hot is not None:
             rep.warmup_computed = int(hot.batch_warm[:nb].sum().item())

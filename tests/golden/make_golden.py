@@ -195,6 +195,13 @@ def main():
                 "max_weight_deltas": r.max_weight_deltas,
                 "reuse_hits": [row["reuse_hits"] for row in r.batch_rows],
                 "fallbacks": [row["fallbacks"] for row in r.batch_rows],
+                # transfer-accounting columns of the per-batch CSV (reporting.py:23-27)
+                "raw_rows": [row["raw_rows"] for row in r.batch_rows],
+                "cache_hit_rows": [row["cache_hit_rows"] for row in r.batch_rows],
+                "raw_elems": [row["raw_elems"] for row in r.batch_rows],
+                "emb_elems": [row["emb_elems"] for row in r.batch_rows],
+                "aux_elems": [row["aux_elems"] for row in r.batch_rows],
+                "grad_elems": [row["grad_elems"] for row in r.batch_rows],
                 "stage_events": [list(e) for e in r.stage_events],
                 "max_gap": r.max_gap, "max_gap_batch": r.max_gap_batch,
                 "warmup_computed": r.warmup_computed,

@@ -69,6 +69,8 @@ def test_training_matches_reference(golden, golden_meta, ggraphs, name):
         np.testing.assert_allclose(rep.losses, want["losses"], rtol=2e-3)
         assert [r["reuse_hits"] for r in rep.batch_rows] == want["reuse_hits"]
         assert [r["fallbacks"] for r in rep.batch_rows] == want["fallbacks"]
+        for col in ("raw_rows", "cache_hit_rows", "raw_elems", "emb_elems", "aux_elems", "grad_elems"):
+            assert [r[col] for r in rep.batch_rows] == want[col], col  # batch CSV transfer columns
         assert [list(e) for e in rep.stage_events] == want["stage_events"]
         assert rep.warmup_computed == want["warmup_computed"]
         if meta["config"].get("strategy", "layer-based") == "layer-based":

@@ -18,7 +18,7 @@ def main():
     K = 100
     ds = make_dataset("c2", cache_dir=bench.CACHE)
     cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
-                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0)
+                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0, report_transfers=False)
     tr = Trainer(ds, cfg)
     e = tr.engine
     batches, rseeds = bench.epoch_batches(ds, K + 4)

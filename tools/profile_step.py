@@ -23,7 +23,7 @@ def main():
     workload = sys.argv[1] if len(sys.argv) > 1 else "c2"
     ds = make_dataset(workload, cache_dir="/tmp/hg_bench_cache")
     cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
-                      strategy="case1", hot_ratio=0.0, use_graph=False)
+                      strategy="case1", hot_ratio=0.0, use_graph=False, report_transfers=False)
     tr = Trainer(ds, cfg)
     order = runplan.shuffle_epoch(ds.train_ids(), 0, 0)
     batches = runplan.split_batches(order, 1024)
