@@ -34,7 +34,8 @@ namespace {
 using namespace hgtc;
 
 constexpr int FWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-5 split, w6-9 epilogue
-constexpr int WG_THREADS = 192;   // w0 TMA, w1 MMA, w2-5 split (+ final epilogue)
+constexpr int WG_THREADS = 320;   // w0 TMA, w1 MMA, w2-9 split (w2-5 also the final epilogue)
+constexpr int WG_SPLIT = WG_THREADS - 64;
 constexpr int A_BYTES = 128 * 128;  // 128 rows x 32 fp32 (fwd) / 32 rows x 128 fp32 (wgrad)
 
 template <int BN>
@@ -529,7 +530,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
 #pragma unroll
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&splt[i], 4);
+            mbar_init(&splt[i], WG_SPLIT / 32);
             mbar_init(&empty[i], 1);
         }
         mbar_init(&done, 1);
@@ -548,6 +549,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
             for (int j = 0; j < nsteps; ++j) {
                 const int st = j % S;
                 if (j >= S) mbar_wait(&empty[st], (uint32_t)(((j / S) - 1) & 1));
+                TL(0, j);
                 uint8_t* base = smem + st * STAGE;
                 const int y = mbeg + 32 * j;
                 mbar_expect_tx(&full[st], A_BYTES + G_TILE);
@@ -563,6 +565,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
             for (int j = 0; j < nsteps; ++j) {
                 const int st = j % S;
                 mbar_wait(&splt[st], (uint32_t)((j / S) & 1));
+                TL(3, j);
                 tc_fence_after();
                 const uint32_t a_hi = smem_u32(smem + st * STAGE), a_lo = a_hi + A_BYTES;
                 const uint32_t g_hi = a_hi + 2 * A_BYTES, g_lo = g_hi + G_TILE;
@@ -581,6 +584,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                     }
                 }
                 mma_commit(&empty[st]);
+                TL(4, j);
             }
             mma_commit(&done);
         }
@@ -589,36 +593,55 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
         for (int j = 0; j < nsteps; ++j) {
             const int st = j % S;
             mbar_wait(&full[st], (uint32_t)((j / S) & 1));
+            if (warp == 2 && lane == 0) TL(1, j);
             uint8_t* base = smem + st * STAGE;
             const int valid = mend - (mbeg + 32 * j);  // rows < valid are real
+            if (!(c_dbg & 2)) {
+                // all loads of the stage first (ILP: the split is latency-bound with
+                // 4 warps), then lo = x - hi and the stores; rows past M -> zeros
+                constexpr int NA = A_BYTES / 16 / WG_SPLIT;
+                constexpr int NGC = (G_TILE / 16 + WG_SPLIT - 1) / WG_SPLIT;
+                float4 va[NA], vg[NGC];
 #pragma unroll
-            for (int i = 0; i < ((c_dbg & 2) ? 0 : A_BYTES / 16 / 128); ++i) {
-                const int off = (t + 128 * i) * 16;
-                if (((off & 4095) >> 7) < valid) {
-                    split_lo16(base + off, base + A_BYTES + off);
-                } else {
-                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                    *reinterpret_cast<float4*>(base + off) = z;
-                    *reinterpret_cast<float4*>(base + A_BYTES + off) = z;
+                for (int i = 0; i < NA; ++i) va[i] = *reinterpret_cast<const float4*>(base + (t + WG_SPLIT * i) * 16);
+                uint8_t* gb = base + 2 * A_BYTES;
+#pragma unroll
+                for (int i = 0; i < NGC; ++i)
+                    if (t + WG_SPLIT * i < G_TILE / 16) vg[i] = *reinterpret_cast<const float4*>(gb + (t + WG_SPLIT * i) * 16);
+                const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < NA; ++i) {
+                    const int off = (t + WG_SPLIT * i) * 16;
+                    if (((off & 4095) >> 7) < valid) {
+                        const float4 v = va[i];
+                        *reinterpret_cast<float4*>(base + A_BYTES + off) =
+                            make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+                    } else {
+                        *reinterpret_cast<float4*>(base + off) = z;
+                        *reinterpret_cast<float4*>(base + A_BYTES + off) = z;
+                    }
                 }
-            }
-            uint8_t* gb = base + 2 * A_BYTES;
 #pragma unroll
-            for (int i = 0; i < ((c_dbg & 2) ? 0 : G_TILE / 16 / 128); ++i) {
-                const int off = (t + 128 * i) * 16;
-                if (((off & 4095) >> 7) < valid) {
-                    split_lo16(gb + off, gb + G_TILE + off);
-                } else {
-                    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-                    *reinterpret_cast<float4*>(gb + off) = z;
-                    *reinterpret_cast<float4*>(gb + G_TILE + off) = z;
+                for (int i = 0; i < NGC; ++i) {
+                    if (t + WG_SPLIT * i >= G_TILE / 16) break;
+                    const int off = (t + WG_SPLIT * i) * 16;
+                    if (((off & 4095) >> 7) < valid) {
+                        const float4 v = vg[i];
+                        *reinterpret_cast<float4*>(gb + G_TILE + off) =
+                            make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+                    } else {
+                        *reinterpret_cast<float4*>(gb + off) = z;
+                        *reinterpret_cast<float4*>(gb + G_TILE + off) = z;
+                    }
                 }
             }
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&splt[st]);
+            if (warp == 2 && lane == 0) TL(2, j);
         }
-        // ---- epilogue: partial rows k of this K tile (TMEM lane = k - kt*128)
+        // ---- epilogue (warps 2-5, one per TMEM lane quarter): partial rows k of this K tile
+        if (warp < 6) {
         mbar_wait(&done, 0u);
         tc_fence_after();
         const int q = warp & 3;
@@ -645,6 +668,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
             }
         }
         tc_fence_before();
+        }
     }
     __syncthreads();
     if (warp == 1) {

@@ -24,10 +24,18 @@ def main():
     s = torch.cuda.current_stream().cuda_stream
     img = torch.zeros(int(lib.hg_gemm_tc_bimg_size(K, K, N)) // 4 + 4, device="cuda")
     _lib.call("hg_gemm_tc_prep_b", ptr(W), N, 1, K, K, N, ptr(img), s)
+    G = torch.randn(M, N, device="cuda")
+    o1, o2 = torch.empty(K, N, device="cuda"), torch.empty(K, N, device="cuda")
+    ws = torch.zeros(int(lib.hg_wgrad_tc_ws_size(K, N, M, 2)), device="cuda")
+    which = sys.argv[1] if len(sys.argv) > 1 else "fwd"
     for dbg in (8, 8 | 3):
         lib.hg_set_tuning(9, dbg)
         for _ in range(3):
-            _lib.call("hg_gemm_tc", ptr(A1), K, K, ptr(A2), K, K, ptr(img), ptr(C), N, N, ptr(dM), M, 1, s)
+            if which == "fwd":
+                _lib.call("hg_gemm_tc", ptr(A1), K, K, ptr(A2), K, K, ptr(img), ptr(C), N, N, ptr(dM), M, 1, s)
+            else:
+                _lib.call("hg_wgrad_tc", ptr(A1), K, ptr(A2), K, K, ptr(G), N, N, ptr(dM), M, ptr(o1), ptr(o2),
+                          ptr(ws), s)
         torch.cuda.synchronize()
         tl = np.zeros((8, 64), dtype=np.uint64)
         _lib.call("hg_debug_timeline", tl.ctypes.data)
