@@ -159,3 +159,24 @@ def test_bwd_scatter_flags_nonfinite():
     torch.cuda.synchronize()
     assert int(flags.item()) == 1
     assert int(acc.abs().sum().item()) == 0  # accumulator left cleared
+
+
+@pytest.mark.parametrize("model,fan,opt", [("sage", (40, 3), "sgd"), ("gcn", (3, 40), "adam"),
+                                           ("sage", (1,), "sgd"), ("gcn", (6, 1, 2), "sgd")])
+def test_training_edge_shapes_vs_oracle(model, fan, opt):
+    """Engine paths the golden runs do not reach — fanout > 32 (sequential draw
+    kernel) at the bottom and at the top, fanout 1, a one-layer model (no hidden
+    ReLU, logits straight from the bottom layer), a partial last batch — against
+    the CPU oracle on the same graph bytes (fp64), per-batch losses rtol 2e-3."""
+    from oracle import oracle as O
+    from paper_2311_13225_b200.datagen import make_dataset
+    from paper_2311_13225_b200.orchestrator import TrainConfig, run_training
+    ds = make_dataset("tiny")
+    kw = dict(model=model, layers=len(fan), fanouts=fan, hidden_dim=16, batch_size=96, epochs=1, lr=0.05,
+              seed=9, optimizer=opt, strategy="case1")
+    reps = run_training(ds, None, TrainConfig(**kw))
+    og = O.Graph(offsets=ds.offsets, targets=ds.targets.astype(np.int64))
+    od = O.VertexData(features=ds.features.astype(np.float64), labels=ds.labels, train_mask=ds.train_mask,
+                      val_mask=ds.val_mask, test_mask=ds.test_mask)
+    ref, _, _ = O.run_training(og, od, kw, evaluate_each_epoch=False)
+    np.testing.assert_allclose(reps[0].losses, ref[0]["losses"], rtol=2e-3)
