@@ -77,6 +77,14 @@ int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream);
  *      bumps *tag_ctr so the next use of minpos starts clean (first-occurrence
  *      entries are left holding their local id under the reserved tag 0xFFFFFFFF). */
 int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout);
+/* hg_sample_layer + hg_dedup_relabel in one call (same arguments, same outputs);
+ * optionally (hg_set_tuning key 8) blocks with fanout <= 32 and cap_dst <= 16384
+ * run as one cooperative kernel (draw | grid sync | mark/scan/emit | grid sync | relabel). */
+int hg_sample_block(const int64_t* offsets, const int32_t* targets, const int32_t* frontier, const int32_t* d_n_dst,
+                    int32_t cap_dst, int32_t fanout, const uint64_t* d_seed, int32_t layer, int32_t* counts,
+                    int32_t* slots, int32_t* slot_local, uint64_t* minpos, int32_t* tag_ctr, int32_t* src_vertices,
+                    int32_t* d_n_src, int32_t cap_src, int32_t* nself, int32_t* outdeg, int32_t* ws,
+                    int32_t* scratch, void* stream);
 int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
                      const int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
                      int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
@@ -192,7 +200,9 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
  * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always;
  * key 5: programmatic dependent launch of the step kernels, 1 (default; env HG_PDL=0 at load turns it off) / 0;
  * key 6: TS-form GEMM keeps the whole B image resident in smem when it fits, A ring released by the split warps (1) / streams B per stage (0, default);
- * key 7: paired hi|lo MMAs (N = 2*BN operand, two instructions per K slice instead of three) for BN <= 64 (1, default) / 0) */
+ * key 7: paired hi|lo MMAs (N = 2*BN operand, two instructions per K slice instead of three) for BN <= 64 (1, default) / 0;
+ * key 8: hg_sample_block runs small blocks as one cooperative kernel (1) / three kernels (0, default: the
+ *        grid syncs measured slower than the launch gaps they replace)) */
 int hg_set_tuning(int32_t key, int32_t value);
 /* profiling aid: the 8 x 64 globaltimer stamps (ns) of the tensor-core GEMM's
  * pipeline timeline probe (hg_set_tuning key 9, bit 3) */

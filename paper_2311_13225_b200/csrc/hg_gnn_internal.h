@@ -40,3 +40,5 @@ int hg_wgrad_skinny_launch(const float* A1, int lda1, const float* A2, int lda2,
 bool hg_l2_window_attr(cudaLaunchAttribute* a);
 
 void hg_set_pdl(int v);
+
+void hg_set_block_coop(int v);

@@ -27,8 +27,12 @@
 // id's first occurrence is the position that won.  The tag decreases with every
 // use of the table (a device counter bumped by the relabel kernel), so entries
 // left by earlier blocks always lose and the table never needs resetting.
+#include <cooperative_groups.h>
+
 #include "hg_common.cuh"
 #include "hg_gnn_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -56,15 +60,12 @@ __device__ __forceinline__ unsigned long long fo_key(uint32_t tag, long long pos
 // draw kernel, fanout <= 32: one W-lane segment per destination
 // --------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ offsets,
-                                                    const int* __restrict__ targets,
-                                                    const int* __restrict__ frontier, const int* d_n,
-                                                    int cap, int f, const uint64_t* __restrict__ d_seed,
-                                                    int layer, int* __restrict__ counts,
-                                                    int* __restrict__ slots, unsigned long long* __restrict__ minpos,
-                                                    const int* __restrict__ tag_ctr, int* __restrict__ nself) {
-    hg_pdl_begin();
-    __shared__ int s_last[256];
+__device__ __forceinline__ void draw_seg_body(const int64_t* __restrict__ offsets, const int* __restrict__ targets,
+                                              const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                                              const uint64_t* __restrict__ d_seed, int layer,
+                                              int* __restrict__ counts, int* __restrict__ slots,
+                                              unsigned long long* __restrict__ minpos, const int* __restrict__ tag_ctr,
+                                              int* __restrict__ nself, int* s_last) {
     const int n = hg_load_count(d_n, cap);
     const uint32_t tag = minpos ? fo_tag(tag_ctr) : 0u;
     const uint64_t stream = layer >= 0 ? hg_derive2(*d_seed, HG_SAMPLE_TAG, (uint64_t)layer) : *d_seed;
@@ -122,6 +123,20 @@ __global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ 
             if (sub == 0) nself[i] = __popc(ns);
         }
     }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_sample_seg(const int64_t* __restrict__ offsets,
+                                                    const int* __restrict__ targets,
+                                                    const int* __restrict__ frontier, const int* d_n,
+                                                    int cap, int f, const uint64_t* __restrict__ d_seed,
+                                                    int layer, int* __restrict__ counts,
+                                                    int* __restrict__ slots, unsigned long long* __restrict__ minpos,
+                                                    const int* __restrict__ tag_ctr, int* __restrict__ nself) {
+    hg_pdl_begin();
+    __shared__ int s_last[256];
+    draw_seg_body<W>(offsets, targets, frontier, d_n, cap, f, d_seed, layer, counts, slots, minpos, tag_ctr, nself,
+                     s_last);
 }
 
 // --------------------------------------------------------------------------
@@ -217,21 +232,20 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__ frontier, const int* d_n, int cap,
-                                                         int f, const int* __restrict__ counts,
-                                                         const int* __restrict__ slots,
-                                                         unsigned long long* __restrict__ minpos,
-                                                         const int* __restrict__ tag_ctr, int* __restrict__ rank,
-                                                         int* __restrict__ src_vertices, int* __restrict__ d_n_src,
-                                                         unsigned long long* __restrict__ status,
-                                                         const int* __restrict__ d_gen, int* __restrict__ outdeg) {
-    hg_pdl_begin();
+// one tile t of the mark/scan/emit pass (t = blockIdx.x in k_markscan; a
+// strided loop over tiles in the cooperative fused block kernel)
+__device__ __forceinline__ void markscan_tile(int t, const int* __restrict__ frontier, const int* d_n, int cap,
+                                              int f, const int* __restrict__ counts, const int* __restrict__ slots,
+                                              unsigned long long* __restrict__ minpos,
+                                              const int* __restrict__ tag_ctr, int* __restrict__ rank,
+                                              int* __restrict__ src_vertices, int* __restrict__ d_n_src,
+                                              unsigned long long* __restrict__ status,
+                                              const int* __restrict__ d_gen, int* __restrict__ outdeg) {
     __shared__ int s_warp[MS_THREADS / 32];
     __shared__ int s_prefix;
     const int n = hg_load_count(d_n, cap);
     const uint32_t tag = fo_tag(tag_ctr);
     const long long P = (long long)n * (f + 1);
-    const int t = blockIdx.x;
     const long long p0 = (long long)t * MS_TILE;
     if (p0 >= P) {
         if (t == 0 && threadIdx.x == 0) *d_n_src = 0;
@@ -322,6 +336,20 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
         }
     }
     if (p0 + MS_TILE >= P && threadIdx.x == 0) *d_n_src = s_prefix + tile_total;
+    __syncthreads();  // s_warp / s_prefix are reused by the CTA's next tile
+}
+
+__global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__ frontier, const int* d_n, int cap,
+                                                         int f, const int* __restrict__ counts,
+                                                         const int* __restrict__ slots,
+                                                         unsigned long long* __restrict__ minpos,
+                                                         const int* __restrict__ tag_ctr, int* __restrict__ rank,
+                                                         int* __restrict__ src_vertices, int* __restrict__ d_n_src,
+                                                         unsigned long long* __restrict__ status,
+                                                         const int* __restrict__ d_gen, int* __restrict__ outdeg) {
+    hg_pdl_begin();
+    markscan_tile(blockIdx.x, frontier, d_n, cap, f, counts, slots, minpos, tag_ctr, rank, src_vertices, d_n_src,
+                  status, d_gen, outdeg);
 }
 
 // per destination: local id = rank[minpos[id]]; sort the segment by local id
@@ -329,14 +357,12 @@ __global__ void __launch_bounds__(MS_THREADS) k_markscan(const int* __restrict__
 // global ids back into slots and local ids into slot_local; per-dst non-self
 // count (SAGE, gnnmath.py:145-154) and block out-degree (GCN, gnnmath.py:96).
 template <int W>
-__global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict__ frontier, const int* d_n,
-                                                          int cap, int f, const int* __restrict__ counts,
-                                                          int* __restrict__ slots, int* __restrict__ slot_local,
-                                                          const unsigned long long* __restrict__ minpos,
-                                                          const int* __restrict__ rank,
-                                                          int* __restrict__ nself, int* __restrict__ outdeg,
-                                                          int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
-    hg_pdl_begin();
+__device__ __forceinline__ void relabel_seg_body(const int* __restrict__ frontier, const int* d_n, int cap, int f,
+                                                 const int* __restrict__ counts, int* __restrict__ slots,
+                                                 int* __restrict__ slot_local,
+                                                 const unsigned long long* __restrict__ minpos,
+                                                 int* __restrict__ nself, int* __restrict__ outdeg,
+                                                 int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
     const int n = hg_load_count(d_n, cap);
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // retire this use of the table and of the scan status
         *tag_ctr += 1;
@@ -371,6 +397,48 @@ __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict_
         }
         if (sub == 0 && nself) nself[i] = __popc(nonself);
     }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict__ frontier, const int* d_n,
+                                                          int cap, int f, const int* __restrict__ counts,
+                                                          int* __restrict__ slots, int* __restrict__ slot_local,
+                                                          const unsigned long long* __restrict__ minpos,
+                                                          const int* __restrict__ rank,
+                                                          int* __restrict__ nself, int* __restrict__ outdeg,
+                                                          int* __restrict__ tag_ctr, int* __restrict__ d_gen) {
+    hg_pdl_begin();
+    relabel_seg_body<W>(frontier, d_n, cap, f, counts, slots, slot_local, minpos, nself, outdeg, tag_ctr, d_gen);
+}
+
+// ---------------------------------------------------------------------------
+// Small blocks (the upper layers: a few thousand destinations) in ONE
+// cooperative launch: draw -> grid sync -> mark/scan/emit (the decoupled
+// look-back tiles strided over the co-resident CTAs) -> grid sync -> relabel.
+// Same code and results as the three-kernel sequence; two launch gaps fewer.
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(256) k_block_coop(const int64_t* __restrict__ offsets,
+                                                    const int* __restrict__ targets,
+                                                    const int* __restrict__ frontier, const int* d_n, int cap,
+                                                    int f, const uint64_t* __restrict__ d_seed, int layer,
+                                                    int* __restrict__ counts, int* __restrict__ slots,
+                                                    int* __restrict__ slot_local,
+                                                    unsigned long long* __restrict__ minpos, int* __restrict__ tag_ctr,
+                                                    int* __restrict__ src_vertices, int* __restrict__ d_n_src,
+                                                    int* __restrict__ nself, int* __restrict__ outdeg,
+                                                    int* __restrict__ rank, unsigned long long* __restrict__ status,
+                                                    int* __restrict__ d_gen, int tiles) {
+    __shared__ int s_last[256];
+    cg::grid_group grid = cg::this_grid();
+    draw_seg_body<W>(offsets, targets, frontier, d_n, cap, f, d_seed, layer, counts, slots, minpos, tag_ctr, nullptr,
+                     s_last);
+    grid.sync();
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+        markscan_tile(t, frontier, d_n, cap, f, counts, slots, minpos, tag_ctr, rank, src_vertices, d_n_src, status,
+                      d_gen, outdeg);
+    grid.sync();
+    relabel_seg_body<W>(frontier, d_n, cap, f, counts, slots, slot_local, minpos, nself, outdeg, tag_ctr, d_gen);
 }
 
 __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* d_n, int cap, int f,
@@ -578,6 +646,79 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
                                                                     flags, nself, outdeg, tag_ctr, d_gen);
     }
     return hg_check_launch("dedup_relabel");
+}
+
+// Draw + dedup + relabel of one layer (hg_sample_layer followed by
+// hg_dedup_relabel).  Small blocks (fanout <= 32, cap_dst <= 16384: the upper
+// layers) run as ONE cooperative kernel (k_block_coop); larger ones as the
+// three-kernel sequence.  Same outputs either way.
+namespace {
+template <int W>
+int launch_block_coop(cudaStream_t s, const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                      const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed, int32_t layer,
+                      int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos, int32_t* tag_ctr,
+                      int32_t* src_vertices, int32_t* d_n_src, int32_t* nself, int32_t* outdeg, int32_t* ws) {
+    static int max_ctas = -1;
+    if (max_ctas < 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_coop<W>, 256, 0);
+        max_ctas = per_sm * HG_NUM_SMS;
+    }
+    const long long P = (long long)cap_dst * (fanout + 1);
+    const int tiles = (int)((P + MS_TILE - 1) / MS_TILE);
+    int grid = hg_grid((long long)cap_dst * W, 256, 8);
+    grid = grid > tiles ? grid : tiles;
+    grid = grid < max_ctas ? grid : max_ctas;
+    int* rank = ws;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + ((P + 1) & ~1LL));
+    int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeCooperative;
+    a[0].val.cooperative = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_block_coop<W>, offsets, targets, frontier, d_n_dst, cap_dst,
+                                             fanout, d_seed, layer, counts, slots, slot_local,
+                                             (unsigned long long*)minpos, tag_ctr, src_vertices, d_n_src, nself,
+                                             outdeg, rank, status, d_gen, tiles);
+    if (e != cudaSuccess) {
+        hg_set_error("sample_block: cooperative launch failed: %s", cudaGetErrorString(e));
+        return HG_ECUDA;
+    }
+    return HG_OK;
+}
+int g_block_coop = 0;  // hg_set_tuning key 8 (measured slower than the kernel sequence: grid syncs cost more than PDL launch gaps)
+}  // namespace
+
+void hg_set_block_coop(int v) { g_block_coop = v ? 1 : 0; }
+
+extern "C" int hg_sample_block(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                               const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                               int32_t layer, int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
+                               int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src,
+                               int32_t* nself, int32_t* outdeg, int32_t* ws, int32_t* scratch, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fanout < 1 || cap_dst < 0) { hg_set_error("sample_block: bad fanout/cap"); return HG_EINVAL; }
+    if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("sample_block(empty)"); }
+    if (g_block_coop && fanout <= 32 && cap_dst <= 16384) {
+        int rc;
+        switch (seg_width(fanout)) {
+            case 4: rc = launch_block_coop<4>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
+            case 8: rc = launch_block_coop<8>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
+            case 16: rc = launch_block_coop<16>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
+            default: rc = launch_block_coop<32>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
+        }
+        return rc ? rc : hg_check_launch("sample_block");
+    }
+    int rc = sample_layer_impl(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots,
+                               minpos, tag_ctr, scratch, nullptr, s);
+    if (rc) return rc;
+    return hg_dedup_relabel(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, tag_ctr,
+                            src_vertices, d_n_src, cap_src, nself, outdeg, ws, stream);
 }
 
 // Compacted Block edges; starts: cap_dst ints workspace (+ scan ws after it).

@@ -170,12 +170,11 @@ class LayerSampler:
                       self.f, ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.nself),
                       ptr(self.scratch), s)
             return self
-        _lib.call("hg_sample_layer", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
-                  ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos.table),
-                  ptr(self.minpos.tag), ptr(self.scratch), s)
-        _lib.call("hg_dedup_relabel", ptr(frontier), ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slots),
-                  ptr(self.slot_local), ptr(self.minpos.table), ptr(self.minpos.tag), ptr(self.src), ptr(self.n_src), cap_src, ptr(self.nself),
-                  ptr(self.outdeg), ptr(self.ws), s)
+        # draw + dedup + relabel (one cooperative kernel for small blocks)
+        _lib.call("hg_sample_block", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
+                  ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.slot_local),
+                  ptr(self.minpos.table), ptr(self.minpos.tag), ptr(self.src), ptr(self.n_src), cap_src,
+                  ptr(self.nself), ptr(self.outdeg), ptr(self.ws), ptr(self.scratch), s)
         if self.need_csc and with_csc:
             self.build_csc(d_n_dst, stream, cap)
         return self
