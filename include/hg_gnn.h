@@ -167,6 +167,27 @@ int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_t ld_dagg, 
                              const int32_t* d_n_src, int32_t cap_src, const float* hmask, int32_t ld_hmask,
                              const uint8_t* inj_mask, int64_t* acc_ws, float* dx, int32_t ld_dx, int32_t* d_flags,
                              void* stream);
+/* Top SAGE layer fused (K = d_in <= 64, C = classes <= 64, fanout <= 32): mean of the
+ * non-self neighbours (local ids into hin) -> logits = [h_self | mean] [W_self; W_neigh]
+ * (W: the layer's flat [2K x C] weights) -> softmax-CE (loss into *d_loss, dlogits)
+ * -> dself = dlogits W_self^T (into dself_out) -> dmean = dlogits W_neigh^T scattered
+ * into the layer below exactly like hg_aggregate_bwd_scatter's scatter pass (fast path
+ * into dx, else the fixed-point acc_ws of row stride F_acc); follow with
+ * hg_aggregate_bwd_finish.  row_ws: cap + 1 floats as hg_softmax_xent's. */
+int hg_sage_top_fused(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier, const int32_t* d_n,
+                      int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                      const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg, const float* W,
+                      int32_t C, const int32_t* labels, const int32_t* seeds, const int32_t* d_div, float* logits,
+                      int32_t ld_c, float* dlogits, float* agg_out, int32_t ld_agg, float* dself_out,
+                      int32_t ld_dself, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
+                      int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx, int32_t* d_flags, float* row_ws,
+                      float* d_loss, void* stream);
+/* the finish pass of hg_aggregate_bwd_scatter alone (convert the fixed-point sums, add
+ * dself for s < n_dst, ReLU' / injected-row masks, clear the accumulator) */
+int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int32_t F, const int32_t* d_n_dst, int32_t cap_dst,
+                            const int32_t* d_n_src, int32_t cap_src, const int32_t* outdeg, const float* hmask,
+                            int32_t ld_hmask, const uint8_t* inj_mask, int64_t* acc_ws, float* dx, int32_t ld_dx,
+                            void* stream);
 /* per sorted transposed edge: (dst, weight), dst = -1 for empty slots / SAGE self edges;
  * optional input of hg_aggregate_bwd (csc_dst/csc_w NULL => derived on the fly) */
 int hg_csc_weights(int32_t model, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,

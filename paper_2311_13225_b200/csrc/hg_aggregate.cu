@@ -733,3 +733,233 @@ extern "C" int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_
     if (rc) { hg_set_error("aggregate_bwd_scatter: unsupported width"); return rc; }
     return hg_check_launch("aggregate_bwd_scatter");
 }
+
+// ---------------------------------------------------------------------------
+// Top SAGE layer in ONE kernel (the chain agg -> transform -> softmax-CE ->
+// dX -> transposed scatter of the top layer, gnnmath.py:157-200 +
+// 263-274, one warp per seed row): each warp gathers the mean of its
+// destination's non-self neighbours (local ids) and its self row, computes the
+// logits against [W_self; W_neigh] held in shared memory (fp32 FMA, k order),
+// the softmax / loss / dlogits, then dself = dlogits W_self^T and
+// dmean = dlogits W_neigh^T, and scatters w * dmean into the layer below
+// (single-contribution fast path / fixed-point accumulator, as k_bwd_scatter).
+// Outputs: mean rows and dlogits (for the weight gradients), dself rows (for the
+// finish pass), logits, per-row losses with a last-block fixed-order mean.
+// Replaces five dependent launches on the training critical path.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int TOP_THREADS = 256;
+
+__global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
+    const float* __restrict__ hin, int ld_in, int K, const int* __restrict__ frontier, const int* d_n, int cap, int f,
+    const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
+    const int* __restrict__ nself, const int* __restrict__ outdeg, const float* __restrict__ W, int C,
+    const int* __restrict__ labels, const int* __restrict__ seeds, const int* __restrict__ d_div,
+    float* __restrict__ logits, int ld_c, float* __restrict__ dlogits, float* __restrict__ agg_out, int ld_agg,
+    float* __restrict__ dself_out, int ld_dself, const float* __restrict__ hmask, int ld_hmask,
+    const uint8_t* __restrict__ inj, unsigned long long* __restrict__ acc, int F_acc, float* __restrict__ dx,
+    int ld_dx, int* __restrict__ d_flags, float* __restrict__ row_loss, float* __restrict__ d_loss) {
+    hg_pdl_begin();
+    extern __shared__ float sW[];  // [2K][C]: W_self rows then W_neigh rows
+    __shared__ double s_part[TOP_THREADS / 32];
+    __shared__ bool s_last;
+    for (int e = threadIdx.x; e < 2 * K * C; e += TOP_THREADS) sW[e] = W[e];
+    __syncthreads();
+    const int n = hg_load_count(d_n, cap);
+    const float grad_scale = 1.0f / (float)(d_div ? *d_div : (n > 0 ? n : 1));
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * TOP_THREADS) >> 5;
+    const float* Ws = sW;
+    const float* Wn = sW + K * C;
+    bool bad = false;
+    for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
+        const int cnt = counts[i];
+        const int v = frontier[i];
+        const int ns = nself[i];
+        const float wd = ns > 0 ? 1.0f / (float)ns : 0.f;
+        const int64_t sb = (int64_t)i * f;
+        // ---- self row (local id i) and the mean of the non-self neighbours, edge order
+        const int k0 = lane, k1 = lane + 32;
+        const float s0 = k0 < K ? hin[(int64_t)i * ld_in + k0] : 0.f;
+        const float s1 = k1 < K ? hin[(int64_t)i * ld_in + k1] : 0.f;
+        // lane j < cnt holds edge j: local source (-1 for the self edge) and its out-degree
+        int my_s = -1, my_od = 0;
+        if (lane < cnt) {
+            my_s = slot_local[sb + lane];
+            if (slot_g[sb + lane] == v) my_s = -1;  // SAGE drops self edges (gnnmath.py:148)
+            else my_od = outdeg[my_s];
+        }
+        float m0 = 0.f, m1 = 0.f;
+        for (int j0 = 0; j0 < cnt; j0 += 8) {  // 8 neighbour rows in flight, summed in edge order
+            float x0[8], x1[8];
+            int sj[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                sj[u] = __shfl_sync(0xffffffffu, my_s, (j0 + u) & 31);
+                if (j0 + u >= cnt) sj[u] = -1;
+                x0[u] = (sj[u] >= 0 && k0 < K) ? hin[(int64_t)sj[u] * ld_in + k0] : 0.f;
+                x1[u] = (sj[u] >= 0 && k1 < K) ? hin[(int64_t)sj[u] * ld_in + k1] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (sj[u] >= 0) { m0 = fmaf(wd, x0[u], m0); m1 = fmaf(wd, x1[u], m1); }
+        }
+        if (k0 < K) agg_out[(int64_t)i * ld_agg + k0] = m0;
+        if (k1 < K) agg_out[(int64_t)i * ld_agg + k1] = m1;
+        // ---- logits: z[c] = sum_k self[k] W_self[k][c] + sum_k mean[k] W_neigh[k][c]
+        const int c0 = lane, c1 = lane + 32;
+        float z0 = 0.f, z1 = 0.f;
+        const int cc0 = c0 < C ? c0 : 0, cc1 = c1 < C ? c1 : 0;  // clamped smem columns (results masked)
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) {
+            const float a = __shfl_sync(0xffffffffu, k < 32 ? s0 : s1, k & 31);
+            z0 = fmaf(a, Ws[k * C + cc0], z0);
+            z1 = fmaf(a, Ws[k * C + cc1], z1);
+        }
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) {
+            const float b = __shfl_sync(0xffffffffu, k < 32 ? m0 : m1, k & 31);
+            z0 = fmaf(b, Wn[k * C + cc0], z0);
+            z1 = fmaf(b, Wn[k * C + cc1], z1);
+        }
+        if (c0 < C) logits[(int64_t)i * ld_c + c0] = z0;
+        if (c1 < C) logits[(int64_t)i * ld_c + c1] = z1;
+        // ---- softmax cross-entropy (gnnmath.py:263-274)
+        float mx = fmaxf(c0 < C ? z0 : -INFINITY, c1 < C ? z1 : -INFINITY);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float e0 = c0 < C ? expf(z0 - mx) : 0.f, e1 = c1 < C ? expf(z1 - mx) : 0.f;
+        float se = e0 + e1;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const int y = labels[seeds ? seeds[i] : i];
+        const float zy = __shfl_sync(0xffffffffu, y < 32 ? z0 : z1, y & 31);
+        const float inv = 1.f / se;
+        const float d0 = c0 < C ? (e0 * inv - (c0 == y ? 1.f : 0.f)) * grad_scale : 0.f;
+        const float d1 = c1 < C ? (e1 * inv - (c1 == y ? 1.f : 0.f)) * grad_scale : 0.f;
+        if (c0 < C) dlogits[(int64_t)i * ld_c + c0] = d0;
+        if (c1 < C) dlogits[(int64_t)i * ld_c + c1] = d1;
+        if (lane == 0) row_loss[i] = logf(se) - (zy - mx);
+        // ---- dself = dlogits W_self^T, dmean = dlogits W_neigh^T (lane owns k0, k1)
+        float ds0 = 0.f, ds1 = 0.f, dm0 = 0.f, dm1 = 0.f;
+        const int kk0 = k0 < K ? k0 : 0, kk1 = k1 < K ? k1 : 0;
+#pragma unroll 8
+        for (int c = 0; c < C; ++c) {
+            const float dl = __shfl_sync(0xffffffffu, c < 32 ? d0 : d1, c & 31);
+            ds0 = fmaf(dl, Ws[kk0 * C + c], ds0);
+            dm0 = fmaf(dl, Wn[kk0 * C + c], dm0);
+            ds1 = fmaf(dl, Ws[kk1 * C + c], ds1);
+            dm1 = fmaf(dl, Wn[kk1 * C + c], dm1);
+        }
+        if (k0 < K) dself_out[(int64_t)i * ld_dself + k0] = ds0;
+        if (k1 < K) dself_out[(int64_t)i * ld_dself + k1] = ds1;
+        // ---- transposed scatter of w * dmean into the layer below (as k_bwd_scatter)
+        const float a0 = wd * dm0, a1 = wd * dm1;
+        if (cnt > 0 && !(fabsf(a0) < FX_GUARD && fabsf(a1) < FX_GUARD)) bad = true;
+        for (int j0 = 0; j0 < cnt; j0 += 8) {  // 8 edges at a time: their masks load together
+            int sj[8], od[8];
+            float h0[8], h1[8];
+            bool zr[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                sj[u] = __shfl_sync(0xffffffffu, my_s, (j0 + u) & 31);
+                od[u] = __shfl_sync(0xffffffffu, my_od, (j0 + u) & 31);
+                if (j0 + u >= cnt) sj[u] = -1;
+                const bool fast = sj[u] >= n && od[u] == 1;
+                h0[u] = (fast && hmask && k0 < K) ? hmask[(int64_t)sj[u] * ld_hmask + k0] : 1.f;
+                h1[u] = (fast && hmask && k1 < K) ? hmask[(int64_t)sj[u] * ld_hmask + k1] : 1.f;
+                zr[u] = fast && inj && inj[sj[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int sv = sj[u];
+                if (sv < 0) continue;
+                if (sv >= n && od[u] == 1) {  // single contribution: final masked row
+                    if (k0 < K) dx[(int64_t)sv * ld_dx + k0] = (zr[u] || !(h0[u] > 0.f)) ? 0.f : a0;
+                    if (k1 < K) dx[(int64_t)sv * ld_dx + k1] = (zr[u] || !(h1[u] > 0.f)) ? 0.f : a1;
+                } else {
+                    unsigned long long* row = acc + (int64_t)sv * F_acc;
+                    bool b2 = false;
+                    if (k0 < K) fx_add(row + k0, a0, b2);
+                    if (k1 < K) fx_add(row + k1, a1, b2);
+                }
+            }
+        }
+    }
+    if (bad && d_flags) atomicOr(d_flags, 1);
+    // ---- last block: fixed-order mean of the row losses (ticket in row_loss[cap])
+    unsigned* ticket = reinterpret_cast<unsigned*>(row_loss + cap);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double part = 0.0;
+    for (int r = threadIdx.x; r < n; r += TOP_THREADS) part += (double)__ldcg(row_loss + r);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) s_part[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int k = 0; k < TOP_THREADS / 32; ++k) tot += s_part[k];
+        *d_loss = n > 0 ? (float)(tot / (double)n) : 0.f;
+        *ticket = 0u;
+    }
+}
+}  // namespace
+
+extern "C" int hg_sage_top_fused(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier,
+                                 const int32_t* d_n, int32_t cap, int32_t fanout, const int32_t* counts,
+                                 const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself,
+                                 const int32_t* outdeg, const float* W, int32_t C, const int32_t* labels,
+                                 const int32_t* seeds, const int32_t* d_div, float* logits, int32_t ld_c,
+                                 float* dlogits, float* agg_out, int32_t ld_agg, float* dself_out, int32_t ld_dself,
+                                 const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask, int64_t* acc_ws,
+                                 int32_t F_acc, float* dx, int32_t ld_dx, int32_t* d_flags, float* row_ws,
+                                 float* d_loss, void* stream) {
+    if (K < 1 || K > 64 || C < 1 || C > 64) {
+        hg_set_error("sage_top_fused: needs K, C in [1, 64] (got %d, %d)", K, C);
+        return HG_EUNSUPPORTED;
+    }
+    if (cap <= 0) { hg_set_error("sage_top_fused: empty batch"); return HG_EINVAL; }
+    if (fanout > 32) { hg_set_error("sage_top_fused: fanout > 32"); return HG_EUNSUPPORTED; }
+    int grid = hg_ceil_div(cap, TOP_THREADS / 32);
+    grid = grid < 2 * HG_NUM_SMS ? grid : 2 * HG_NUM_SMS;
+    const int smem = 2 * K * C * 4;
+    hg_launch(k_sage_top, dim3(grid), dim3(TOP_THREADS), (size_t)smem, (cudaStream_t)stream, hin, ld_in, K, frontier,
+              d_n, cap, fanout, counts, slot_g, slot_local, nself, outdeg, W, C, labels, seeds, d_div, logits, ld_c,
+              dlogits, agg_out, ld_agg, dself_out, ld_dself, hmask, ld_hmask, inj_mask,
+              reinterpret_cast<unsigned long long*>(acc_ws), F_acc, dx, ld_dx, d_flags, row_ws, d_loss);
+    return hg_check_launch("sage_top_fused");
+}
+
+// finish pass of hg_aggregate_bwd_scatter alone (after a fused scatter)
+extern "C" int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int32_t F, const int32_t* d_n_dst,
+                                       int32_t cap_dst, const int32_t* d_n_src, int32_t cap_src,
+                                       const int32_t* outdeg, const float* hmask, int32_t ld_hmask,
+                                       const uint8_t* inj_mask, int64_t* acc_ws, float* dx, int32_t ld_dx,
+                                       void* stream) {
+    if (F % 4 || ld_dx % 4 || (dself && ld_dself % 4) || (hmask && ld_hmask % 4)) {
+        hg_set_error("aggregate_bwd_finish: widths must be multiples of 4");
+        return HG_EINVAL;
+    }
+    if (cap_src == 0) return HG_OK;
+    const int F4 = F / 4;
+    int LPR, NV;
+    pick_lanes(F4, LPR, NV);
+    dim3 g2(hg_grid((long long)cap_src * LPR, 256, 8));
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(acc_ws);
+#define HG_FIN(L, V)                                                                                              \
+    if (LPR == L && NV == V) {                                                                                    \
+        hg_launch(k_bwd_finish<L, V>, g2, dim3(256), 0, s, acc, F4, dself, ld_dself, d_n_dst, cap_dst, d_n_src,     \
+                  cap_src, outdeg, hmask, ld_hmask, inj_mask, dx, ld_dx);                                         \
+        return hg_check_launch("aggregate_bwd_finish");                                                          \
+    }
+    HG_FIN(8, 1) HG_FIN(16, 1) HG_FIN(32, 1) HG_FIN(32, 2) HG_FIN(32, 4) HG_FIN(32, 8)
+#undef HG_FIN
+    hg_set_error("aggregate_bwd_finish: unsupported width");
+    return HG_EUNSUPPORTED;
+}

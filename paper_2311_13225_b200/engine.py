@@ -258,6 +258,10 @@ class TrainEngine:
             else:
                 nm = 2 if self.sage else 1
                 self.img_dx.append([dense.BImage(self.dims[l + 1], 0, self.dims[l], 0, dev) for _ in range(nm)])
+        # the top SAGE layer's aggregate -> transform -> loss -> dX -> scatter in one kernel
+        self.top_fused = (self.sage and self.L >= 2 and self.bwd_scatter and self.dims[self.L - 1] <= 64
+                          and self.dims[self.L] <= 64 and self.fan[self.L - 1] <= 32
+                          and self.fused_dx[self.L - 1] and os.environ.get("HG_TOP_FUSED", "1") != "0")
         self.graph = None
         self.g_sample = None
         self.g_train = None
@@ -381,6 +385,8 @@ class TrainEngine:
         model = 0 if self.sage else 1
         # ---------------- forward ----------------
         for l in range(L):
+            if l == L - 1 and self.top_fused:
+                break  # folded into the fused top-layer kernel below
             smp = self.samplers[l]
             fr, n = self.frontier(l)
             d_in, d_out = self.dims[l], self.dims[l + 1]
@@ -413,9 +419,22 @@ class TrainEngine:
         # ---------------- loss ----------------
         mark("loss")
         C = self.dims[L]
-        _lib.call("hg_softmax_xent", ptr(self.out[L - 1]), self.ld[L], C, ptr(self.counts_in[0:1]), self.batch_cap,
-                  ptr(g.labels), ptr(self.seeds), ptr(self.counts_in[1:2]), ptr(self.dz[L - 1]), self.ld[L],
-                  ptr(self.d_loss), ptr(self.row_loss), s)
+        if self.top_fused:
+            l = L - 1
+            smp = self.samplers[l]
+            fr, n = self.frontier(l)
+            d_in = self.dims[l]
+            _lib.call("hg_sage_top_fused", ptr(self.out[l - 1]), self.ld[l], d_in, ptr(fr), ptr(n), self.cap_dst[l],
+                      self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local), ptr(smp.nself),
+                      ptr(smp.outdeg), ptr(P.view(l, 0)), C, ptr(g.labels), ptr(self.seeds),
+                      ptr(self.counts_in[1:2]), ptr(self.out[l]), self.ld[L], ptr(self.dz[l]), ptr(self.agg[l]),
+                      self.ld[l], ptr(self.dcat[l]), 2 * d_in, ptr(self.out[l - 1]), self.ld[l],
+                      ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), self.ld[l], ptr(self.dz[l - 1]),
+                      self.ld[l], ptr(self.fx_flags), ptr(self.row_loss), ptr(self.d_loss), s)
+        else:
+            _lib.call("hg_softmax_xent", ptr(self.out[L - 1]), self.ld[L], C, ptr(self.counts_in[0:1]),
+                      self.batch_cap, ptr(g.labels), ptr(self.seeds), ptr(self.counts_in[1:2]), ptr(self.dz[L - 1]),
+                      self.ld[L], ptr(self.d_loss), ptr(self.row_loss), s)
         # ---------------- backward ----------------
         mark("bwd")
         # weight gradients of layer l only need dz[l]: they run on a side stream (a
@@ -438,6 +457,12 @@ class TrainEngine:
                 dense.wgrad(ptr(agg_l), self.ld[l], None, 0, d_in, ptr(self.dz[l]), self.ld[l + 1], d_out,
                             ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), ws_)
             if l == 0:
+                continue
+            if l == L - 1 and self.top_fused:  # dX and the scatter ran in the fused top kernel
+                _lib.call("hg_aggregate_bwd_finish", ptr(self.dcat[l]), 2 * self.dims[l], self.ld[l], ptr(n),
+                          self.cap_dst[l], ptr(smp.n_src), self.cap_src[l], ptr(smp.outdeg), ptr(self.out[l - 1]),
+                          self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), ptr(self.dz[l - 1]),
+                          self.ld[l], s)
                 continue
             if self.fused_dx[l]:  # [dself | dmean] = dz [W_self; W_neigh]^T in one GEMM
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), 2 * d_in, ptr(self.dcat[l]),
