@@ -182,6 +182,20 @@ int hg_sage_top_fused(const float* hin, int32_t ld_in, int32_t K, const int32_t*
                       int32_t ld_dself, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
                       int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx, int32_t* d_flags, float* row_ws,
                       float* d_loss, void* stream);
+/* Middle SAGE layers (d_in, d_out <= 64, fanout <= 32), warp per destination, W = the
+ * layer's flat [2K x N] weights: forward = mean of non-self neighbours (into agg_out) +
+ * act([h_self | mean] W) (into out); backward = dself (into dself_out) and the
+ * transposed scatter of w * (dz W_neigh^T) as hg_aggregate_bwd_scatter's scatter pass,
+ * followed by hg_aggregate_bwd_finish. */
+int hg_sage_mid_fwd(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier, const int32_t* d_n,
+                    int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                    const int32_t* slot_local, const int32_t* nself, const float* W, int32_t N, int32_t act,
+                    float* out, int32_t ld_out, float* agg_out, int32_t ld_agg, void* stream);
+int hg_sage_mid_bwd(const float* dz, int32_t ld_dz, int32_t N, const int32_t* frontier, const int32_t* d_n,
+                    int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                    const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg, const float* W, int32_t K,
+                    float* dself_out, int32_t ld_dself, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
+                    int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx, int32_t* d_flags, void* stream);
 /* the finish pass of hg_aggregate_bwd_scatter alone (convert the fixed-point sums, add
  * dself for s < n_dst, ReLU' / injected-row masks, clear the accumulator) */
 int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int32_t F, const int32_t* d_n_dst, int32_t cap_dst,

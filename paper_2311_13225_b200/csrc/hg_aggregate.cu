@@ -750,6 +750,26 @@ extern "C" int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_
 namespace {
 constexpr int TOP_THREADS = 256;
 
+// W [rows x N] (row-major, global) -> shared memory with row stride NS, 8 loads
+// in flight per thread (a CTA-wide staging that otherwise costs one L2 round trip
+// per element slot)
+__device__ __forceinline__ void stage_w(float* sW, const float* __restrict__ W, int rows, int N, int NS) {
+    const int total = rows * N;
+    for (int e0 = threadIdx.x; e0 < total; e0 += 8 * TOP_THREADS) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * TOP_THREADS;
+            v[u] = e < total ? __ldg(W + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * TOP_THREADS;
+            if (e < total) sW[(e / N) * NS + e % N] = v[u];
+        }
+    }
+}
+
 __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
     const float* __restrict__ hin, int ld_in, int K, const int* __restrict__ frontier, const int* d_n, int cap, int f,
     const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
@@ -763,14 +783,15 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
     extern __shared__ float sW[];  // [2K][C]: W_self rows then W_neigh rows
     __shared__ double s_part[TOP_THREADS / 32];
     __shared__ bool s_last;
-    for (int e = threadIdx.x; e < 2 * K * C; e += TOP_THREADS) sW[e] = W[e];
+    const int CS = C | 1;  // odd row stride: conflict-free column walks in the dX loop
+    stage_w(sW, W, 2 * K, C, CS);
     __syncthreads();
     const int n = hg_load_count(d_n, cap);
     const float grad_scale = 1.0f / (float)(d_div ? *d_div : (n > 0 ? n : 1));
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * TOP_THREADS) >> 5;
     const float* Ws = sW;
-    const float* Wn = sW + K * C;
+    const float* Wn = sW + K * CS;
     bool bad = false;
     for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
         const int cnt = counts[i];
@@ -813,14 +834,14 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
 #pragma unroll 8
         for (int k = 0; k < K; ++k) {
             const float a = __shfl_sync(0xffffffffu, k < 32 ? s0 : s1, k & 31);
-            z0 = fmaf(a, Ws[k * C + cc0], z0);
-            z1 = fmaf(a, Ws[k * C + cc1], z1);
+            z0 = fmaf(a, Ws[k * CS + cc0], z0);
+            z1 = fmaf(a, Ws[k * CS + cc1], z1);
         }
 #pragma unroll 8
         for (int k = 0; k < K; ++k) {
             const float b = __shfl_sync(0xffffffffu, k < 32 ? m0 : m1, k & 31);
-            z0 = fmaf(b, Wn[k * C + cc0], z0);
-            z1 = fmaf(b, Wn[k * C + cc1], z1);
+            z0 = fmaf(b, Wn[k * CS + cc0], z0);
+            z1 = fmaf(b, Wn[k * CS + cc1], z1);
         }
         if (c0 < C) logits[(int64_t)i * ld_c + c0] = z0;
         if (c1 < C) logits[(int64_t)i * ld_c + c1] = z1;
@@ -846,10 +867,10 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
 #pragma unroll 8
         for (int c = 0; c < C; ++c) {
             const float dl = __shfl_sync(0xffffffffu, c < 32 ? d0 : d1, c & 31);
-            ds0 = fmaf(dl, Ws[kk0 * C + c], ds0);
-            dm0 = fmaf(dl, Wn[kk0 * C + c], dm0);
-            ds1 = fmaf(dl, Ws[kk1 * C + c], ds1);
-            dm1 = fmaf(dl, Wn[kk1 * C + c], dm1);
+            ds0 = fmaf(dl, Ws[kk0 * CS + c], ds0);
+            dm0 = fmaf(dl, Wn[kk0 * CS + c], dm0);
+            ds1 = fmaf(dl, Ws[kk1 * CS + c], ds1);
+            dm1 = fmaf(dl, Wn[kk1 * CS + c], dm1);
         }
         if (k0 < K) dself_out[(int64_t)i * ld_dself + k0] = ds0;
         if (k1 < K) dself_out[(int64_t)i * ld_dself + k1] = ds1;
@@ -927,7 +948,7 @@ extern "C" int hg_sage_top_fused(const float* hin, int32_t ld_in, int32_t K, con
     if (fanout > 32) { hg_set_error("sage_top_fused: fanout > 32"); return HG_EUNSUPPORTED; }
     int grid = hg_ceil_div(cap, TOP_THREADS / 32);
     grid = grid < 2 * HG_NUM_SMS ? grid : 2 * HG_NUM_SMS;
-    const int smem = 2 * K * C * 4;
+    const int smem = 2 * K * (C | 1) * 4;
     hg_launch(k_sage_top, dim3(grid), dim3(TOP_THREADS), (size_t)smem, (cudaStream_t)stream, hin, ld_in, K, frontier,
               d_n, cap, fanout, counts, slot_g, slot_local, nself, outdeg, W, C, labels, seeds, d_div, logits, ld_c,
               dlogits, agg_out, ld_agg, dself_out, ld_dself, hmask, ld_hmask, inj_mask,
@@ -962,4 +983,201 @@ extern "C" int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int
 #undef HG_FIN
     hg_set_error("aggregate_bwd_finish: unsupported width");
     return HG_EUNSUPPORTED;
+}
+
+// ---------------------------------------------------------------------------
+// Middle SAGE layers (0 < l < L-1, d_in, d_out <= 64, fanout <= 32), one warp per
+// destination row, W_l = [W_self; W_neigh] in shared memory:
+//   k_sage_mid_fwd: mean of the non-self neighbours + h = ReLU([self | mean] W)
+//                   (gnnmath.py:157-178; replaces aggregate + GEMM launches)
+//   k_sage_mid_bwd: dself = dz W_self^T, dmean = dz W_neigh^T and the transposed
+//                   scatter of w * dmean (gnnmath.py:194-199; replaces dX GEMM +
+//                   scatter), followed by hg_aggregate_bwd_finish.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(TOP_THREADS) k_sage_mid_fwd(
+    const float* __restrict__ hin, int ld_in, int K, const int* __restrict__ frontier, const int* d_n, int cap, int f,
+    const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
+    const int* __restrict__ nself, const float* __restrict__ W, int N, int act, float* __restrict__ out, int ld_out,
+    float* __restrict__ agg_out, int ld_agg) {
+    hg_pdl_begin();
+    extern __shared__ float sW[];
+    // row stride NS = N | 1 (odd): the backward's column walks (fixed c, lane = k) are
+    // then bank-conflict free
+    const int NS = N | 1;
+    stage_w(sW, W, 2 * K, N, NS);
+    __syncthreads();
+    const int n = hg_load_count(d_n, cap);
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * TOP_THREADS) >> 5;
+    const float* Ws = sW;
+    const float* Wn = sW + K * NS;
+    const int k0 = lane, k1 = lane + 32;
+    const int c0 = lane, c1 = lane + 32;
+    const int cc0 = c0 < N ? c0 : 0, cc1 = c1 < N ? c1 : 0;
+    for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
+        const int cnt = counts[i];
+        const int v = frontier[i];
+        const int ns = nself[i];
+        const float wd = ns > 0 ? 1.0f / (float)ns : 0.f;
+        const int64_t sb = (int64_t)i * f;
+        const float s0 = k0 < K ? hin[(int64_t)i * ld_in + k0] : 0.f;
+        const float s1 = k1 < K ? hin[(int64_t)i * ld_in + k1] : 0.f;
+        int my_s = -1;
+        if (lane < cnt) {
+            my_s = slot_local[sb + lane];
+            if (slot_g[sb + lane] == v) my_s = -1;  // SAGE drops self edges (gnnmath.py:148)
+        }
+        float m0 = 0.f, m1 = 0.f;
+        for (int j0 = 0; j0 < cnt; j0 += 8) {
+            float x0[8], x1[8];
+            int sj[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                sj[u] = __shfl_sync(0xffffffffu, my_s, (j0 + u) & 31);
+                if (j0 + u >= cnt) sj[u] = -1;
+                x0[u] = (sj[u] >= 0 && k0 < K) ? hin[(int64_t)sj[u] * ld_in + k0] : 0.f;
+                x1[u] = (sj[u] >= 0 && k1 < K) ? hin[(int64_t)sj[u] * ld_in + k1] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (sj[u] >= 0) { m0 = fmaf(wd, x0[u], m0); m1 = fmaf(wd, x1[u], m1); }
+        }
+        if (k0 < K) agg_out[(int64_t)i * ld_agg + k0] = m0;
+        if (k1 < K) agg_out[(int64_t)i * ld_agg + k1] = m1;
+        float z0 = 0.f, z1 = 0.f;
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) {
+            const float a = __shfl_sync(0xffffffffu, k < 32 ? s0 : s1, k & 31);
+            z0 = fmaf(a, Ws[k * NS + cc0], z0);
+            z1 = fmaf(a, Ws[k * NS + cc1], z1);
+        }
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) {
+            const float b = __shfl_sync(0xffffffffu, k < 32 ? m0 : m1, k & 31);
+            z0 = fmaf(b, Wn[k * NS + cc0], z0);
+            z1 = fmaf(b, Wn[k * NS + cc1], z1);
+        }
+        if (c0 < N) out[(int64_t)i * ld_out + c0] = act ? fmaxf(z0, 0.f) : z0;
+        if (c1 < N) out[(int64_t)i * ld_out + c1] = act ? fmaxf(z1, 0.f) : z1;
+    }
+}
+
+__global__ void __launch_bounds__(TOP_THREADS) k_sage_mid_bwd(
+    const float* __restrict__ dz, int ld_dz, int N, const int* __restrict__ frontier, const int* d_n, int cap, int f,
+    const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
+    const int* __restrict__ nself, const int* __restrict__ outdeg, const float* __restrict__ W, int K,
+    float* __restrict__ dself_out, int ld_dself, const float* __restrict__ hmask, int ld_hmask,
+    const uint8_t* __restrict__ inj, unsigned long long* __restrict__ acc, int F_acc, float* __restrict__ dx,
+    int ld_dx, int* __restrict__ d_flags) {
+    hg_pdl_begin();
+    extern __shared__ float sW[];
+    // row stride NS = N | 1 (odd): the backward's column walks (fixed c, lane = k) are
+    // then bank-conflict free
+    const int NS = N | 1;
+    stage_w(sW, W, 2 * K, N, NS);
+    __syncthreads();
+    const int n = hg_load_count(d_n, cap);
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * TOP_THREADS) >> 5;
+    const float* Ws = sW;
+    const float* Wn = sW + K * NS;
+    const int k0 = lane, k1 = lane + 32;
+    const int kk0 = k0 < K ? k0 : 0, kk1 = k1 < K ? k1 : 0;
+    bool bad = false;
+    for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
+        const int cnt = counts[i];
+        const int v = frontier[i];
+        const int ns = nself[i];
+        const float wd = ns > 0 ? 1.0f / (float)ns : 0.f;
+        const int64_t sb = (int64_t)i * f;
+        int my_s = -1, my_od = 0;
+        if (lane < cnt) {
+            my_s = slot_local[sb + lane];
+            if (slot_g[sb + lane] == v) my_s = -1;
+            else my_od = outdeg[my_s];
+        }
+        const float g0 = lane < N ? dz[(int64_t)i * ld_dz + lane] : 0.f;
+        const float g1 = lane + 32 < N ? dz[(int64_t)i * ld_dz + lane + 32] : 0.f;
+        float ds0 = 0.f, ds1 = 0.f, dm0 = 0.f, dm1 = 0.f;
+#pragma unroll 8
+        for (int c = 0; c < N; ++c) {
+            const float g = __shfl_sync(0xffffffffu, c < 32 ? g0 : g1, c & 31);
+            ds0 = fmaf(g, Ws[kk0 * NS + c], ds0);
+            dm0 = fmaf(g, Wn[kk0 * NS + c], dm0);
+            ds1 = fmaf(g, Ws[kk1 * NS + c], ds1);
+            dm1 = fmaf(g, Wn[kk1 * NS + c], dm1);
+        }
+        if (k0 < K) dself_out[(int64_t)i * ld_dself + k0] = ds0;
+        if (k1 < K) dself_out[(int64_t)i * ld_dself + k1] = ds1;
+        const float a0 = wd * dm0, a1 = wd * dm1;
+        if (cnt > 0 && !(fabsf(a0) < FX_GUARD && fabsf(a1) < FX_GUARD)) bad = true;
+        for (int j0 = 0; j0 < cnt; j0 += 8) {
+            int sj[8], od[8];
+            float h0[8], h1[8];
+            bool zr[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                sj[u] = __shfl_sync(0xffffffffu, my_s, (j0 + u) & 31);
+                od[u] = __shfl_sync(0xffffffffu, my_od, (j0 + u) & 31);
+                if (j0 + u >= cnt) sj[u] = -1;
+                const bool fast = sj[u] >= n && od[u] == 1;
+                h0[u] = (fast && hmask && k0 < K) ? hmask[(int64_t)sj[u] * ld_hmask + k0] : 1.f;
+                h1[u] = (fast && hmask && k1 < K) ? hmask[(int64_t)sj[u] * ld_hmask + k1] : 1.f;
+                zr[u] = fast && inj && inj[sj[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int sv = sj[u];
+                if (sv < 0) continue;
+                if (sv >= n && od[u] == 1) {
+                    if (k0 < K) dx[(int64_t)sv * ld_dx + k0] = (zr[u] || !(h0[u] > 0.f)) ? 0.f : a0;
+                    if (k1 < K) dx[(int64_t)sv * ld_dx + k1] = (zr[u] || !(h1[u] > 0.f)) ? 0.f : a1;
+                } else {
+                    unsigned long long* row = acc + (int64_t)sv * F_acc;
+                    bool b2 = false;
+                    if (k0 < K) fx_add(row + k0, a0, b2);
+                    if (k1 < K) fx_add(row + k1, a1, b2);
+                }
+            }
+        }
+    }
+    if (bad && d_flags) atomicOr(d_flags, 1);
+}
+}  // namespace
+
+extern "C" int hg_sage_mid_fwd(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier,
+                               const int32_t* d_n, int32_t cap, int32_t fanout, const int32_t* counts,
+                               const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself, const float* W,
+                               int32_t N, int32_t act, float* out, int32_t ld_out, float* agg_out, int32_t ld_agg,
+                               void* stream) {
+    if (K < 1 || K > 64 || N < 1 || N > 64 || fanout > 32) {
+        hg_set_error("sage_mid_fwd: needs d_in, d_out in [1, 64] and fanout <= 32");
+        return HG_EUNSUPPORTED;
+    }
+    if (cap <= 0) return HG_OK;
+    int grid = hg_ceil_div(cap, TOP_THREADS / 32);
+    grid = grid < 4 * HG_NUM_SMS ? grid : 4 * HG_NUM_SMS;
+    hg_launch(k_sage_mid_fwd, dim3(grid), dim3(TOP_THREADS), (size_t)(2 * K * (N | 1) * 4), (cudaStream_t)stream, hin, ld_in,
+              K, frontier, d_n, cap, fanout, counts, slot_g, slot_local, nself, W, N, act, out, ld_out, agg_out, ld_agg);
+    return hg_check_launch("sage_mid_fwd");
+}
+
+extern "C" int hg_sage_mid_bwd(const float* dz, int32_t ld_dz, int32_t N, const int32_t* frontier, const int32_t* d_n,
+                               int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
+                               const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg, const float* W,
+                               int32_t K, float* dself_out, int32_t ld_dself, const float* hmask, int32_t ld_hmask,
+                               const uint8_t* inj_mask, int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx,
+                               int32_t* d_flags, void* stream) {
+    if (K < 1 || K > 64 || N < 1 || N > 64 || fanout > 32) {
+        hg_set_error("sage_mid_bwd: needs d_in, d_out in [1, 64] and fanout <= 32");
+        return HG_EUNSUPPORTED;
+    }
+    if (cap <= 0) return HG_OK;
+    int grid = hg_ceil_div(cap, TOP_THREADS / 32);
+    grid = grid < 4 * HG_NUM_SMS ? grid : 4 * HG_NUM_SMS;
+    hg_launch(k_sage_mid_bwd, dim3(grid), dim3(TOP_THREADS), (size_t)(2 * K * (N | 1) * 4), (cudaStream_t)stream, dz, ld_dz,
+              N, frontier, d_n, cap, fanout, counts, slot_g, slot_local, nself, outdeg, W, K, dself_out, ld_dself,
+              hmask, ld_hmask, inj_mask, reinterpret_cast<unsigned long long*>(acc_ws), F_acc, dx, ld_dx, d_flags);
+    return hg_check_launch("sage_mid_bwd");
 }

@@ -262,6 +262,12 @@ class TrainEngine:
         self.top_fused = (self.sage and self.L >= 2 and self.bwd_scatter and self.dims[self.L - 1] <= 64
                           and self.dims[self.L] <= 64 and self.fan[self.L - 1] <= 32
                           and self.fused_dx[self.L - 1] and os.environ.get("HG_TOP_FUSED", "1") != "0")
+        # middle SAGE layers: aggregate + transform, and dX + scatter, as one kernel each
+        # (off by default: measured slower than aggregate + TMA GEMM at ~6K rows — a warp-per-row
+        # SIMT transform cannot keep enough rows in flight per SM; HG_MID_FUSED=1 enables it)
+        mid_ok = os.environ.get("HG_MID_FUSED", "0") == "1" and self.sage and self.bwd_scatter
+        self.mid_fused = [mid_ok and 0 < l < self.L - 1 and self.dims[l] <= 64 and self.dims[l + 1] <= 64
+                          and self.fan[l] <= 32 and self.fused_dx[l] for l in range(self.L)]
         self.graph = None
         self.g_sample = None
         self.g_train = None
@@ -397,6 +403,11 @@ class TrainEngine:
             mark("fwd0_agg" if l == 0 else "fwd_upper" if l == 1 else "")
             sb0, ag0 = self._bottom_bufs()
             agg_l = ag0 if l == 0 else self.agg[l]
+            if self.mid_fused[l]:  # aggregate + transform + ReLU in one kernel
+                _lib.call("hg_sage_mid_fwd", ptr(hin), ld_in, d_in, ptr(fr), ptr(n), self.cap_dst[l], self.fan[l],
+                          ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local), ptr(smp.nself), ptr(P.view(l, 0)),
+                          d_out, 1 if l < L - 1 else 0, ptr(self.out[l]), self.ld[l + 1], ptr(agg_l), self.ld[l], s)
+                continue
             if l == 0:
                 if not self.early_agg0():
                     self._enqueue_agg0(s, inj)
@@ -458,7 +469,13 @@ class TrainEngine:
                             ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), ws_)
             if l == 0:
                 continue
-            if l == L - 1 and self.top_fused:  # dX and the scatter ran in the fused top kernel
+            if self.mid_fused[l]:  # dself + scatter of dmean in one kernel, then the finish pass
+                _lib.call("hg_sage_mid_bwd", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(fr), ptr(n), self.cap_dst[l],
+                          self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local), ptr(smp.nself),
+                          ptr(smp.outdeg), ptr(P.view(l, 0)), d_in, ptr(self.dcat[l]), 2 * d_in, ptr(self.out[l - 1]),
+                          self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), self.ld[l],
+                          ptr(self.dz[l - 1]), self.ld[l], ptr(self.fx_flags), s)
+            if (l == L - 1 and self.top_fused) or self.mid_fused[l]:  # dX + scatter already ran
                 _lib.call("hg_aggregate_bwd_finish", ptr(self.dcat[l]), 2 * self.dims[l], self.ld[l], ptr(n),
                           self.cap_dst[l], ptr(smp.n_src), self.cap_src[l], ptr(smp.outdeg), ptr(self.out[l - 1]),
                           self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), ptr(self.dz[l - 1]),

@@ -182,22 +182,25 @@ def test_training_edge_shapes_vs_oracle(model, fan, opt):
     np.testing.assert_allclose(reps[0].losses, ref[0]["losses"], rtol=2e-3)
 
 
-@pytest.mark.parametrize("layers,hot", [(2, 0.3), (3, 0.2), (2, 0.0)])
+@pytest.mark.parametrize("layers,hot", [(2, 0.3), (3, 0.2), (2, 0.0), (4, 0.2)])
 def test_top_fused_matches_unfused(monkeypatch, layers, hot):
     """The fused top SAGE layer kernel (aggregate -> transform -> softmax-CE -> dX ->
-    scatter in one launch, HG_TOP_FUSED) reproduces the unfused kernel chain to
+    scatter in one launch, HG_TOP_FUSED) and the fused middle layers
+    (HG_MID_FUSED) reproduce the unfused kernel chain to
     fp32 rounding over a whole run, incl. hot-embedding injection below a 2-layer
     top (the scatter then writes the injected-row-masked bottom gradient)."""
     from paper_2311_13225_b200.datagen import make_dataset
     from paper_2311_13225_b200.orchestrator import TrainConfig, run_training
     ds = make_dataset("tiny")
-    fan = (5, 4, 3)[:layers]
+    fan = (5, 4, 3, 2)[:layers]
     kw = dict(model="sage", layers=layers, fanouts=fan, hidden_dim=32, batch_size=96, epochs=2, lr=0.05, seed=11,
               super_batch_n=2, hot_ratio=hot, presample_rounds=1,
               strategy="layer-based" if hot > 0 else "case1")
     monkeypatch.setenv("HG_TOP_FUSED", "0")
+    monkeypatch.setenv("HG_MID_FUSED", "0")
     a = run_training(ds, None, TrainConfig(**kw))
     monkeypatch.setenv("HG_TOP_FUSED", "1")
+    monkeypatch.setenv("HG_MID_FUSED", "1")
     b = run_training(ds, None, TrainConfig(**kw))
     for ra, rb in zip(a, b):
         np.testing.assert_allclose(ra.losses, rb.losses, rtol=1e-5)
