@@ -520,9 +520,10 @@ def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):
     marks = tuple(m for m in e.MARKS if e.hot is not None or m != "fwd0_agg")  # no empty segments
     if early:  # the bottom aggregation closes the sample half; the train half starts at its GEMM
         marks = tuple(m for m in marks if m != "fwd0_gemm") + ("sample_agg0",)
+    marks = marks + tuple(f"sample_l{l}" for l in range(e.L - 1))  # per-layer sampling
     gs, segs = e.capture_segments(split_at=marks)
     sample_segs = [("sample", gs)] if not isinstance(gs, list) else \
-        [("sample" if n == "start" else "bottom_agg", g) for n, g in gs]
+        [(f"sample_l{e.L - 1}" if n == "start" else "bottom_agg" if n == "sample_agg0" else n, g) for n, g in gs]
     segs = sample_segs + [(("train_start" if n == "start" else n), g) for n, g in segs]
     tot = {n: 0.0 for n, _ in segs}
     e.cur = 0

@@ -794,6 +794,7 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
     const float* Wn = sW + K * CS;
     bool bad = false;
     for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
+        const int y = labels[seeds ? seeds[i] : i];  // issued early: two dependent loads
         const int cnt = counts[i];
         const int v = frontier[i];
         const int ns = nself[i];
@@ -853,7 +854,6 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
         float se = e0 + e1;
 #pragma unroll
         for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-        const int y = labels[seeds ? seeds[i] : i];
         const float zy = __shfl_sync(0xffffffffu, y < 32 ? z0 : z1, y & 31);
         const float inv = 1.f / se;
         const float d0 = c0 < C ? (e0 * inv - (c0 == y ? 1.f : 0.f)) * grad_scale : 0.f;

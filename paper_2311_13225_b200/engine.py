@@ -362,6 +362,8 @@ class TrainEngine:
         mark = mark or (lambda name: None)
         sc = self.side[1]
         for l in range(self.L - 1, -1, -1):
+            if l < self.L - 1:
+                mark(f"sample_l{l}")
             fr, n = self.frontier(l)
             self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False, dedup=not self._bottom_draws_only(l))
             if l > 0 and not self.bwd_scatter:
