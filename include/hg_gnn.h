@@ -89,6 +89,23 @@ int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t ca
                      const int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
                      int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
                      int32_t* outdeg, int32_t* ws, void* stream);
+/* hg_dedup_relabel in two halves.  hg_dedup_mark: src_vertices, *d_n_src, outdeg
+ * reset (what the NEXT layer's draw needs).  hg_block_relabel: slots order,
+ * slot_local, nself, outdeg, tag retirement (what only the training step needs);
+ * it may run on a second stream concurrently with the next layer's sampling when
+ * that layer uses a different first-occurrence table.  hg_sample_block_mark =
+ * hg_sample_layer + hg_dedup_mark. */
+int hg_dedup_mark(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                  const int32_t* counts, const int32_t* slots, uint64_t* minpos, const int32_t* tag_ctr,
+                  int32_t* src_vertices, int32_t* d_n_src, int32_t* outdeg, int32_t* ws, void* stream);
+int hg_block_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                     const int32_t* counts, int32_t* slots, int32_t* slot_local, const uint64_t* minpos,
+                     int32_t* tag_ctr, int32_t* nself, int32_t* outdeg, int32_t* ws, void* stream);
+int hg_sample_block_mark(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                         const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                         int32_t layer, int32_t* counts, int32_t* slots, uint64_t* minpos, int32_t* tag_ctr,
+                         int32_t* src_vertices, int32_t* d_n_src, int32_t* outdeg, int32_t* ws, int32_t* scratch,
+                         void* stream);
 
 /* Block.edge_src / edge_dst (sampler.py:45-78) from the slot form. */
 int64_t hg_block_edges_ws_size(int32_t cap_dst);

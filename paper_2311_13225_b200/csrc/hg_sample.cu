@@ -195,17 +195,6 @@ __global__ void k_sample_seq(const int64_t* __restrict__ offsets, const int* __r
     }
 }
 
-__device__ __forceinline__ bool pos_item(long long p, int n, int f, const int* frontier, const int* counts,
-                                         const int* slots, int& u) {
-    if (p < n) { u = frontier[p]; return true; }
-    const long long q = p - n;
-    const int i = (int)(q / f);
-    const int j = (int)(q - (long long)i * f);
-    if (j >= counts[i]) return false;
-    u = slots[q];
-    return true;
-}
-
 // ---------------------------------------------------------------------------
 // Single-pass first-occurrence compaction (replaces flag -> 3-kernel scan ->
 // emit): each 2048-position tile marks its first occurrences (minpos[u] == p),
@@ -257,15 +246,46 @@ __device__ __forceinline__ void markscan_tile(int t, const int* __restrict__ fro
     unsigned flags = 0;
     int cnt = 0;
     const long long my0 = p0 + (long long)threadIdx.x * MS_ITEMS;
+    // three rounds of independent loads (ids and counts, then the table) instead
+    // of a dependent counts -> slots -> minpos chain per item; the (dst, draw)
+    // coordinates of the thread's contiguous positions are stepped, one division
+    int si = 0, sj = 0;
+    if (my0 > n) {
+        const long long q0 = my0 - n;
+        si = (int)(q0 / f);
+        sj = (int)(q0 - (long long)si * f);
+    }
+    int jk[MS_ITEMS], ck[MS_ITEMS];
 #pragma unroll
     for (int k = 0; k < MS_ITEMS; ++k) {
         const long long p = my0 + k;
-        int x = -1;
-        if (p < P && pos_item(p, n, f, frontier, counts, slots, x) && minpos[x] == fo_key(tag, p)) {
+        u[k] = -1;
+        jk[k] = 0;
+        ck[k] = 1;
+        if (p < P) {
+            if (p < n) {
+                u[k] = frontier[p];
+            } else {
+                u[k] = slots[p - n];
+                ck[k] = counts[si];
+                jk[k] = sj;
+                if (++sj == f) { sj = 0; ++si; }
+            }
+        }
+    }
+    unsigned long long mk[MS_ITEMS];
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        mk[k] = 0;
+        if (u[k] >= 0 && jk[k] < ck[k]) mk[k] = minpos[u[k]];
+    }
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        const long long p = my0 + k;
+        if (p < P && jk[k] < ck[k] && mk[k] == fo_key(tag, p)) {
             flags |= 1u << k;
             ++cnt;
         }
-        u[k] = x;
     }
     // block exclusive scan of per-thread counts
     int x = cnt;
@@ -617,10 +637,12 @@ extern "C" int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout) {
     return (int64_t)(((P + 1) & ~1LL) + 2 * tiles + 4);
 }
 
-extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                                const int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
-                                int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
-                                int32_t* outdeg, int32_t* ws, void* stream) {
+// First half of hg_dedup_relabel: the mark/scan/emit pass alone.  Produces
+// src_vertices[0..n_src), *d_n_src and resets outdeg[0..n_src); the table
+// entries of first occurrences now hold local ids for hg_block_relabel.
+extern "C" int hg_dedup_mark(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                             const int32_t* counts, const int32_t* slots, uint64_t* minpos, const int32_t* tag_ctr,
+                             int32_t* src_vertices, int32_t* d_n_src, int32_t* outdeg, int32_t* ws, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("dedup(empty)"); }
     const long long P = (long long)cap_dst * (fanout + 1);
@@ -631,6 +653,22 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
     hg_launch(k_markscan, (unsigned)tiles, MS_THREADS, 0, s, frontier, d_n_dst, cap_dst, fanout, counts, slots,
                                                       (unsigned long long*)minpos, tag_ctr, flags, src_vertices,
                                                       d_n_src, status, d_gen, outdeg);
+    return hg_check_launch("dedup_mark");
+}
+
+// Second half: per-destination local ids + segment sort, nself / outdeg, and the
+// retirement of the table's tag and the workspace's scan generation.  Nothing in
+// the next layer's draw / mark reads its outputs, so it may run on another stream
+// concurrently with them provided they use a DIFFERENT first-occurrence table.
+extern "C" int hg_block_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                                const int32_t* counts, int32_t* slots, int32_t* slot_local, const uint64_t* minpos,
+                                int32_t* tag_ctr, int32_t* nself, int32_t* outdeg, int32_t* ws, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cap_dst == 0) return HG_OK;
+    const long long P = (long long)cap_dst * (fanout + 1);
+    const long long tiles = (P + MS_TILE - 1) / MS_TILE;
+    int* flags = ws;
+    int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
     if (fanout <= 32) {
         const int W = seg_width(fanout);
         const int grid = hg_grid((long long)cap_dst * W, 256, hg_sample_ctas_per_sm());
@@ -645,7 +683,18 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
                                                                     slot_local, (const unsigned long long*)minpos,
                                                                     flags, nself, outdeg, tag_ctr, d_gen);
     }
-    return hg_check_launch("dedup_relabel");
+    return hg_check_launch("block_relabel");
+}
+
+extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                                const int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
+                                int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t cap_src, int32_t* nself,
+                                int32_t* outdeg, int32_t* ws, void* stream) {
+    int rc = hg_dedup_mark(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos, tag_ctr, src_vertices, d_n_src,
+                           outdeg, ws, stream);
+    if (rc) return rc;
+    return hg_block_relabel(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, tag_ctr, nself,
+                            outdeg, ws, stream);
 }
 
 // Draw + dedup + relabel of one layer (hg_sample_layer followed by
@@ -719,6 +768,22 @@ extern "C" int hg_sample_block(const int64_t* offsets, const int32_t* targets, c
     if (rc) return rc;
     return hg_dedup_relabel(frontier, d_n_dst, cap_dst, fanout, counts, slots, slot_local, minpos, tag_ctr,
                             src_vertices, d_n_src, cap_src, nself, outdeg, ws, stream);
+}
+
+extern "C" int hg_sample_block_mark(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
+                                    const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
+                                    int32_t layer, int32_t* counts, int32_t* slots, uint64_t* minpos,
+                                    int32_t* tag_ctr, int32_t* src_vertices, int32_t* d_n_src, int32_t* outdeg,
+                                    int32_t* ws, int32_t* scratch, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fanout < 1 || cap_dst < 0) { hg_set_error("sample_block_mark: bad fanout/cap"); return HG_EINVAL; }
+    if (!minpos) { hg_set_error("sample_block_mark: minpos required"); return HG_EINVAL; }
+    if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("sample_block_mark(empty)"); }
+    int rc = sample_layer_impl(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots,
+                               minpos, tag_ctr, scratch, nullptr, s);
+    if (rc) return rc;
+    return hg_dedup_mark(frontier, d_n_dst, cap_dst, fanout, counts, slots, minpos, tag_ctr, src_vertices, d_n_src,
+                         outdeg, ws, stream);
 }
 
 // Compacted Block edges; starts: cap_dst ints workspace (+ scan ws after it).

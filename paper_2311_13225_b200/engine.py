@@ -194,14 +194,20 @@ class TrainEngine:
         # transposed aggregation of layers >= 1: deterministic fixed-point scatter
         # (default) or the CSC gather over a stable src-major view (HG_BWD=csc)
         self.bwd_scatter = os.environ.get("HG_BWD", "scatter").lower() != "csc"
+        # relabel halves of layers >= 1 off the sampling critical path (HG_SPLIT_RELABEL=0: in line)
+        self.split_relabel = os.environ.get("HG_SPLIT_RELABEL", "1") != "0"
         self.sets = []
         for k in range(n_sets):
-            mp = None if k == 0 else dg.minpos.like()
+            mp = dg.minpos if k == 0 else dg.minpos.like()
+            # layers of opposite parity use different first-occurrence tables: a
+            # layer's relabel half runs on a side stream concurrently with the next
+            # layer's draw + mark (enqueue_sample_part)
+            mps = (mp, mp.like() if self.L > 1 and self.split_relabel else mp)
             # outdeg: GCN norm; with the scatter backward also the per-source edge
             # counts that select its single-contribution fast path
             smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage,
                                 need_outdeg=(not self.sage) or (l > 0 and self.bwd_scatter),
-                                need_csc=l > 0 and not self.bwd_scatter, minpos=mp) for l in range(self.L)]
+                                need_csc=l > 0 and not self.bwd_scatter, minpos=mps[l % 2]) for l in range(self.L)]
             self.sets.append(SampleSet(samplers=smp, seeds=z32(self.batch_cap), counts_in=z32(2),
                                        bp=torch.zeros(BP_SIZE, dtype=torch.int64, device=dev)))
         self.cur = 0
@@ -359,21 +365,39 @@ class TrainEngine:
         early_agg0); the transposed (backward) views of the CSC path are built on
         a side stream (a parallel graph branch) joined at the end."""
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
-        mark = mark or (lambda name: None)
         sc = self.side[1]
+        forked = False
+        if mark is not None:  # a mark may end a capture segment: join the side branch first
+            user_mark = mark
+
+            def mark(name):
+                nonlocal forked
+                if forked:
+                    main.wait_stream(sc)
+                    forked = False
+                user_mark(name)
+        else:
+            mark = lambda name: None  # noqa: E731
         for l in range(self.L - 1, -1, -1):
             if l < self.L - 1:
                 mark(f"sample_l{l}")
             fr, n = self.frontier(l)
-            self.samplers[l].run(fr, n, self.bp, l, main, with_csc=False, dedup=not self._bottom_draws_only(l))
+            smp = self.samplers[l]
+            if forked and l + 2 < self.L and self.samplers[l + 2].minpos is smp.minpos:
+                main.wait_stream(sc)  # the table is still being read by layer l+2's relabel
+            split = self.split_relabel and l > 0 and not self._bottom_draws_only(l)
+            smp.run(fr, n, self.bp, l, main, with_csc=False, dedup=not self._bottom_draws_only(l),
+                    relabel_stream=sc if split else None)
+            forked = forked or split
             if l > 0 and not self.bwd_scatter:
                 sc.wait_stream(main)
-                self.samplers[l].build_csc(n, sc, frontier=fr)
-        if self.L > 1 and not self.bwd_scatter:
-            main.wait_stream(sc)
+                smp.build_csc(n, sc, frontier=fr)
+                forked = True
         if self.early_agg0():
             mark("sample_agg0")
             self._enqueue_agg0(main.cuda_stream)
+        if forked:  # the relabel halves also overlap the bottom aggregation
+            main.wait_stream(sc)
 
     def enqueue_train_part(self, stream=None, mark=None):
         main = stream if stream is not None else torch.cuda.current_stream(self.device)

@@ -143,10 +143,14 @@ class LayerSampler:
             self.csc_w = torch.zeros(max(cap_dst * self.f, 1), dtype=torch.float32, device=dev)
 
     def run(self, frontier, d_n_dst, d_seed, layer: int, stream=None, cap_dst: int | None = None,
-            with_csc: bool = True, dedup: bool = True):
+            with_csc: bool = True, dedup: bool = True, relabel_stream=None):
         """Enqueue the block build for `frontier` (device int32, count *d_n_dst).
         ``with_csc=False`` defers the transposed view to ``build_csc`` (e.g. on a
-        side stream, off the forward critical path)."""
+        side stream, off the forward critical path).  ``relabel_stream``: the
+        relabel half (segment order, slot_local, nself, outdeg) runs there after
+        the draw + mark half on ``stream``; src / n_src are ready on ``stream``,
+        the rest once ``relabel_stream`` is joined.  The next layer's sampler on
+        ``stream`` must then use a different first-occurrence table."""
         cap = self.cap_dst if cap_dst is None else int(cap_dst)
         assert cap <= self.cap_dst
         if cap != self.cap_dst:
@@ -169,6 +173,18 @@ class LayerSampler:
             _lib.call("hg_sample_layer_draws", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap,
                       self.f, ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.nself),
                       ptr(self.scratch), s)
+            return self
+        if relabel_stream is not None:
+            _lib.call("hg_sample_block_mark", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap,
+                      self.f, ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.minpos.table),
+                      ptr(self.minpos.tag), ptr(self.src), ptr(self.n_src), ptr(self.outdeg), ptr(self.ws),
+                      ptr(self.scratch), s)
+            relabel_stream.wait_stream(_as_stream(stream, g.device))
+            _lib.call("hg_block_relabel", ptr(frontier), ptr(d_n_dst), cap, self.f, ptr(self.counts),
+                      ptr(self.slots), ptr(self.slot_local), ptr(self.minpos.table), ptr(self.minpos.tag),
+                      ptr(self.nself), ptr(self.outdeg), ptr(self.ws), relabel_stream.cuda_stream)
+            if self.need_csc and with_csc:
+                self.build_csc(d_n_dst, relabel_stream, cap)
             return self
         # draw + dedup + relabel (one cooperative kernel for small blocks)
         _lib.call("hg_sample_block", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
