@@ -156,7 +156,7 @@ class TrainEngine:
 
     def __init__(self, dg: DeviceGraph, model: str, dims, fanouts, batch_cap: int, lr: float,
                  optimizer: str = "sgd", weights=None, hot: HotBuffers | None = None, max_batches: int = 1,
-                 allreduce=None, n_sets: int = 2):
+                 allreduce=None, n_sets: int | None = None):
         _lib.load()
         if model not in ("gcn", "sage"):
             raise ValueError(f"unknown model {model!r}")
@@ -197,6 +197,8 @@ class TrainEngine:
         # relabel halves of layers >= 1 off the sampling critical path (HG_SPLIT_RELABEL=0: in line)
         self.split_relabel = os.environ.get("HG_SPLIT_RELABEL", "1") != "0"
         self.sets = []
+        # sample sets in flight (the pipeline reuses set k % n_sets after batch k - n_sets trained)
+        n_sets = int(os.environ.get("HG_SETS", "2")) if n_sets is None else int(n_sets)
         for k in range(n_sets):
             mp = dg.minpos if k == 0 else dg.minpos.like()
             # layers of opposite parity use different first-occurrence tables: a

@@ -1,2 +1,2 @@
-for c in 8 4 2; do HG_AGG_CTAS_PER_SM=$c timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- agg ctas/SM $c"; done
-HG_EARLY_AGG=0 timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- early off"
+for k in "" "hg_aggregate_fwd:0" "hg_gemm_tc:0" "hg_wgrad_tc" "hg_wgrad_tc:2" "hg_aggregate_bwd_scatter,hg_aggregate_bwd_finish" "hg_sage_top_fused" "hg_sgd_fused" "hg_aggregate_fwd:0,hg_gemm_tc:0,hg_wgrad_tc:2"; do
+  HG_WHATIF_SKIP="$k" timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- skip [$k]"; done

@@ -14,7 +14,38 @@ from paper_2311_13225_b200.datagen import make_dataset  # noqa: E402
 from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer  # noqa: E402
 
 
+def install_skips(spec):
+    """HG_WHATIF_SKIP="name[:k],...": drop the k-th (every, without :k) call of an
+    entry point within each captured half — results become garbage, only the
+    timing of the remaining work is meaningful.  Float-output kernels only."""
+    from paper_2311_13225_b200 import _lib, engine
+    rules = [(r.split(":")[0], int(r.split(":")[1]) if ":" in r else None) for r in spec.split(",") if r]
+    counts = {}
+    real = _lib.call
+
+    def call(name, *args):
+        k = counts.get(name, 0)
+        counts[name] = k + 1
+        for n, idx in rules:
+            if n == name and (idx is None or idx == k):
+                return 0
+        return real(name, *args)
+
+    _lib.call = call
+    for half in ("enqueue_sample_part", "enqueue_train_part"):
+        f = getattr(engine.TrainEngine, half)
+
+        def wrapped(self, *a, _f=f, **kw):
+            counts.clear()
+            return _f(self, *a, **kw)
+
+        setattr(engine.TrainEngine, half, wrapped)
+
+
 def main():
+    import os
+    if os.environ.get("HG_WHATIF_SKIP"):
+        install_skips(os.environ["HG_WHATIF_SKIP"])
     K = 100
     ds = make_dataset("c2", cache_dir=bench.CACHE)
     cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
