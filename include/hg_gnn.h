@@ -301,6 +301,20 @@ int hg_sgd_fused(float* w, const float* g, int64_t n, float lr, int32_t n_img, c
 int hg_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
             int32_t* d_t, uint32_t* d_maxdelta, void* stream);
 
+/* ---- native step driver: the per-batch loop of Trainer.train_batches
+ *      (orchestrator.py:520-560) over captured half-step graphs.  For step k:
+ *      H2D of host_stage[k*slot_bytes, +copy_bytes[k]) into dev_stage[k % n_sets]
+ *      + sample_execs[k % n_sets] on sample_stream (after batch k - n_sets
+ *      trained); train_execs[k % n_sets] on train_stream (after that sample half),
+ *      which records batch k's loss at d_loss_arr[k] (bp[3] = k); at the end one
+ *      D2H of d_loss_arr[0, n_steps) into host_loss.  Execs are cudaGraphExec_t; host_stage
+ *      and host_loss pinned; both streams start after caller_stream, which waits
+ *      for both at the end (asynchronous: synchronise caller_stream to read). */
+int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* sample_execs, const int64_t* train_execs,
+                    void* caller_stream, void* sample_stream, void* train_stream, const int64_t* dev_stage,
+                    const uint8_t* host_stage, int64_t slot_bytes, const int64_t* copy_bytes,
+                    const float* d_loss_arr, float* host_loss);
+
 /* ---- K11 historical-embedding store (store.py:24-146; orchestrator.py:259-271,
  *      381-395 producer, 480-504 consumer, gnnmath.py:240-245 injection).
  *  bp: per-batch int64 parameter block (see hg_train.cu BP_* indices). */

@@ -143,6 +143,17 @@ class SampleSet:
     seeds: torch.Tensor      # int32 [batch_cap]
     counts_in: torch.Tensor  # int32 [2]: n_seeds, gradient divisor (global batch)
     bp: torch.Tensor         # int64 [BP_SIZE] parameter block
+    stage: torch.Tensor      # uint8: bp | counts_in | seeds as ONE buffer (one H2D copy per batch)
+
+
+STAGE_COUNTS = BP_SIZE * 8       # byte offsets inside SampleSet.stage
+STAGE_SEEDS = BP_SIZE * 8 + 16
+
+
+def stage_views(stage: torch.Tensor):
+    """(bp int64[BP_SIZE], counts int32[2], seeds int32[...]) views of a staging buffer."""
+    return (stage[:STAGE_COUNTS].view(torch.int64), stage[STAGE_COUNTS:STAGE_COUNTS + 8].view(torch.int32),
+            stage[STAGE_SEEDS:].view(torch.int32))
 
 
 class TrainEngine:
@@ -210,8 +221,9 @@ class TrainEngine:
             smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage,
                                 need_outdeg=(not self.sage) or (l > 0 and self.bwd_scatter),
                                 need_csc=l > 0 and not self.bwd_scatter, minpos=mps[l % 2]) for l in range(self.L)]
-            self.sets.append(SampleSet(samplers=smp, seeds=z32(self.batch_cap), counts_in=z32(2),
-                                       bp=torch.zeros(BP_SIZE, dtype=torch.int64, device=dev)))
+            stage = torch.zeros(STAGE_SEEDS + 4 * self.batch_cap, dtype=torch.uint8, device=dev)
+            bp, counts_in, seeds = stage_views(stage)
+            self.sets.append(SampleSet(samplers=smp, seeds=seeds, counts_in=counts_in, bp=bp, stage=stage))
         self.cur = 0
         # ---- parameters ----
         self.params = DenseParams(model, self.dims, weights, dev)
@@ -769,9 +781,12 @@ class BatchFeeder:
     def __init__(self, engine: TrainEngine, slots: int = 4):
         self.e = engine
         cap = engine.batch_cap
-        self.seeds = [torch.zeros(cap, dtype=torch.int32).pin_memory() for _ in range(slots)]
-        self.counts = [torch.zeros(2, dtype=torch.int32).pin_memory() for _ in range(slots)]
-        self.bp = [torch.zeros(BP_SIZE, dtype=torch.int64).pin_memory() for _ in range(slots)]
+        # pinned images of SampleSet.stage (bp | counts | seeds): one H2D copy per batch
+        self.stage = [torch.zeros(STAGE_SEEDS + 4 * cap, dtype=torch.uint8).pin_memory() for _ in range(slots)]
+        views = [stage_views(t) for t in self.stage]
+        self.bp = [v[0] for v in views]
+        self.counts = [v[1] for v in views]
+        self.seeds = [v[2] for v in views]
         self.events = [None] * slots
         self.k = 0
         self.h2d_bytes = 0
@@ -792,10 +807,9 @@ class BatchFeeder:
         self.bp[k].numpy()[:] = np.array([rs], dtype=np.uint64).view(np.int64)[0], n, reading_batch, \
             batch_in_epoch, cpu_tag, table_sel, cur_stamp, warm
         e = self.e.sets[self.e.cur if set_index is None else set_index]
-        e.seeds[:n].copy_(self.seeds[k][:n], non_blocking=True)
-        e.counts_in.copy_(self.counts[k], non_blocking=True)
-        e.bp.copy_(self.bp[k], non_blocking=True)
+        nb = STAGE_SEEDS + 4 * n
+        e.stage[:nb].copy_(self.stage[k][:nb], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
         self.events[k] = ev
-        self.h2d_bytes = n * 4 + 8 + BP_SIZE * 8
+        self.h2d_bytes = nb

@@ -19,6 +19,7 @@ idle time, hotness.py:129), i.e. the reference with simulate_costs=False.
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -27,7 +28,7 @@ import torch
 
 from . import _lib, dense, runplan
 from .device import DeviceGraph, pad4, ptr, stream_ptr, u64_tensor
-from .engine import BatchFeeder, HotBuffers, Pipeline, TrainEngine
+from .engine import STAGE_COUNTS, STAGE_SEEDS, BatchFeeder, HotBuffers, Pipeline, TrainEngine
 from .gnnmath import init_params
 from .hotness import estimate_hotness, select_hot
 from .sampler import Fanouts, LayerSampler
@@ -456,6 +457,8 @@ class Trainer:
         its own pinned slot.  Returns one handle per batch (call -> float loss)."""
         pipe, e = self.pipeline, self.engine
         n = len(batches)
+        if n and e.g_sample is not None and os.environ.get("HG_NATIVE_LOOP", "1") != "0":
+            return self._train_batches_native(batches)
         pin = torch.zeros(max(n, 1), dtype=torch.float32).pin_memory()
         v0 = self.version
 
@@ -476,6 +479,64 @@ class Trainer:
                 pin[i:i + 1].copy_(e.d_loss, non_blocking=True)
         done.record(pipe.st)
         pipe.drain()
+        self.version += n
+
+        def handle(i):
+            def get():
+                done.synchronize()
+                return float(pin[i].item())
+            return get
+        return [handle(i) for i in range(n)]
+
+    def _train_batches_native(self, batches):
+        """train_batches through the native step driver (hg_pipeline_run): the
+        batches' inputs are packed into pinned staging slots (SampleSet.stage
+        layout) up front, then one C call enqueues every step's H2D, both
+        half-step graphs and the loss D2H — no Python work per step."""
+        e, pipe = self.engine, self.pipeline
+        n, cap = len(batches), e.batch_cap
+        rec = int(e.loss_arr.numel())  # batch k records its loss at loss_arr[bp[3] = k]
+        if n > rec:
+            hs = []
+            for i in range(0, n, rec):
+                hs += self._train_batches_native(batches[i:i + rec])
+            return hs
+        slot = STAGE_SEEDS + 4 * cap
+        prev = getattr(self, "_native_done", None)
+        if prev is not None:
+            prev.synchronize()  # the staging slots of the previous call may still be in flight
+        buf = getattr(self, "_native_stage", None)
+        if buf is None or buf.shape[0] < n:
+            buf = torch.zeros((max(n, 64), slot), dtype=torch.uint8).pin_memory()
+            self._native_stage = buf
+        hn = buf.numpy()
+        bp = hn[:n, :STAGE_COUNTS].view(np.int64)
+        cnt = hn[:n, STAGE_COUNTS:STAGE_COUNTS + 8].view(np.int32)
+        sd = hn[:n, STAGE_SEEDS:].view(np.int32)
+        nbytes = np.empty(n, np.int64)
+        v0 = self.version
+        for i, (seeds, rs) in enumerate(batches):
+            seeds = np.asarray(seeds)
+            k = int(seeds.shape[0])
+            if k > cap:
+                raise ValueError("batch larger than the engine's capacity")
+            sd[i, :k] = seeds
+            cnt[i] = (k, self.dist.global_batch(seeds) if self.dist else k)
+            bp[i] = (np.array([int(rs) & 0xFFFFFFFFFFFFFFFF], np.uint64).view(np.int64)[0], k, v0 + i, i, -1, 0,
+                     -1, 0)
+            nbytes[i] = STAGE_SEEDS + 4 * k
+        pin = torch.zeros(n, dtype=torch.float32).pin_memory()
+        execs_s = np.array([g.raw_cuda_graph_exec() for g in e.g_sample], np.int64)
+        execs_t = np.array([g.raw_cuda_graph_exec() for g in e.g_train], np.int64)
+        stages = np.array([st.stage.data_ptr() for st in e.sets], np.int64)
+        cur = torch.cuda.current_stream(e.device)
+        _lib.call("hg_pipeline_run", n, len(e.sets), execs_s.ctypes.data, execs_t.ctypes.data, cur.cuda_stream,
+                  pipe.ss.cuda_stream, pipe.st.cuda_stream, stages.ctypes.data, buf.data_ptr(), slot,
+                  nbytes.ctypes.data, ptr(e.loss_arr), pin.data_ptr())
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._native_done = done
+        self.feeder.h2d_bytes = int(nbytes[0])
         self.version += n
 
         def handle(i):
