@@ -1,2 +1,1 @@
-for k in "" "hg_aggregate_fwd:0" "hg_gemm_tc:0" "hg_wgrad_tc" "hg_wgrad_tc:2" "hg_aggregate_bwd_scatter,hg_aggregate_bwd_finish" "hg_sage_top_fused" "hg_sgd_fused" "hg_aggregate_fwd:0,hg_gemm_tc:0,hg_wgrad_tc:2"; do
-  HG_WHATIF_SKIP="$k" timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- skip [$k]"; done
+for a in 4 32; do for f in 4 32; do HG_ACT_ALIGN=$a HG_FEAT_ALIGN=$f timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- act $a feat $f"; done; done
