@@ -1,1 +1,2 @@
-for a in 4 32; do for f in 4 32; do HG_ACT_ALIGN=$a HG_FEAT_ALIGN=$f timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- act $a feat $f"; done; done
+for e in 1 0; do HG_EARLY_AGG=$e timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- early agg $e"; done
+HG_EARLY_AGG=0 HG_WHATIF_SKIP="hg_gemm_tc:0" timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3 | tr '\n' ' '; echo " <- early agg 0, no bottom GEMM"
