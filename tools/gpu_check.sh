@@ -1,3 +1,5 @@
+#!/bin/bash
+# Quick GPU check: full gpu test suite, pipeline probe, bench headline + phases, launch list.
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_h.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_h.log
 timeout 600 python tools/overlap_probe.py 2>/dev/null | head -3
 timeout 600 python bench.py --no-cpu-baseline --phases > gpurun_out/b_h.json 2>/dev/null; python -c "
