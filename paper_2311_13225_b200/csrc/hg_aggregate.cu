@@ -779,13 +779,15 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
     float* __restrict__ dself_out, int ld_dself, const float* __restrict__ hmask, int ld_hmask,
     const uint8_t* __restrict__ inj, unsigned long long* __restrict__ acc, int F_acc, float* __restrict__ dx,
     int ld_dx, int* __restrict__ d_flags, float* __restrict__ row_loss, float* __restrict__ d_loss) {
-    hg_pdl_begin();
     extern __shared__ float sW[];  // [2K][C]: W_self rows then W_neigh rows
     __shared__ double s_part[TOP_THREADS / 32];
     __shared__ bool s_last;
     const int CS = C | 1;  // odd row stride: conflict-free column walks in the dX loop
+    // the weights were last written by the previous step's update, long complete:
+    // staged before griddepcontrol.wait, overlapping the previous kernel's tail
     stage_w(sW, W, 2 * K, C, CS);
     __syncthreads();
+    hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     const float grad_scale = 1.0f / (float)(d_div ? *d_div : (n > 0 ? n : 1));
     const int lane = threadIdx.x & 31;

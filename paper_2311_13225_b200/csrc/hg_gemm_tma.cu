@@ -70,7 +70,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2, int ls1, int ls2,
            const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
            int M_cap, int act) {
-    hg_pdl_begin();
     constexpr int S = fwd_stages<BN>();
     constexpr int STAGE = fwd_stage_bytes<BN>();
     constexpr int B_BYTES = 2 * BN * 128;
@@ -81,15 +80,11 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
     __shared__ uint64_t full[S], splt[S], empty[S], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int M = hg_load_count(d_M, M_cap);
-    const int n_mt = (M + 127) >> 7;
-    if ((int)blockIdx.x >= n_mt) return;
-    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int nk = nk1 + nk2;
-    const int iters = n_my * nk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.y * BN;
 
+    // prologue before griddepcontrol.wait (overlaps the previous kernel's tail)
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < S; ++i) {
@@ -111,6 +106,15 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
+    hg_pdl_begin();
+    const int M = hg_load_count(d_M, M_cap);
+    const int n_mt = (M + 127) >> 7;
+    if ((int)blockIdx.x >= n_mt) {
+        if (warp == 1) tmem_dealloc(tmem, NCOLS);
+        return;
+    }
+    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = n_my * nk;
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
@@ -260,7 +264,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1)
 k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2, int ls1, int ls2,
               const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
               int M_cap, int act) {
-    hg_pdl_begin();
     constexpr int S = ts_nstages<BN, PAIR>();
     constexpr int STAGE = ts_stage_bytes<BN, RESB>();
     constexpr int B_BYTES = 2 * BN * 128;
@@ -278,15 +281,12 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
     __shared__ uint64_t full[S], splt[S], empty[S], afree[S], tfull[2], tempty[2], bfull;
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int M = hg_load_count(d_M, M_cap);
-    const int n_mt = (M + 127) >> 7;
-    if ((int)blockIdx.x >= n_mt) return;
-    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int nk = nk1 + nk2;
-    const int iters = n_my * nk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.y * BN;
 
+    // prologue (barriers, TMEM, descriptor prefetch) touches nothing the previous
+    // kernel writes: it runs before griddepcontrol.wait, overlapping that kernel's tail
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < S; ++i) {
@@ -311,6 +311,15 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
+    hg_pdl_begin();
+    const int M = hg_load_count(d_M, M_cap);
+    const int n_mt = (M + 127) >> 7;
+    if ((int)blockIdx.x >= n_mt) {  // nothing to do: give the TMEM back
+        if (warp == 1) tmem_dealloc(tmem, 512);
+        return;
+    }
+    const int n_my = (n_mt - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = n_my * nk;
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
@@ -503,7 +512,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
             int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
-    hg_pdl_begin();
     constexpr int S = wg_stages<BN>();
     constexpr int STAGE = wg_stage_bytes<BN>();
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
@@ -515,17 +523,12 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
     __shared__ uint64_t full[S], splt[S], empty[S], done;
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int M = hg_load_count(d_M, M_cap);
-    const int rpc = wg_rows_per_chunk(M, n_chunks);
     const int chunk = blockIdx.y;
-    const int mbeg = chunk * rpc;
-    if (mbeg >= M) return;  // the reduction skips chunks past M
-    const int mend = min(M, mbeg + rpc);
     const int src = blockIdx.x / ktiles, kt = blockIdx.x - src * ktiles;
     const CUtensorMap* tmA = src ? &tmA2 : &tmA1;
-    const int nsteps = (mend - mbeg + 31) >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    // prologue before griddepcontrol.wait (overlaps the previous kernel's tail)
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < S; ++i) {
@@ -543,6 +546,16 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
+    hg_pdl_begin();
+    const int M = hg_load_count(d_M, M_cap);
+    const int rpc = wg_rows_per_chunk(M, n_chunks);
+    const int mbeg = chunk * rpc;
+    if (mbeg >= M) {  // the reduction skips chunks past M
+        if (warp == 1) tmem_dealloc(tmem, NCOLS);
+        return;
+    }
+    const int mend = min(M, mbeg + rpc);
+    const int nsteps = (mend - mbeg + 31) >> 5;
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer: 4 A boxes (32 k x 32 rows) + NG G boxes per step
