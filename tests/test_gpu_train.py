@@ -232,3 +232,42 @@ def test_native_step_driver_equals_python_loop(monkeypatch, model):
     assert np.array_equal(out["0"][0], out["1"][0])
     assert np.array_equal(out["0"][1], out["1"][1])
     assert out["0"][2] == out["1"][2] == 10
+
+
+@pytest.mark.parametrize("model", ["sage", "gcn"])
+def test_schedule_switches_bitwise(monkeypatch, model):
+    """Scheduling switches change where and when kernels run, never the arithmetic:
+    relabel halves on a side branch (HG_SPLIT_RELABEL) vs in line, programmatic
+    dependent launch (with pre-wait prologues) on vs off, the bottom aggregation in
+    the sample half (HG_EARLY_AGG) vs the train half, three sample sets vs two —
+    whole runs give bit-identical losses and weights."""
+    from paper_2311_13225_b200 import _lib
+    from paper_2311_13225_b200.datagen import make_dataset
+    from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer
+    ds = make_dataset("tiny")
+    kw = dict(model=model, layers=3, fanouts=(4, 3, 2), hidden_dim=16, batch_size=64, epochs=2, lr=0.05, seed=5,
+              strategy="case1")
+    lib = _lib.load()
+
+    def run(env, pdl=1):
+        for k in ("HG_SPLIT_RELABEL", "HG_EARLY_AGG", "HG_SETS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        lib.hg_set_tuning(5, pdl)
+        try:
+            tr = Trainer(ds, TrainConfig(**kw))
+            losses, first = [], 0
+            for epoch in range(2):
+                plan = tr.build_epoch_plan(epoch, first)
+                losses.append(tr.run_epoch(plan).losses)
+                first += len(plan.batches)
+            return np.concatenate(losses), tr.engine.params.flat.cpu().numpy().copy()
+        finally:
+            lib.hg_set_tuning(5, 1)
+
+    ref = run({})
+    for env, pdl in (({"HG_SPLIT_RELABEL": "0"}, 1), ({}, 0), ({"HG_EARLY_AGG": "0"}, 1), ({"HG_SETS": "3"}, 1)):
+        got = run(env, pdl)
+        assert np.array_equal(ref[0], got[0]), (env, pdl)
+        assert np.array_equal(ref[1], got[1]), (env, pdl)
