@@ -786,13 +786,17 @@ int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, co
     const bool resb = g_resb && nk * 2 * BN * 128 <= RESB_MAX_BYTES;
     const int smem = resb ? ts_stages<BN>() * ts_stage_bytes<BN, true>() + nk * 2 * BN * 128 + 1024
                           : ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024;
-    const bool pair = g_pair && BN <= 64 && !resb;
+    const bool pair = g_pair && BN <= 64;
     constexpr bool PB = BN <= 64;
     const int smem_pair = ts_nstages<BN, PB>() * ts_stage_bytes<BN, false>() + 1024;
+    // resident B + paired MMAs: the A ring only (TMEM-limited depth) behind the whole B image
+    const int smem_resb_pair = ts_nstages<BN, PB>() * ts_stage_bytes<BN, true>() + nk * 2 * BN * 128 + 1024;
     static bool attr = false;
     if (!attr) {
         const int mx = ts_stages<BN>() * ts_stage_bytes<BN, true>() + RESB_MAX_BYTES + 1024;
         cudaFuncSetAttribute(k_gemm_tma_ts<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, true, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ts_nstages<BN, PB>() * ts_stage_bytes<BN, true>() + RESB_MAX_BYTES + 1024);
         cudaFuncSetAttribute(k_gemm_tma_ts<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024);
         cudaFuncSetAttribute(k_gemm_tma_ts<BN, false, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair);
@@ -800,7 +804,10 @@ int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, co
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
-    if (resb)
+    if (resb && pair)
+        hg_launch(k_gemm_tma_ts<BN, true, (BN <= 64)>, dim3(gx, n_nt), FWD_THREADS, smem_resb_pair, s, m1, m2, nk1, nk2,
+                  ls1, ls2, bimg, C, ldc, N, d_M, M_cap, act);
+    else if (resb)
         hg_launch(k_gemm_tma_ts<BN, true, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc,
                   N, d_M, M_cap, act);
     else if (pair)

@@ -58,7 +58,9 @@ def main():
     wg_bytes = M * 2 * K * 4 + M * N * 4
     for name, legacy, form, sk, resb, pair in (("legacy cp.async", 1, 1, 0, 0, 0), ("tma SS", 0, 0, 0, 0, 0),
                                                ("tma TS", 0, 1, 0, 0, 0), ("tma TS resident B", 0, 1, 0, 1, 0),
-                                               ("tma TS paired", 0, 1, 0, 0, 1), ("skinny simt", 0, 1, 1, 0, 1)):
+                                               ("tma TS paired", 0, 1, 0, 0, 1),
+                                               ("tma TS paired resident B", 0, 1, 0, 1, 1),
+                                               ("skinny simt", 0, 1, 1, 0, 1)):
         lib.hg_set_tuning(7, pair)
         lib.hg_set_tuning(6, resb)
         lib.hg_set_tuning(4, sk)
