@@ -234,13 +234,13 @@ __device__ __forceinline__ void markscan_tile(int t, const int* __restrict__ fro
     __shared__ int s_prefix;
     const int n = hg_load_count(d_n, cap);
     const uint32_t tag = fo_tag(tag_ctr);
+    const uint32_t gen = (uint32_t)(*d_gen) + 1u;  // issued with the two loads above
     const long long P = (long long)n * (f + 1);
     const long long p0 = (long long)t * MS_TILE;
     if (p0 >= P) {
         if (t == 0 && threadIdx.x == 0) *d_n_src = 0;
         return;  // no later tile waits on this one
     }
-    const uint32_t gen = (uint32_t)(*d_gen) + 1u;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int u[MS_ITEMS];
     unsigned flags = 0;
