@@ -254,7 +254,9 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
  * key 6: TS-form GEMM keeps the whole B image resident in smem when it fits, A ring released by the split warps (1) / streams B per stage (0, default);
  * key 7: paired hi|lo MMAs (N = 2*BN operand, two instructions per K slice instead of three) for BN <= 64 (1, default) / 0;
  * key 8: hg_sample_block runs small blocks as one cooperative kernel (1) / three kernels (0, default: the
- *        grid syncs measured slower than the launch gaps they replace)) */
+ *        grid syncs measured slower than the launch gaps they replace));
+ * key 11: weight gradient with A^T's hi/lo written to TMEM by the split warps, MMAs reading only G from
+ *        shared memory (1, default) / both operands from shared memory (0) */
 int hg_set_tuning(int32_t key, int32_t value);
 /* profiling aid: the 8 x 64 globaltimer stamps (ns) of the tensor-core GEMM's
  * pipeline timeline probe (hg_set_tuning key 9, bit 3) */

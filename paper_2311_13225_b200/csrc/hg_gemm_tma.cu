@@ -507,7 +507,12 @@ __device__ __forceinline__ int wg_rows_per_chunk(int M, int n_chunks) {
 // PAIR (BN <= 64): the G hi and lo tiles are consecutive MN groups of one
 // MN-major operand [G_hi | G_lo] (N = 2*BN): A_hi x [G_hi | G_lo] + A_lo x G_hi,
 // two MMAs per K slice instead of three; the epilogue adds the halves.
-template <int BN, bool PAIR>
+// TSA: A^T through TMEM — A is loaded unswizzled (32 rows x 128 k, one TMA box),
+// the split warps write its hi / lo columns straight into TMEM (lane = k,
+// column = reduction row) and the MMAs read only G from shared memory: the
+// per-step smem traffic drops from ~128 KB (A lo written back, A read by the
+// MMAs) to ~80 KB, which is what paces the SS form.
+template <int BN, bool PAIR, bool TSA>
 __global__ void __launch_bounds__(WG_THREADS, 1)
 k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
@@ -516,9 +521,11 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
     constexpr int STAGE = wg_stage_bytes<BN>();
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
     constexpr int NG = BN / 32;       // G boxes (32 columns each) per stage
-    constexpr uint32_t NCOLS = tmem_cols<PAIR ? 2 * BN : BN>();
-    constexpr uint32_t IDESC = idesc_tf32(128, BN, 1, 1);
-    constexpr uint32_t IDESC2 = idesc_tf32(128, 2 * BN, 1, 1);
+    constexpr uint32_t ACC = PAIR ? 2 * BN : BN;
+    constexpr uint32_t NCOLS = TSA ? 512u : tmem_cols<ACC>();
+    static_assert(!TSA || ACC + S * 64 <= 512, "TMEM budget");
+    constexpr uint32_t IDESC = idesc_tf32(128, BN, TSA ? 0 : 1, 1);
+    constexpr uint32_t IDESC2 = idesc_tf32(128, 2 * BN, TSA ? 0 : 1, 1);
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[S], splt[S], empty[S], done;
     __shared__ uint32_t s_tmem;
@@ -566,8 +573,13 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 uint8_t* base = smem + st * STAGE;
                 const int y = mbeg + 32 * j;
                 mbar_expect_tx(&full[st], A_BYTES + G_TILE);
+                if (TSA) {
+                    tma_load_2d(smem_u32(base), tmA, kt * 128, y, &full[st]);  // [32 rows][128 k], row-major
+                } else {
 #pragma unroll
-                for (int g = 0; g < 4; ++g) tma_load_2d(smem_u32(base + g * 4096), tmA, kt * 128 + g * 32, y, &full[st]);
+                    for (int g = 0; g < 4; ++g)
+                        tma_load_2d(smem_u32(base + g * 4096), tmA, kt * 128 + g * 32, y, &full[st]);
+                }
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
                     tma_load_2d(smem_u32(base + 2 * A_BYTES + g * 4096), &tmG, g * 32, y, &full[st]);
@@ -587,7 +599,17 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                     if (c_dbg & 1) break;
                     const uint64_t dah = sdesc(a_hi + s * 1024, lbo, sbo, 1), dal = sdesc(a_lo + s * 1024, lbo, sbo, 1);
                     const uint64_t dgh = sdesc(g_hi + s * 1024, lbo, sbo, 1), dgl = sdesc(g_lo + s * 1024, lbo, sbo, 1);
-                    if (PAIR) {
+                    if (TSA) {  // A^T hi / lo columns of this stage in TMEM, 8 reduction rows per slice
+                        const uint32_t ta = tmem + ACC + (uint32_t)(st * 64) + (uint32_t)(s * 8);
+                        if (PAIR) {
+                            mma_tf32_ts(tmem, ta, dgh, IDESC2, (j | s) ? 1u : 0u);
+                            mma_tf32_ts(tmem, ta + 32, dgh, IDESC, 1u);
+                        } else {
+                            mma_tf32_ts(tmem, ta, dgh, IDESC, (j | s) ? 1u : 0u);
+                            mma_tf32_ts(tmem, ta, dgl, IDESC, 1u);
+                            mma_tf32_ts(tmem, ta + 32, dgh, IDESC, 1u);
+                        }
+                    } else if (PAIR) {
                         mma_tf32(tmem, dah, dgh, IDESC2, (j | s) ? 1u : 0u);
                         mma_tf32(tmem, dal, dgh, IDESC, 1u);
                     } else {
@@ -609,12 +631,28 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
             if (warp == 2 && lane == 0) TL(1, j);
             uint8_t* base = smem + st * STAGE;
             const int valid = mend - (mbeg + 32 * j);  // rows < valid are real
+            if (TSA && !(c_dbg & 2)) {
+                // A^T into TMEM: warp w writes lanes 32*(w%4).. (k), columns 16*half.. (rows)
+                const int q = warp & 3, half = (warp - 2) >> 2;
+                const int k = q * 32 + lane;
+                uint32_t hi[16], lo[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const int m = half * 16 + c;
+                    const float x = m < valid ? *reinterpret_cast<const float*>(base + m * 512 + k * 4) : 0.f;
+                    hi[c] = __float_as_uint(x);
+                    lo[c] = __float_as_uint(tf32_lo(x));
+                }
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + ACC + (uint32_t)(st * 64) + (uint32_t)(half * 16);
+                tmem_st16(ta, hi);
+                tmem_st16(ta + 32, lo);
+            }
             if (!(c_dbg & 2)) {
                 // all loads of the stage first (ILP: the split is latency-bound with
                 // 4 warps), then lo = x - hi and the stores; rows past M -> zeros
-                constexpr int NA = A_BYTES / 16 / WG_SPLIT;
+                constexpr int NA = TSA ? 0 : A_BYTES / 16 / WG_SPLIT;
                 constexpr int NGC = (G_TILE / 16 + WG_SPLIT - 1) / WG_SPLIT;
-                float4 va[NA], vg[NGC];
+                float4 va[NA > 0 ? NA : 1], vg[NGC];
 #pragma unroll
                 for (int i = 0; i < NA; ++i) va[i] = *reinterpret_cast<const float4*>(base + (t + WG_SPLIT * i) * 16);
                 uint8_t* gb = base + 2 * A_BYTES;
@@ -647,6 +685,10 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                         *reinterpret_cast<float4*>(gb + G_TILE + off) = z;
                     }
                 }
+            }
+            if (TSA) {
+                tmem_wait_st();
+                tc_fence_before();
             }
             fence_proxy_async();
             __syncwarp();
@@ -720,6 +762,7 @@ __global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restric
 }
 
 int g_pair = 1;  // paired hi|lo MMA form for BN <= 64, fwd and wgrad (hg_set_tuning key 7)
+int g_wg_tsa = 1;  // wgrad with A^T through TMEM (hg_set_tuning key 11)
 
 // ---------------------------------------------------------------------------
 // host: tensor maps through the driver entry point (no libcuda link needed)
@@ -823,21 +866,27 @@ int g_fwd_form = 1;  // 1: TS form for BN <= 128 (hg_set_tuning key 3), 0: SS fo
 
 template <int BN>
 int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, const CUtensorMap& mg, int K,
-              int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo) {
+              int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo,
+              bool tsa) {
     const int smem = wg_stages<BN>() * wg_stage_bytes<BN>() + 1024;
     constexpr bool PB = BN <= 64;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_wgrad_tma<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_wgrad_tma<BN, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, PB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, PB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    if (g_pair && PB)
-        hg_launch(k_wgrad_tma<BN, PB>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial,
-                  lbo, sbo);
-    else
-        hg_launch(k_wgrad_tma<BN, false>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks,
-                  partial, lbo, sbo);
+#define HG_WG(P, T)                                                                                                  \
+    hg_launch(k_wgrad_tma<BN, P, T>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial, \
+              lbo, sbo)
+    const bool pair = g_pair && PB;
+    if (pair && tsa) HG_WG(PB, true);
+    else if (pair) HG_WG(PB, false);
+    else if (tsa) HG_WG(false, true);
+    else HG_WG(false, false);
+#undef HG_WG
     return hg_check_launch("wgrad_tma");
 }
 
@@ -845,6 +894,7 @@ int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMa
 
 void hg_tma_set_fwd_form(int v) { g_fwd_form = v; }
 void hg_tma_set_resb(int v) { g_resb = v ? 1 : 0; }
+void hg_tma_set_wg_tsa(int v) { g_wg_tsa = v ? 1 : 0; }
 void hg_tma_set_pair(int v) { g_pair = v ? 1 : 0; }
 void hg_tma_set_dbg(int v) { cudaMemcpyToSymbol(c_dbg, &v, sizeof(int)); }
 // timeline probe read-back: 8 x 64 globaltimer stamps (ns)
@@ -902,17 +952,21 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
     if (M_cap > 0) {
         CUtensorMap m1, m2, mg;
         const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-        int rc = make_map(&m1, A1, K, M_cap, lda1, 32, 32, sw);
-        if (!rc && A2) rc = make_map(&m2, A2, K, M_cap, lda2, 32, 32, sw);
+        // TS form: A as plain [32 rows][128 k] boxes (read by the split warps, never by the MMA)
+        const bool tsa = g_wg_tsa != 0;
+        const int abox = tsa ? 128 : 32;
+        const CUtensorMapSwizzle asw = tsa ? CU_TENSOR_MAP_SWIZZLE_NONE : sw;
+        int rc = make_map(&m1, A1, K, M_cap, lda1, abox, 32, asw);
+        if (!rc && A2) rc = make_map(&m2, A2, K, M_cap, lda2, abox, 32, asw);
         if (!A2) m2 = m1;
         if (!rc) rc = make_map(&mg, G, N, M_cap, ldg, 32, 32, sw);
         if (rc) return rc;
         const int Nr = (N + 15) & ~15;
         dim3 grid(ktiles * n_src, n_chunks);
-        if (Nr <= 32) rc = launch_wg<32>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
-        else if (Nr <= 64) rc = launch_wg<64>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
-        else if (Nr <= 128) rc = launch_wg<128>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
-        else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo);
+        if (Nr <= 32) rc = launch_wg<32>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
+        else if (Nr <= 64) rc = launch_wg<64>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
+        else if (Nr <= 128) rc = launch_wg<128>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
+        else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
         if (rc) return rc;
     }
     hg_launch(k_wgrad_tma_reduce, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K * N, n_chunks, d_M, M_cap,

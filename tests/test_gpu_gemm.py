@@ -22,20 +22,23 @@ def _ld(k):
     return (k + 3) // 4 * 4
 
 
-@pytest.fixture(params=["tc", "tc_resb", "tc_unpaired", "skinny"])
+@pytest.fixture(params=["tc", "tc_resb", "tc_unpaired", "tc_wg_ss", "tc_wg_ss_unpaired", "skinny"])
 def path(request):
-    """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores (default), the resident-B
-    TS form (hg_set_tuning key 6), or the optional SIMT latency kernels for
-    small M (key 4)."""
+    """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores (default: paired MMAs, wgrad
+    with A^T through TMEM), the resident-B TS form (hg_set_tuning key 6), unpaired
+    MMAs (key 7), the shared-memory wgrad form (key 11), or the optional SIMT
+    latency kernels for small M (key 4)."""
     from paper_2311_13225_b200 import _lib
     lib = _lib.load()
     lib.hg_set_tuning(4, 1 if request.param == "skinny" else 0)
     lib.hg_set_tuning(6, 1 if request.param == "tc_resb" else 0)
-    lib.hg_set_tuning(7, 0 if request.param == "tc_unpaired" else 1)
+    lib.hg_set_tuning(7, 0 if request.param.endswith("unpaired") else 1)
+    lib.hg_set_tuning(11, 0 if request.param.startswith("tc_wg_ss") else 1)
     yield request.param
     lib.hg_set_tuning(4, 0)
     lib.hg_set_tuning(6, 0)
     lib.hg_set_tuning(7, 1)
+    lib.hg_set_tuning(11, 1)
 
 
 @pytest.mark.parametrize("fn", ["hg_gemm_tc", "hg_gemm_f32"])

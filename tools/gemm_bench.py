@@ -56,11 +56,13 @@ def main():
     ref = None
     fwd_bytes = M * 2 * K * 4 + M * N * 4
     wg_bytes = M * 2 * K * 4 + M * N * 4
-    for name, legacy, form, sk, resb, pair in (("legacy cp.async", 1, 1, 0, 0, 0), ("tma SS", 0, 0, 0, 0, 0),
-                                               ("tma TS", 0, 1, 0, 0, 0), ("tma TS resident B", 0, 1, 0, 1, 0),
-                                               ("tma TS paired", 0, 1, 0, 0, 1),
-                                               ("tma TS paired resident B", 0, 1, 0, 1, 1),
-                                               ("skinny simt", 0, 1, 1, 0, 1)):
+    for name, legacy, form, sk, resb, pair, wts in (("legacy cp.async", 1, 1, 0, 0, 0, 1), ("tma SS", 0, 0, 0, 0, 0, 1),
+                                                    ("tma TS", 0, 1, 0, 0, 0, 1), ("tma TS resident B", 0, 1, 0, 1, 0, 1),
+                                                    ("tma TS paired", 0, 1, 0, 0, 1, 1),
+                                                    ("tma TS paired resident B", 0, 1, 0, 1, 1, 1),
+                                                    ("paired, SS-form wgrad", 0, 1, 0, 0, 1, 0),
+                                                    ("skinny simt", 0, 1, 1, 0, 1, 1)):
+        lib.hg_set_tuning(11, wts)
         lib.hg_set_tuning(7, pair)
         lib.hg_set_tuning(6, resb)
         lib.hg_set_tuning(4, sk)
