@@ -10,7 +10,7 @@
 #include "hg_tc.cuh"
 using namespace hgtc;
 
-template <int N, bool TS>
+template <int N, bool TS, bool BMN = false>
 __global__ void __launch_bounds__(128, 1) k_rate(int iters, unsigned long long* cycles) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -26,14 +26,15 @@ __global__ void __launch_bounds__(128, 1) k_rate(int iters, unsigned long long* 
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s_tmem;
-    constexpr uint32_t IDESC = idesc_tf32(128, N, 0, 0);
+    constexpr uint32_t IDESC = idesc_tf32(128, N, 0, BMN ? 1 : 0);
     if (threadIdx.x == 0) {
         const uint32_t a = smem_u32(smem), b = a + 16384;
         const unsigned long long t0 = clock64();
         for (int i = 0; i < iters; ++i) {
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-                const uint64_t db = sdesc(b + s * 32, 16, 1024);
+                // B K-major (SWIZZLE_128B) or MN-major (SWIZZLE_128B_BASE32B, as the wgrad's G operand)
+                const uint64_t db = BMN ? sdesc(b + s * 1024, 4096, 512, 1) : sdesc(b + s * 32, 16, 1024);
                 if (TS) {
                     mma_tf32_ts(tmem, tmem + 256 + s * 8, db, IDESC, (i | s) ? 1u : 0u);
                 } else {
@@ -54,19 +55,19 @@ __global__ void __launch_bounds__(128, 1) k_rate(int iters, unsigned long long* 
     }
 }
 
-template <int N, bool TS>
+template <int N, bool TS, bool BMN = false>
 void run(const char* name) {
     unsigned long long* d;
     cudaMalloc(&d, 8);
     const int smem = 16384 + 256 * 128 + 1024;
-    cudaFuncSetAttribute(k_rate<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_rate<N, TS, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 4096;
-    k_rate<N, TS><<<148, 128, smem>>>(16, d);
+    k_rate<N, TS, BMN><<<148, 128, smem>>>(16, d);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    k_rate<N, TS><<<148, 128, smem>>>(iters, d);
+    k_rate<N, TS, BMN><<<148, 128, smem>>>(iters, d);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -89,5 +90,9 @@ int main() {
     run<128, true>("TS (A from TMEM)");
     run<192, true>("TS (A from TMEM)");
     run<256, true>("TS (A from TMEM)");
+    run<64, true, true>("TS, B MN-major");
+    run<128, true, true>("TS, B MN-major");
+    run<64, false, true>("SS, B MN-major");
+    run<128, false, true>("SS, B MN-major");
     return 0;
 }
