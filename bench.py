@@ -151,9 +151,12 @@ def cpu_model():
     return "unknown"
 
 
-def epoch_batches(ds, n_needed, bs=1024, seed=0, rank=0, world=1):
-    """Full batches from successive epoch shuffles (runplan semantics); in weak
-    scaling each rank takes its own disjoint batches."""
+def epoch_batches(ds, n_needed, bs=1024, seed=0, rank=0, world=1, strong=False):
+    """Full batches from successive epoch shuffles (runplan semantics) with their
+    batch rng seeds (batch b of epoch e: batch_sample_seed(seed, e, b)).  Weak
+    scaling: rank r takes the epoch's batches b with b % world == r.  Strong
+    scaling: every rank walks the same global batches and takes its contiguous
+    shard (parallel.shard) of each."""
     from paper_2311_13225_b200 import runplan
     train = ds.train_ids()
     out, seeds = [], []
@@ -164,10 +167,13 @@ def epoch_batches(ds, n_needed, bs=1024, seed=0, rank=0, world=1):
         for b, x in enumerate(batches):
             if x.shape[0] != bs:
                 continue
-            if (b % world) != rank:
+            if strong:
+                from paper_2311_13225_b200.parallel import shard
+                x = shard(x, world, rank)
+            elif (b % world) != rank:
                 continue
             out.append(x)
-            seeds.append(runplan.batch_sample_seed(seed, epoch, b // world))
+            seeds.append(runplan.batch_sample_seed(seed, epoch, b))
             if len(out) >= n_needed:
                 break
         epoch += 1
@@ -202,6 +208,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phases", action="store_true", help="also report a per-phase time breakdown")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: 1024 seeds per rank per step (global 1024*N); strong: a fixed global batch of "
+                         "1024 split into N contiguous shards (the parity form, SURVEY §8(e))")
     ap.add_argument("--epoch-mode", default=None, metavar="SPEC",
                     help="extra measurement (not the driver's line): whole epochs through Trainer.run_epoch, "
                          "SPEC = 'c2:sage:hot=0.2:n=4' or 'c3:gcn:hot=0.2:n=4:fan=4,4:bs=10000'")
@@ -250,16 +259,22 @@ def main():
         else:
             assert [n for n, _ in segs] == ["start", "fwd0_gemm"], [n for n, _ in segs]
     K, W = args.steps, args.warmup
-    batches, rseeds = epoch_batches(ds, W + K, rank=rank, world=world)
+    strong = args.scaling == "strong"
+    batches, rseeds = epoch_batches(ds, W + K, rank=rank, world=world, strong=strong)
+    n_loc = int(batches[0].shape[0])  # seeds per rank per step (every shard of 1024 has the same size
+    if strong and any(b.shape[0] != n_loc for b in batches):  # when world divides 1024)
+        raise SystemExit("strong scaling needs equal shards (world must divide 1024)")
+    if dist_ctx:
+        dist_ctx.set_global_batch(1024 if strong else 1024 * world)
     # stage every step's inputs in HBM (value = device-resident inputs)
     d_seeds = torch.as_tensor(np.stack(batches).astype(np.int32), device=dev)
     bp = np.zeros((W + K, 8), dtype=np.int64)
     for i in range(W + K):
         bp[i, 0] = np.array([rseeds[i] & 0xFFFFFFFFFFFFFFFF], np.uint64).view(np.int64)[0]
-        bp[i, 1], bp[i, 2], bp[i, 3], bp[i, 4] = 1024, i, 0, -1
+        bp[i, 1], bp[i, 2], bp[i, 3], bp[i, 4] = n_loc, i, 0, -1
     d_bp = torch.as_tensor(bp, device=dev)
-    n_div = 1024 * world
-    d_counts = torch.tensor([1024, n_div], dtype=torch.int32, device=dev)
+    n_div = 1024 if strong else 1024 * world
+    d_counts = torch.tensor([n_loc, n_div], dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     ss, st = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     nset = len(e.sets)
@@ -274,7 +289,7 @@ def main():
             ss.wait_event(trained[k])
         with torch.cuda.stream(ss):
             s = e.sets[k]
-            s.seeds.copy_(d_seeds[i], non_blocking=True)
+            s.seeds[:n_loc].copy_(d_seeds[i], non_blocking=True)
             s.bp.copy_(d_bp[i], non_blocking=True)
             s.counts_in.copy_(d_counts, non_blocking=True)
             if split and early:  # instrumented: events bracket the bottom aggregation segment
@@ -358,7 +373,8 @@ def main():
     ms = t_start.elapsed_time(t_end)
     if dist_ctx:
         ms = dist_ctx.max_over_ranks(ms)
-    value = world * 1024 * K / (ms / 1000.0)
+    global_batch = 1024 if strong else 1024 * world
+    value = global_batch * K / (ms / 1000.0)
     agg_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]))
     # algorithmic bytes of the dominant kernel per launch:
     # unique src rows read + edge ids + per-dst metadata + [self | mean] rows written
@@ -366,7 +382,7 @@ def main():
     sizes = []
     e.cur = 0
     for i in range(min(K, 16)):
-        e.seeds.copy_(d_seeds[W + i])
+        e.seeds[:n_loc].copy_(d_seeds[W + i])
         e.bp.copy_(d_bp[W + i])
         e.counts_in.copy_(d_counts)
         e.enqueue_sample()  # full dedup of every layer (the step itself skips it for SAGE's bottom block)
@@ -376,7 +392,10 @@ def main():
         E0 = int(e.samplers[0].counts[:n_dst0].sum().item())
         sizes.append((n_dst0, n_src0, E0))
     n_dst0, n_src0, E0 = (float(np.mean([s[j] for s in sizes])) for j in range(3))
-    alg_bytes = n_src0 * F * 4 + E0 * 8 + n_dst0 * 12 + 2 * n_dst0 * F * 4
+    # SURVEY §8(d) "aggregate fwd" formula: unique source rows read (src prefix = dst) +
+    # the mean rows written, (n_src + n_dst) * F * 4, + edge ids (4 + 4) + offsets
+    alg_bytes = (n_src0 + n_dst0) * F * 4 + E0 * 8 + (n_dst0 + 1) * 8
+    self_copy_bytes = n_dst0 * F * 4  # SAGE self rows written for the GEMM (implementation choice)
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -421,7 +440,7 @@ def main():
     e2e_ms = max(e2e_event_ms, wall * 1000.0)
     if dist_ctx:
         e2e_ms = dist_ctx.max_over_ranks(e2e_ms)
-    e2e_value = world * 1024 * e2e_K / (e2e_ms / 1000.0)
+    e2e_value = global_batch * e2e_K / (e2e_ms / 1000.0)
     if not np.all(np.isfinite(losses)):
         raise SystemExit("non-finite loss in bench")
     phases = None
@@ -439,15 +458,17 @@ def main():
                               f"{cpu_model()}"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "ms_per_step_instrumented_serial": i_start.elapsed_time(i_end) / K,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "fp32", "data": "synthetic",
             "config": dict(WORKLOAD, parallelism=f"dp{world}" if world > 1 else "single",
                            l2_flush="inputs > L2: 0.96 GB feature table + 0.26 GB CSR, random rows per step",
-                           global_batch=1024 * world),
+                           global_batch=global_batch, seeds_per_rank=n_loc),
             "roofline": {"bound": "hbm", "kernel": "k_agg_fwd (bottom fused gather+mean, SAGE)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": agg_ms,
+                         "alg_bytes_formula": "SURVEY §8(d): (n_src0 + n_dst0)*F*4 + E0*8 + (n_dst0+1)*8",
+                         "extra_bytes_self_rows": self_copy_bytes,
                          "kernel_timing": "CUDA events on the kernel's stream over a second pass of the same steps "
                                           "with the sample and train halves back to back (the headline pass "
                                           "overlaps them)",
@@ -532,7 +553,7 @@ def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):
     tot = {n: 0.0 for n, _ in segs}
     e.cur = 0
     for r in range(reps):
-        e.seeds.copy_(d_seeds[i0 + r % d_seeds.shape[0]])
+        e.seeds[:d_seeds.shape[1]].copy_(d_seeds[i0 + r % d_seeds.shape[0]])
         e.bp.copy_(d_bp[i0 + r % d_bp.shape[0]])
         e.counts_in.copy_(d_counts)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(segs) + 1)]

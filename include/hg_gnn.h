@@ -172,11 +172,13 @@ int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const fl
                      const float* csc_w, void* stream);
 /* Transposed aggregation by deterministic fixed-point scatter (default path for
  * layers >= 1): dx[s] = mask(dself[s] (s < n_dst) + sum_e w_e dagg[dst_e]) with
- * the sum accumulated as int64 at scale 2^40 (order-independent, bit-exact
- * across runs) in acc_ws (int64 [cap_src x F], zero on first use, left zeroed);
+ * the sum accumulated in two-word fixed point (hi = v*2^20, lo = remainder*2^60, two
+ * int64 words; order-independent, bit-exact across runs, exact for every fp32
+ * contribution >= 2^-37) in acc_ws (int64 [cap_src x 2F]: a row's F hi words then its
+ * F lo words; zero on first use, left zeroed);
  * outdeg (required): sampled edges per local source (hg_dedup_relabel's outdeg);
  * sources s >= n_dst with outdeg 1 get their final row stored directly;
- * d_flags[0] |= 1 if a contribution is >= 2^20 or non-finite. */
+ * d_flags[0] |= 1 if a contribution is non-finite, |= 2 if outdeg * |v| >= 2^42. */
 int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself,
                              int32_t ld_dself, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
                              int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
@@ -189,7 +191,7 @@ int hg_aggregate_bwd_scatter(int32_t model, const float* dagg, int32_t ld_dagg, 
  * (W: the layer's flat [2K x C] weights) -> softmax-CE (loss into *d_loss, dlogits)
  * -> dself = dlogits W_self^T (into dself_out) -> dmean = dlogits W_neigh^T scattered
  * into the layer below exactly like hg_aggregate_bwd_scatter's scatter pass (fast path
- * into dx, else the fixed-point acc_ws of row stride F_acc); follow with
+ * into dx, else the two-word fixed-point acc_ws of row stride 2 * F_acc); follow with
  * hg_aggregate_bwd_finish.  row_ws: cap + 1 floats as hg_softmax_xent's. */
 int hg_sage_top_fused(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier, const int32_t* d_n,
                       int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
@@ -199,20 +201,6 @@ int hg_sage_top_fused(const float* hin, int32_t ld_in, int32_t K, const int32_t*
                       int32_t ld_dself, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
                       int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx, int32_t* d_flags, float* row_ws,
                       float* d_loss, void* stream);
-/* Middle SAGE layers (d_in, d_out <= 64, fanout <= 32), warp per destination, W = the
- * layer's flat [2K x N] weights: forward = mean of non-self neighbours (into agg_out) +
- * act([h_self | mean] W) (into out); backward = dself (into dself_out) and the
- * transposed scatter of w * (dz W_neigh^T) as hg_aggregate_bwd_scatter's scatter pass,
- * followed by hg_aggregate_bwd_finish. */
-int hg_sage_mid_fwd(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier, const int32_t* d_n,
-                    int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
-                    const int32_t* slot_local, const int32_t* nself, const float* W, int32_t N, int32_t act,
-                    float* out, int32_t ld_out, float* agg_out, int32_t ld_agg, void* stream);
-int hg_sage_mid_bwd(const float* dz, int32_t ld_dz, int32_t N, const int32_t* frontier, const int32_t* d_n,
-                    int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
-                    const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg, const float* W, int32_t K,
-                    float* dself_out, int32_t ld_dself, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
-                    int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx, int32_t* d_flags, void* stream);
 /* the finish pass of hg_aggregate_bwd_scatter alone (convert the fixed-point sums, add
  * dself for s < n_dst, ReLU' / injected-row masks, clear the accumulator) */
 int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int32_t F, const int32_t* d_n_dst, int32_t cap_dst,
@@ -273,13 +261,15 @@ int hg_wgrad_tc(const float* A1, int32_t lda1, const float* A2, int32_t lda2, in
                 int32_t ldg, int32_t N, const int32_t* d_M, int32_t M_cap, float* out1, float* out2, float* ws,
                 void* stream);
 
-/* Per-batch needed bottom rows (transfer.py:59-73; the batch CSV's raw_rows): distinct
- * sources of non-injected destinations + their self rows, added to
- * out[bp[3]]; tag_of: int32[V] (any initial contents below 0 / never equal to a
- * future reading_batch + 1), tag = bp[2] + 1. */
+/* Per-batch needed bottom rows (transfer.py:59-73, 87-115; the batch CSV's raw_rows and
+ * cache_hit_rows): distinct sources of non-injected destinations + their self rows;
+ * rows whose vertex is flagged in cached[V] (the case3/case4 static feature cache,
+ * nullable) are added to out_hits[bp[3]], the rest to out[bp[3]]; tag_of: int32[V]
+ * (any initial contents below 0 / never equal to a future reading_batch + 1),
+ * tag = bp[2] + 1. */
 int hg_count_needed_rows(const int32_t* frontier, const int32_t* d_n, int32_t cap, int32_t fanout,
                          const int32_t* counts, const int32_t* slots, const uint8_t* inj_mask, const int64_t* bp,
-                         int32_t* tag_of, int32_t* out, void* stream);
+                         const uint8_t* cached, int32_t* tag_of, int32_t* out, int32_t* out_hits, void* stream);
 
 /* ---- K9/K10 loss and updates (gnnmath.py:263-312; orchestrator.py:246-255) */
 /* dlogits = (softmax - onehot) / *d_div (d_div NULL: / n); *d_loss = mean CE over
@@ -335,6 +325,10 @@ int hg_inject_rows(const uint8_t* inj_mask, const int32_t* inj_slot, const int32
 /* ---- epoch planning helpers (orchestrator.py:200-229 queue replay) ------ */
 int hg_tag_vertices(const int32_t* ids, const int32_t* d_n, int32_t cap, int32_t* tag_of, int32_t tag,
                     void* stream);
+/* sample_khop_skip_hot hot flags (sampler.py:150-163: np.isin(bottom src, hot)):
+ * flags[i] = (tag_of[values[i]] == tag) for i < *d_n (or cap when d_n is NULL) */
+int hg_member_flags(const int32_t* values, const int32_t* d_n, int32_t cap, const int32_t* tag_of, int32_t tag,
+                    uint8_t* flags, void* stream);
 int64_t hg_filter_ws_size(int32_t n);
 int hg_filter_tagged(const int32_t* list, int32_t n, const int32_t* tag_of, int32_t tag, int32_t* out,
                      int32_t* d_n_out, int32_t* ws, void* stream);

@@ -513,6 +513,15 @@ class Store:
         self.cur, self.stg = {}, {}
         self.sb, self.w0, self.wlen = 0, int(window_start), self.n
 
+    def staged_count(self):  # store.py:132-134
+        return len(self.stg)
+
+    def live_entries(self):  # store.py:136-138
+        return len(self.cur) + len(self.stg)
+
+    def memory_bytes(self):  # store.py:140-142
+        return self.live_entries() * self.emb_dim * 8
+
 
 # ---------------------------------------------------------------------------
 # S4: planning — runplan.py:20-57, orchestrator.py:200-229

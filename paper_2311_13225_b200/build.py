@@ -44,17 +44,35 @@ def nvcc_path() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile csrc/*.cu -> libhg_gnn.so (skipped when up to date)."""
+    """Compile csrc/*.cu -> libhg_gnn.so (skipped when up to date): one object per
+    source, compiled in parallel, then one shared-library link."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    nvcc = nvcc_path()
+    odir = PKG / "build"
+    odir.mkdir(exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = odir / (src.stem + ".o")
+        cmd = [nvcc, *flags, "-c", "-I", str(CSRC), "-I", str(INCLUDE), "-o", str(obj), str(src)]
+        if verbose:
+            print(" ".join(cmd))
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        if proc.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src.name} ({proc.returncode}):\n{proc.stderr[-6000:]}")
+        return obj
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, srcs))
     tmp = LIB.with_suffix(".so.tmp%d" % os.getpid())
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", str(CSRC), "-I", str(INCLUDE), "-o", str(tmp),
-           *map(str, sources())]
-    if verbose:
-        print(" ".join(cmd))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", str(tmp),
+           *map(str, objs)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stderr[-6000:]}")
+        raise RuntimeError(f"nvcc link failed ({proc.returncode}):\n{proc.stderr[-6000:]}")
     os.replace(tmp, LIB)
     return LIB
 

@@ -545,21 +545,46 @@ extern "C" int hg_segment_weighted_rows_f64(const int64_t* edge_src, const int64
 // is associative, so the result is bit-identical for any execution order
 // (eager = graph replay = pipelined) with no sort and no src-major view: the
 // whole per-layer CSC build (radix sort + scans + bounds + weights, ~10
-// kernels) leaves the sampling graph.  Scale 2^40: resolution 9.1e-13, |sum| <
-// 2^23; a contribution >= 2^20 in magnitude (or non-finite) sets d_flags[0]
-// (checked by the host like the reference's non-finite guard,
-// gnnmath.py:100-102).  The finish pass converts, adds the SAGE self term,
-// applies the lower layer's ReLU' / injected-row masks, writes dx, and clears
-// the accumulator for the next step.
+// kernels) leaves the sampling graph.
+//
+// Two-word fixed point: a contribution v (fp32) is split exactly into
+// hi = round(v * 2^20) and lo = round((v - hi * 2^-20) * 2^60), accumulated in
+// two independent int64 words (the row's hi words, then its lo words: an
+// accumulator row is 2F words).  Range |sum| < 2^43, resolution 2^-60 (every
+// fp32 contribution >= 2^-37 in magnitude is represented exactly, smaller ones
+// to 2^-61 absolute), so the sum is the exact sum of the contributions up to
+// one final rounding, for any gradient scale that fp32 itself represents.
+// d_flags bit 0: a non-finite contribution (the reference's non-finite guard,
+// gnnmath.py:100-102); bit 1: outdeg(s) * |v| >= 2^42, i.e. the source's sum
+// could leave the accumulator's range (|v| of order 1e12 — a diverged run).
+// The finish pass converts, adds the SAGE self term, applies the lower
+// layer's ReLU' / injected-row masks, writes dx, and clears the accumulator
+// for the next step.
 // ---------------------------------------------------------------------------
 namespace {
-constexpr double FX_SCALE = 1099511627776.0;  // 2^40
-constexpr float FX_GUARD = 1048576.0f;        // 2^20
+constexpr double FX_HI = 1048576.0;                 // 2^20
+constexpr double FX_HI_INV = 1.0 / 1048576.0;
+constexpr double FX_LO = 1152921504606846976.0;     // 2^60
+constexpr double FX_LO_INV = 1.0 / 1152921504606846976.0;
+constexpr float FX_RANGE = 4398046511104.0f;        // 2^42: bound on outdeg * |v|
 
-__device__ __forceinline__ void fx_add(unsigned long long* p, float v, bool& bad) {
-    if (!(fabsf(v) < FX_GUARD)) bad = true;
-    const long long q = __double2ll_rn((double)v * FX_SCALE);
-    atomicAdd(p, (unsigned long long)q);
+// row = the source's accumulator row (2F words), k = column
+__device__ __forceinline__ void fx_add(unsigned long long* row, int F, int k, float v, int od, int& flags) {
+    if (!isfinite(v)) { flags |= 1; return; }
+    if (!(fabsf(v) * (float)od < FX_RANGE)) flags |= 2;
+    const double d = (double)v;
+    const long long hi = __double2ll_rn(d * FX_HI);
+    const long long lo = __double2ll_rn((d - (double)hi * FX_HI_INV) * FX_LO);
+    atomicAdd(row + k, (unsigned long long)hi);
+    if (lo) atomicAdd(row + F + k, (unsigned long long)lo);
+}
+
+__device__ __forceinline__ float fx_value(unsigned long long hi, unsigned long long lo) {
+    return (float)((double)(long long)hi * FX_HI_INV + (double)(long long)lo * FX_LO_INV);
+}
+
+__device__ __forceinline__ int finite_flag(float4 a) {
+    return (isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w)) ? 0 : 1;
 }
 
 // Sources s >= n_dst with exactly one incoming transposed edge (outdeg[s] == 1;
@@ -591,7 +616,7 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
     const int lr = lane & (LPR - 1);
     const int groups_per_block = blockDim.x / LPR;
     const int F = F4 * 4;
-    bool bad = false;
+    int bad = 0;
     // one lane group per SLOT (edge), not per destination: the ~f dependent
     // loads of a destination's edge loop (slot -> outdeg / mask -> store) run in
     // parallel across groups; the destination's dagg row is re-read per edge
@@ -627,27 +652,25 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
                 const int c = lr + k * LPR;
                 if (c < F4) {
                     float4 a = make_float4(w * x[k].x, w * x[k].y, w * x[k].z, w * x[k].w);
-                    if (!(fabsf(a.x) < FX_GUARD && fabsf(a.y) < FX_GUARD && fabsf(a.z) < FX_GUARD &&
-                          fabsf(a.w) < FX_GUARD))
-                        bad = true;
+                    bad |= finite_flag(a);
                     reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx)[c] = bwd_mask(a, hmask, ld_hmask, s, c, zero_row);
                 }
             }
             continue;
         }
-        unsigned long long* row = acc + (int64_t)s * F;
+        unsigned long long* row = acc + (int64_t)s * 2 * F;
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int c = lr + k * LPR;
             if (c < F4) {
-                fx_add(row + 4 * c + 0, w * x[k].x, bad);
-                fx_add(row + 4 * c + 1, w * x[k].y, bad);
-                fx_add(row + 4 * c + 2, w * x[k].z, bad);
-                fx_add(row + 4 * c + 3, w * x[k].w, bad);
+                fx_add(row, F, 4 * c + 0, w * x[k].x, od, bad);
+                fx_add(row, F, 4 * c + 1, w * x[k].y, od, bad);
+                fx_add(row, F, 4 * c + 2, w * x[k].z, od, bad);
+                fx_add(row, F, 4 * c + 3, w * x[k].w, od, bad);
             }
         }
     }
-    if (bad && d_flags) atomicOr(d_flags, 1);
+    if (bad && d_flags) atomicOr(d_flags, bad);
 }
 
 template <int LPR, int NV>
@@ -667,16 +690,17 @@ __global__ void __launch_bounds__(256) k_bwd_finish(
         if (s >= n_src) continue;
         if (s >= n_dst && outdeg[s] == 1) continue;  // written by the scatter's fast path
         const bool zero_row = inj && inj[s];
-        ulonglong4* arow = reinterpret_cast<ulonglong4*>(acc + (int64_t)s * F);
+        ulonglong4* arow = reinterpret_cast<ulonglong4*>(acc + (int64_t)s * 2 * F);
+        ulonglong4* lrow = arow + F4;
         float4* out = reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx);
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             const int c = lr + k * LPR;
             if (c >= F4) continue;
-            const ulonglong4 q = arow[c];
+            const ulonglong4 q = arow[c], r = lrow[c];
             arow[c] = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
-            float4 a = make_float4((float)((double)(long long)q.x / FX_SCALE), (float)((double)(long long)q.y / FX_SCALE),
-                                   (float)((double)(long long)q.z / FX_SCALE), (float)((double)(long long)q.w / FX_SCALE));
+            lrow[c] = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+            float4 a = make_float4(fx_value(q.x, r.x), fx_value(q.y, r.y), fx_value(q.z, r.z), fx_value(q.w, r.w));
             if (dself && s < n_dst) {  // dx[:n_dst] = dz W_self^T + scatter (gnnmath.py:195-199)
                 const float4 ds = __ldg(reinterpret_cast<const float4*>(dself + (int64_t)s * ld_dself) + c);
                 a.x = ds.x + a.x; a.y = ds.y + a.y; a.z = ds.z + a.z; a.w = ds.w + a.w;
@@ -794,7 +818,7 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
     const int nw = (gridDim.x * TOP_THREADS) >> 5;
     const float* Ws = sW;
     const float* Wn = sW + K * CS;
-    bool bad = false;
+    int bad = 0;
     for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
         const int y = labels[seeds ? seeds[i] : i];  // issued early: two dependent loads
         const int cnt = counts[i];
@@ -878,7 +902,7 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
         if (k1 < K) dself_out[(int64_t)i * ld_dself + k1] = ds1;
         // ---- transposed scatter of w * dmean into the layer below (as k_bwd_scatter)
         const float a0 = wd * dm0, a1 = wd * dm1;
-        if (cnt > 0 && !(fabsf(a0) < FX_GUARD && fabsf(a1) < FX_GUARD)) bad = true;
+        if (cnt > 0 && !(isfinite(a0) && isfinite(a1))) bad |= 1;
         for (int j0 = 0; j0 < cnt; j0 += 8) {  // 8 edges at a time: their masks load together
             int sj[8], od[8];
             float h0[8], h1[8];
@@ -901,15 +925,14 @@ __global__ void __launch_bounds__(TOP_THREADS) k_sage_top(
                     if (k0 < K) dx[(int64_t)sv * ld_dx + k0] = (zr[u] || !(h0[u] > 0.f)) ? 0.f : a0;
                     if (k1 < K) dx[(int64_t)sv * ld_dx + k1] = (zr[u] || !(h1[u] > 0.f)) ? 0.f : a1;
                 } else {
-                    unsigned long long* row = acc + (int64_t)sv * F_acc;
-                    bool b2 = false;
-                    if (k0 < K) fx_add(row + k0, a0, b2);
-                    if (k1 < K) fx_add(row + k1, a1, b2);
+                    unsigned long long* row = acc + (int64_t)sv * 2 * F_acc;
+                    if (k0 < K) fx_add(row, F_acc, k0, a0, od[u], bad);
+                    if (k1 < K) fx_add(row, F_acc, k1, a1, od[u], bad);
                 }
             }
         }
     }
-    if (bad && d_flags) atomicOr(d_flags, 1);
+    if (bad && d_flags) atomicOr(d_flags, bad);
     // ---- last block: fixed-order mean of the row losses (ticket in row_loss[cap])
     unsigned* ticket = reinterpret_cast<unsigned*>(row_loss + cap);
     __threadfence();
@@ -985,201 +1008,4 @@ extern "C" int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int
 #undef HG_FIN
     hg_set_error("aggregate_bwd_finish: unsupported width");
     return HG_EUNSUPPORTED;
-}
-
-// ---------------------------------------------------------------------------
-// Middle SAGE layers (0 < l < L-1, d_in, d_out <= 64, fanout <= 32), one warp per
-// destination row, W_l = [W_self; W_neigh] in shared memory:
-//   k_sage_mid_fwd: mean of the non-self neighbours + h = ReLU([self | mean] W)
-//                   (gnnmath.py:157-178; replaces aggregate + GEMM launches)
-//   k_sage_mid_bwd: dself = dz W_self^T, dmean = dz W_neigh^T and the transposed
-//                   scatter of w * dmean (gnnmath.py:194-199; replaces dX GEMM +
-//                   scatter), followed by hg_aggregate_bwd_finish.
-// ---------------------------------------------------------------------------
-namespace {
-__global__ void __launch_bounds__(TOP_THREADS) k_sage_mid_fwd(
-    const float* __restrict__ hin, int ld_in, int K, const int* __restrict__ frontier, const int* d_n, int cap, int f,
-    const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
-    const int* __restrict__ nself, const float* __restrict__ W, int N, int act, float* __restrict__ out, int ld_out,
-    float* __restrict__ agg_out, int ld_agg) {
-    hg_pdl_begin();
-    extern __shared__ float sW[];
-    // row stride NS = N | 1 (odd): the backward's column walks (fixed c, lane = k) are
-    // then bank-conflict free
-    const int NS = N | 1;
-    stage_w(sW, W, 2 * K, N, NS);
-    __syncthreads();
-    const int n = hg_load_count(d_n, cap);
-    const int lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * TOP_THREADS) >> 5;
-    const float* Ws = sW;
-    const float* Wn = sW + K * NS;
-    const int k0 = lane, k1 = lane + 32;
-    const int c0 = lane, c1 = lane + 32;
-    const int cc0 = c0 < N ? c0 : 0, cc1 = c1 < N ? c1 : 0;
-    for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
-        const int cnt = counts[i];
-        const int v = frontier[i];
-        const int ns = nself[i];
-        const float wd = ns > 0 ? 1.0f / (float)ns : 0.f;
-        const int64_t sb = (int64_t)i * f;
-        const float s0 = k0 < K ? hin[(int64_t)i * ld_in + k0] : 0.f;
-        const float s1 = k1 < K ? hin[(int64_t)i * ld_in + k1] : 0.f;
-        int my_s = -1;
-        if (lane < cnt) {
-            my_s = slot_local[sb + lane];
-            if (slot_g[sb + lane] == v) my_s = -1;  // SAGE drops self edges (gnnmath.py:148)
-        }
-        float m0 = 0.f, m1 = 0.f;
-        for (int j0 = 0; j0 < cnt; j0 += 8) {
-            float x0[8], x1[8];
-            int sj[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                sj[u] = __shfl_sync(0xffffffffu, my_s, (j0 + u) & 31);
-                if (j0 + u >= cnt) sj[u] = -1;
-                x0[u] = (sj[u] >= 0 && k0 < K) ? hin[(int64_t)sj[u] * ld_in + k0] : 0.f;
-                x1[u] = (sj[u] >= 0 && k1 < K) ? hin[(int64_t)sj[u] * ld_in + k1] : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (sj[u] >= 0) { m0 = fmaf(wd, x0[u], m0); m1 = fmaf(wd, x1[u], m1); }
-        }
-        if (k0 < K) agg_out[(int64_t)i * ld_agg + k0] = m0;
-        if (k1 < K) agg_out[(int64_t)i * ld_agg + k1] = m1;
-        float z0 = 0.f, z1 = 0.f;
-#pragma unroll 8
-        for (int k = 0; k < K; ++k) {
-            const float a = __shfl_sync(0xffffffffu, k < 32 ? s0 : s1, k & 31);
-            z0 = fmaf(a, Ws[k * NS + cc0], z0);
-            z1 = fmaf(a, Ws[k * NS + cc1], z1);
-        }
-#pragma unroll 8
-        for (int k = 0; k < K; ++k) {
-            const float b = __shfl_sync(0xffffffffu, k < 32 ? m0 : m1, k & 31);
-            z0 = fmaf(b, Wn[k * NS + cc0], z0);
-            z1 = fmaf(b, Wn[k * NS + cc1], z1);
-        }
-        if (c0 < N) out[(int64_t)i * ld_out + c0] = act ? fmaxf(z0, 0.f) : z0;
-        if (c1 < N) out[(int64_t)i * ld_out + c1] = act ? fmaxf(z1, 0.f) : z1;
-    }
-}
-
-__global__ void __launch_bounds__(TOP_THREADS) k_sage_mid_bwd(
-    const float* __restrict__ dz, int ld_dz, int N, const int* __restrict__ frontier, const int* d_n, int cap, int f,
-    const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
-    const int* __restrict__ nself, const int* __restrict__ outdeg, const float* __restrict__ W, int K,
-    float* __restrict__ dself_out, int ld_dself, const float* __restrict__ hmask, int ld_hmask,
-    const uint8_t* __restrict__ inj, unsigned long long* __restrict__ acc, int F_acc, float* __restrict__ dx,
-    int ld_dx, int* __restrict__ d_flags) {
-    hg_pdl_begin();
-    extern __shared__ float sW[];
-    // row stride NS = N | 1 (odd): the backward's column walks (fixed c, lane = k) are
-    // then bank-conflict free
-    const int NS = N | 1;
-    stage_w(sW, W, 2 * K, N, NS);
-    __syncthreads();
-    const int n = hg_load_count(d_n, cap);
-    const int lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * TOP_THREADS) >> 5;
-    const float* Ws = sW;
-    const float* Wn = sW + K * NS;
-    const int k0 = lane, k1 = lane + 32;
-    const int kk0 = k0 < K ? k0 : 0, kk1 = k1 < K ? k1 : 0;
-    bool bad = false;
-    for (int i = (blockIdx.x * TOP_THREADS + threadIdx.x) >> 5; i < n; i += nw) {
-        const int cnt = counts[i];
-        const int v = frontier[i];
-        const int ns = nself[i];
-        const float wd = ns > 0 ? 1.0f / (float)ns : 0.f;
-        const int64_t sb = (int64_t)i * f;
-        int my_s = -1, my_od = 0;
-        if (lane < cnt) {
-            my_s = slot_local[sb + lane];
-            if (slot_g[sb + lane] == v) my_s = -1;
-            else my_od = outdeg[my_s];
-        }
-        const float g0 = lane < N ? dz[(int64_t)i * ld_dz + lane] : 0.f;
-        const float g1 = lane + 32 < N ? dz[(int64_t)i * ld_dz + lane + 32] : 0.f;
-        float ds0 = 0.f, ds1 = 0.f, dm0 = 0.f, dm1 = 0.f;
-#pragma unroll 8
-        for (int c = 0; c < N; ++c) {
-            const float g = __shfl_sync(0xffffffffu, c < 32 ? g0 : g1, c & 31);
-            ds0 = fmaf(g, Ws[kk0 * NS + c], ds0);
-            dm0 = fmaf(g, Wn[kk0 * NS + c], dm0);
-            ds1 = fmaf(g, Ws[kk1 * NS + c], ds1);
-            dm1 = fmaf(g, Wn[kk1 * NS + c], dm1);
-        }
-        if (k0 < K) dself_out[(int64_t)i * ld_dself + k0] = ds0;
-        if (k1 < K) dself_out[(int64_t)i * ld_dself + k1] = ds1;
-        const float a0 = wd * dm0, a1 = wd * dm1;
-        if (cnt > 0 && !(fabsf(a0) < FX_GUARD && fabsf(a1) < FX_GUARD)) bad = true;
-        for (int j0 = 0; j0 < cnt; j0 += 8) {
-            int sj[8], od[8];
-            float h0[8], h1[8];
-            bool zr[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                sj[u] = __shfl_sync(0xffffffffu, my_s, (j0 + u) & 31);
-                od[u] = __shfl_sync(0xffffffffu, my_od, (j0 + u) & 31);
-                if (j0 + u >= cnt) sj[u] = -1;
-                const bool fast = sj[u] >= n && od[u] == 1;
-                h0[u] = (fast && hmask && k0 < K) ? hmask[(int64_t)sj[u] * ld_hmask + k0] : 1.f;
-                h1[u] = (fast && hmask && k1 < K) ? hmask[(int64_t)sj[u] * ld_hmask + k1] : 1.f;
-                zr[u] = fast && inj && inj[sj[u]];
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int sv = sj[u];
-                if (sv < 0) continue;
-                if (sv >= n && od[u] == 1) {
-                    if (k0 < K) dx[(int64_t)sv * ld_dx + k0] = (zr[u] || !(h0[u] > 0.f)) ? 0.f : a0;
-                    if (k1 < K) dx[(int64_t)sv * ld_dx + k1] = (zr[u] || !(h1[u] > 0.f)) ? 0.f : a1;
-                } else {
-                    unsigned long long* row = acc + (int64_t)sv * F_acc;
-                    bool b2 = false;
-                    if (k0 < K) fx_add(row + k0, a0, b2);
-                    if (k1 < K) fx_add(row + k1, a1, b2);
-                }
-            }
-        }
-    }
-    if (bad && d_flags) atomicOr(d_flags, 1);
-}
-}  // namespace
-
-extern "C" int hg_sage_mid_fwd(const float* hin, int32_t ld_in, int32_t K, const int32_t* frontier,
-                               const int32_t* d_n, int32_t cap, int32_t fanout, const int32_t* counts,
-                               const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself, const float* W,
-                               int32_t N, int32_t act, float* out, int32_t ld_out, float* agg_out, int32_t ld_agg,
-                               void* stream) {
-    if (K < 1 || K > 64 || N < 1 || N > 64 || fanout > 32) {
-        hg_set_error("sage_mid_fwd: needs d_in, d_out in [1, 64] and fanout <= 32");
-        return HG_EUNSUPPORTED;
-    }
-    if (cap <= 0) return HG_OK;
-    int grid = hg_ceil_div(cap, TOP_THREADS / 32);
-    grid = grid < 4 * HG_NUM_SMS ? grid : 4 * HG_NUM_SMS;
-    hg_launch(k_sage_mid_fwd, dim3(grid), dim3(TOP_THREADS), (size_t)(2 * K * (N | 1) * 4), (cudaStream_t)stream, hin, ld_in,
-              K, frontier, d_n, cap, fanout, counts, slot_g, slot_local, nself, W, N, act, out, ld_out, agg_out, ld_agg);
-    return hg_check_launch("sage_mid_fwd");
-}
-
-extern "C" int hg_sage_mid_bwd(const float* dz, int32_t ld_dz, int32_t N, const int32_t* frontier, const int32_t* d_n,
-                               int32_t cap, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
-                               const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg, const float* W,
-                               int32_t K, float* dself_out, int32_t ld_dself, const float* hmask, int32_t ld_hmask,
-                               const uint8_t* inj_mask, int64_t* acc_ws, int32_t F_acc, float* dx, int32_t ld_dx,
-                               int32_t* d_flags, void* stream) {
-    if (K < 1 || K > 64 || N < 1 || N > 64 || fanout > 32) {
-        hg_set_error("sage_mid_bwd: needs d_in, d_out in [1, 64] and fanout <= 32");
-        return HG_EUNSUPPORTED;
-    }
-    if (cap <= 0) return HG_OK;
-    int grid = hg_ceil_div(cap, TOP_THREADS / 32);
-    grid = grid < 4 * HG_NUM_SMS ? grid : 4 * HG_NUM_SMS;
-    hg_launch(k_sage_mid_bwd, dim3(grid), dim3(TOP_THREADS), (size_t)(2 * K * (N | 1) * 4), (cudaStream_t)stream, dz, ld_dz,
-              N, frontier, d_n, cap, fanout, counts, slot_g, slot_local, nself, outdeg, W, K, dself_out, ld_dself,
-              hmask, ld_hmask, inj_mask, reinterpret_cast<unsigned long long*>(acc_ws), F_acc, dx, ld_dx, d_flags);
-    return hg_check_launch("sage_mid_bwd");
 }

@@ -199,12 +199,17 @@ __global__ void k_store_lookup(const int* __restrict__ dst, const int* d_n, int 
             const int slot = slot_of[v];
             if (slot >= 0 && stamp[slot] == cur_stamp) {
                 const int gap = rb - ver[slot];
-                if (gap > gap_bound) ++viol;  // StalenessViolation (store.py:85-92)
-                ++hits;
-                m = 1;
-                inj_slot[i] = slot;
-                const unsigned long long key = ((unsigned long long)(unsigned)gap << 32) | (0xffffffffu - (unsigned)rb);
-                best = best > key ? best : key;
+                if (gap > gap_bound) {
+                    // StalenessViolation (store.py:85-92): counted, never injected — the
+                    // row is computed from features; the host raises at the next check
+                    ++viol;
+                } else {
+                    ++hits;
+                    m = 1;
+                    inj_slot[i] = slot;
+                    const unsigned long long key = ((unsigned long long)(unsigned)gap << 32) | (0xffffffffu - (unsigned)rb);
+                    best = best > key ? best : key;
+                }
             } else {
                 ++miss;
             }
@@ -254,6 +259,14 @@ __global__ void k_inject(const uint8_t* __restrict__ inj_mask, const int* __rest
 __global__ void k_tag(const int* __restrict__ ids, const int* d_n, int cap, int* __restrict__ tag_of, int tag) {
     const int n = hg_load_count(d_n, cap);
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) tag_of[ids[k]] = tag;
+}
+
+// sample_khop_skip_hot (sampler.py:150-163): flags[i] = values[i] is in the tagged set
+__global__ void k_member_flags(const int* __restrict__ values, const int* d_n, int cap, const int* __restrict__ tag_of,
+                               int tag, uint8_t* __restrict__ flags) {
+    const int n = hg_load_count(d_n, cap);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        flags[k] = tag_of[values[k]] == tag;
 }
 
 __global__ void k_filter_flags(const int* __restrict__ list, int n, const int* __restrict__ tag_of, int tag,
@@ -399,6 +412,13 @@ extern "C" int hg_tag_vertices(const int32_t* ids, const int32_t* d_n, int32_t c
     return hg_check_launch("tag_vertices");
 }
 
+extern "C" int hg_member_flags(const int32_t* values, const int32_t* d_n, int32_t cap, const int32_t* tag_of,
+                               int32_t tag, uint8_t* flags, void* stream) {
+    if (cap <= 0) return HG_OK;
+    k_member_flags<<<hg_grid(cap, 256, 8), 256, 0, (cudaStream_t)stream>>>(values, d_n, cap, tag_of, tag, flags);
+    return hg_check_launch("member_flags");
+}
+
 extern "C" int64_t hg_filter_ws_size(int32_t n) { return (int64_t)(n + (long long)hg_scan_ws_ints(n) + 16); }
 
 // out = [x for x in list if tag_of[x] == tag], order kept; *d_n_out = count
@@ -449,12 +469,13 @@ namespace {
 __global__ void __launch_bounds__(256) k_count_needed(const int* __restrict__ frontier, const int* d_n, int cap, int f,
                                                       const int* __restrict__ counts, const int* __restrict__ slots,
                                                       const uint8_t* __restrict__ inj, const int64_t* __restrict__ bp,
-                                                      int* __restrict__ tag_of, int* __restrict__ out) {
+                                                      const uint8_t* __restrict__ cached, int* __restrict__ tag_of,
+                                                      int* __restrict__ out, int* __restrict__ out_hits) {
     hg_pdl_begin();
     const int n = hg_load_count(d_n, cap);
     const int tag = (int)bp[BP_READING_BATCH] + 1;
     const long long Q = (long long)n * (f + 1);
-    int c = 0;
+    int c = 0, h = 0;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Q; q += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(q / (f + 1)), j = (int)(q - (long long)i * (f + 1));
         if (inj && inj[i]) continue;  // injected destination: nothing of it is computed
@@ -462,19 +483,31 @@ __global__ void __launch_bounds__(256) k_count_needed(const int* __restrict__ fr
         if (j == f) v = frontier[i];  // the destination's own self row
         else if (j < counts[i]) v = slots[(int64_t)i * f + j];
         else continue;
-        if (atomicExch(&tag_of[v], tag) != tag) ++c;
+        if (atomicExch(&tag_of[v], tag) != tag) {
+            // a needed row is a raw transfer unless it sits in the static feature
+            // cache (transfer.py:103-114, cache_hit_rows)
+            if (cached && cached[v]) ++h;
+            else ++c;
+        }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&out[(int)bp[BP_BATCH_IN_EPOCH]], c);
+    for (int o = 16; o; o >>= 1) {
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+        h += __shfl_xor_sync(0xffffffffu, h, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (c) atomicAdd(&out[(int)bp[BP_BATCH_IN_EPOCH]], c);
+        if (h && out_hits) atomicAdd(&out_hits[(int)bp[BP_BATCH_IN_EPOCH]], h);
+    }
 }
 }  // namespace
 
 extern "C" int hg_count_needed_rows(const int32_t* frontier, const int32_t* d_n, int32_t cap, int32_t fanout,
                                     const int32_t* counts, const int32_t* slots, const uint8_t* inj_mask,
-                                    const int64_t* bp, int32_t* tag_of, int32_t* out, void* stream) {
+                                    const int64_t* bp, const uint8_t* cached, int32_t* tag_of, int32_t* out,
+                                    int32_t* out_hits, void* stream) {
     if (cap <= 0) return HG_OK;
     hg_launch(k_count_needed, hg_grid((long long)cap * (fanout + 1), 256, 8), 256, 0, (cudaStream_t)stream, frontier,
-              d_n, cap, fanout, counts, slots, inj_mask, bp, tag_of, out);
+              d_n, cap, fanout, counts, slots, inj_mask, bp, cached, tag_of, out, out_hits);
     return hg_check_launch("count_needed_rows");
 }

@@ -38,6 +38,9 @@ SPECS = {
     "c2": dict(V=2_400_000, avg_deg=26.0, exponent=2.5, max_deg=150_000, F=100, C=47),
     # C3: Reddit-shaped (233K V, ~114M entries, 602-dim, 41 classes)
     "c3": dict(V=233_000, avg_deg=489.0, exponent=2.5, max_deg=21_000, F=602, C=41),
+    # learnable C2-shaped graph for accuracy parity (class means + noise, graph.py:336-340
+    # style; the signal is weak enough that test accuracy does not saturate)
+    "c2learn": dict(V=240_000, avg_deg=26.0, exponent=2.5, max_deg=47_000, F=100, C=47, signal=0.3),
     # small learnable variant for accuracy parity (weak signal; does not saturate)
     "learn": dict(V=20_000, avg_deg=12.0, exponent=2.5, max_deg=2_000, F=64, C=8,
                   signal=0.35),
@@ -189,3 +192,14 @@ def make_dataset(name: str, seed: int = 7, scale: float = 1.0,
         save_binary(tmp, ds)
         os.replace(tmp, cache)
     return ds
+
+
+def limit_train(ds: Dataset, n: int) -> Dataset:
+    """The same graph and vertex data with the training mask cut to its first ``n``
+    vertices in id order (bounded-size parity runs at full graph scale)."""
+    ids = np.nonzero(ds.train_mask)[0][:int(n)]
+    train = np.zeros_like(ds.train_mask)
+    train[ids] = True
+    return Dataset(name=f"{ds.name}-train{int(n)}", offsets=ds.offsets, targets=ds.targets,
+                   features=ds.features, labels=ds.labels, train_mask=train, val_mask=ds.val_mask,
+                   test_mask=ds.test_mask, meta=dict(ds.meta, train_limit=int(n)))

@@ -248,7 +248,8 @@ class TrainEngine:
         ws = max(dense.wgrad_ws_size(self.dims[l], self.dims[l + 1], self.cap_dst[l], 2 if self.sage else 1)
                  for l in range(self.L))
         self.wgrad_ws = zf(max(ws, 1))
-        self.fx_acc = [torch.zeros((self.cap_src[l], self.ld[l]), dtype=torch.int64, device=dev)
+        # two-word fixed-point accumulators (hi | lo words per row, hg_aggregate.cu)
+        self.fx_acc = [torch.zeros((self.cap_src[l], 2 * self.ld[l]), dtype=torch.int64, device=dev)
                        if (l > 0 and self.bwd_scatter) else None for l in range(self.L)]
         self.fx_flags = z32(1)
         self.d_loss = zf(1)
@@ -259,6 +260,8 @@ class TrainEngine:
         # per-batch needed bottom rows (the reference's transfer accounting,
         # transfer.py:59-73) on a side branch of the train half
         self.raw_rows_arr = z32(max(max_batches, 1))
+        self.cache_hit_arr = z32(max(max_batches, 1))
+        self.static_cached = None  # uint8 [V]: the case3/case4 static feature cache (accounting only)
         self.account_rows = True  # TrainConfig.report_transfers
         self.need_tag = torch.full((max(V, 1),), -1, dtype=torch.int32, device=dev)
         self.side = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
@@ -282,12 +285,6 @@ class TrainEngine:
         self.top_fused = (self.sage and self.L >= 2 and self.bwd_scatter and self.dims[self.L - 1] <= 64
                           and self.dims[self.L] <= 64 and self.fan[self.L - 1] <= 32
                           and self.fused_dx[self.L - 1] and os.environ.get("HG_TOP_FUSED", "1") != "0")
-        # middle SAGE layers: aggregate + transform, and dX + scatter, as one kernel each
-        # (off by default: measured slower than aggregate + TMA GEMM at ~6K rows — a warp-per-row
-        # SIMT transform cannot keep enough rows in flight per SM; HG_MID_FUSED=1 enables it)
-        mid_ok = os.environ.get("HG_MID_FUSED", "0") == "1" and self.sage and self.bwd_scatter
-        self.mid_fused = [mid_ok and 0 < l < self.L - 1 and self.dims[l] <= 64 and self.dims[l + 1] <= 64
-                          and self.fan[l] <= 32 and self.fused_dx[l] for l in range(self.L)]
         self.graph = None
         self.g_sample = None
         self.g_train = None
@@ -443,11 +440,6 @@ class TrainEngine:
             mark("fwd0_agg" if l == 0 else "fwd_upper" if l == 1 else "")
             sb0, ag0 = self._bottom_bufs()
             agg_l = ag0 if l == 0 else self.agg[l]
-            if self.mid_fused[l]:  # aggregate + transform + ReLU in one kernel
-                _lib.call("hg_sage_mid_fwd", ptr(hin), ld_in, d_in, ptr(fr), ptr(n), self.cap_dst[l], self.fan[l],
-                          ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local), ptr(smp.nself), ptr(P.view(l, 0)),
-                          d_out, 1 if l < L - 1 else 0, ptr(self.out[l]), self.ld[l + 1], ptr(agg_l), self.ld[l], s)
-                continue
             if l == 0:
                 if not self.early_agg0():
                     self._enqueue_agg0(s, inj)
@@ -509,13 +501,7 @@ class TrainEngine:
                             ptr(n), self.cap_dst[l], ptr(P.view(l, 0, P.grad)), None, ptr(self.wgrad_ws), ws_)
             if l == 0:
                 continue
-            if self.mid_fused[l]:  # dself + scatter of dmean in one kernel, then the finish pass
-                _lib.call("hg_sage_mid_bwd", ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(fr), ptr(n), self.cap_dst[l],
-                          self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local), ptr(smp.nself),
-                          ptr(smp.outdeg), ptr(P.view(l, 0)), d_in, ptr(self.dcat[l]), 2 * d_in, ptr(self.out[l - 1]),
-                          self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), self.ld[l],
-                          ptr(self.dz[l - 1]), self.ld[l], ptr(self.fx_flags), s)
-            if (l == L - 1 and self.top_fused) or self.mid_fused[l]:  # dX + scatter already ran
+            if l == L - 1 and self.top_fused:  # dX + scatter already ran in the fused top kernel
                 _lib.call("hg_aggregate_bwd_finish", ptr(self.dcat[l]), 2 * self.dims[l], self.ld[l], ptr(n),
                           self.cap_dst[l], ptr(smp.n_src), self.cap_src[l], ptr(smp.outdeg), ptr(self.out[l - 1]),
                           self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), ptr(self.dz[l - 1]),
@@ -553,7 +539,8 @@ class TrainEngine:
             fr0, n0 = self.frontier(0)
             smp0 = self.samplers[0]
             _lib.call("hg_count_needed_rows", ptr(fr0), ptr(n0), self.cap_dst[0], self.fan[0], ptr(smp0.counts),
-                      ptr(smp0.slots), ptr(inj), ptr(self.bp), ptr(self.need_tag), ptr(self.raw_rows_arr), s)
+                      ptr(smp0.slots), ptr(inj), ptr(self.bp), ptr(self.static_cached), ptr(self.need_tag),
+                      ptr(self.raw_rows_arr), ptr(self.cache_hit_arr), s)
         # ---------------- update ----------------
         mark("update")
         if self.allreduce is not None:
@@ -673,10 +660,14 @@ class TrainEngine:
 
     def check_numerics(self):
         """Raise like the reference's non-finite guard (gnnmath.py:100-102) if a
-        backward scatter saw a non-finite or out-of-range (>= 2^20) value."""
-        if int(self.fx_flags.item()):
+        backward scatter saw a non-finite value (flag bit 0), or a contribution
+        outdeg * |v| >= 2^42 that the fixed-point accumulator cannot hold (bit 1)."""
+        f = int(self.fx_flags.item())
+        if f:
             self.fx_flags.zero_()
-            raise FloatingPointError("non-finite or out-of-range gradient in the transposed aggregation")
+            if f & 1:
+                raise FloatingPointError("non-finite gradient in the transposed aggregation")
+            raise FloatingPointError("gradient magnitude beyond the fixed-point accumulator range (2^42)")
 
     def _save_state(self):
         st = {"flat": self.params.flat.clone(), "md": self.d_maxdelta.clone(),
@@ -695,6 +686,7 @@ class TrainEngine:
         self.fx_flags.zero_()  # the warm-up ran on unfed (empty) sample sets
         self.need_tag.fill_(-1)  # ... and tagged vertices for the row accounting
         self.raw_rows_arr.zero_()
+        self.cache_hit_arr.zero_()
         self.d_maxdelta.copy_(st["md"])
         self.loss_arr.copy_(st["loss"])
         self.md_arr.copy_(st["mdarr"])

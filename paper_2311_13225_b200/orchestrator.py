@@ -36,6 +36,10 @@ from .store import FallbackBudgetExceeded, StalenessViolation
 
 EXECUTIONS = ("serial", "pipelined")
 STRATEGIES = ("case1", "case2", "case3", "case4", "layer-based")  # skeletons.STRATEGIES
+#: the static feature cache budget of the cached-gather baselines case3/case4
+#: (orchestrator.py:345-356): presets.paper_like_preset().cache_budget_bytes (presets.py:58)
+STATIC_CACHE_BUDGET_BYTES = 2.0e5
+REAL_SIZE = 8  # transfer.py accounting unit (8-byte reals)
 
 
 class ConfigError(ValueError):
@@ -62,7 +66,12 @@ class TrainConfig:
     execution: str = "serial"
     stage_budget_frac: float = 1.0
     max_fallback_frac: float = 0.5
-    simulate_costs: bool = False  # accepted for compatibility; the simulator is out of scope
+    # The reference's discrete-event cost simulator (devsim/presets, orchestrator.py:570-575,
+    # 621-637) is out of scope: its only effect on training is the idle-time feedback that
+    # moves hot vertices from "compute" to "feature cache".  Only simulate_costs=False
+    # (the reference's numerics with zero idle time) is accepted; True or a preset raise
+    # ConfigError instead of being silently ignored.
+    simulate_costs: bool = False
     preset: object = None
     use_graph: bool = True  # replay each step as one captured CUDA graph
     report_transfers: bool = True  # per-batch needed-row accounting for the batch CSV (transfer.py:59-73)
@@ -92,6 +101,11 @@ class TrainConfig:
             raise ConfigError(f"epochs must be >= 1, got {self.epochs}")
         if not (0.0 < self.stage_budget_frac <= 1.0):
             raise ConfigError("stage budget fraction must be in (0, 1]")
+        if self.simulate_costs:
+            raise ConfigError("simulate_costs=True needs the reference's device simulator, which this "
+                              "implementation does not provide (use simulate_costs=False)")
+        if self.preset is not None:
+            raise ConfigError("device presets belong to the reference's simulator and are not supported")
 
     def dims(self, feat_dim: int, num_classes: int) -> list:
         return [feat_dim] + [self.hidden_dim] * (self.layers - 1) + [num_classes]
@@ -215,6 +229,11 @@ class Trainer:
                                   optimizer=config.optimizer, weights=weights, max_batches=n_batches,
                                   allreduce=dist.allreduce if dist is not None else None)
         self.engine.account_rows = bool(config.report_transfers)
+        self.static_cache = self._static_cache()
+        if self.static_cache.size:
+            flags = torch.zeros(self.dg.num_vertices, dtype=torch.uint8, device=self.dg.device)
+            flags[torch.as_tensor(self.static_cache, device=self.dg.device)] = 1
+            self.engine.static_cached = flags
         self.version = 0
         # ---- hot list (hotness.py:70-108 via orchestrator.py:692-702) ----
         if hot_list is None:
@@ -242,6 +261,22 @@ class Trainer:
         self.batch_to_group = {}
         if config.use_graph:
             self.engine.capture()
+
+    def _static_cache(self) -> np.ndarray:
+        """The top-degree vertices of the case3/case4 static feature cache
+        (orchestrator.py:345-356; accounting only: they only move rows from the
+        batch CSV's raw_rows to cache_hit_rows)."""
+        cfg = self.cfg
+        if cfg.strategy not in ("case3", "case4"):
+            return np.empty(0, np.int64)
+        budget = STATIC_CACHE_BUDGET_BYTES
+        if cfg.strategy == "case4":
+            budget = max(0.0, budget - (self.dg.num_vertices + 1 + self.dg.num_edges) * 8.0)
+        k = int(budget // (self.dg.feat_dim * REAL_SIZE))
+        if k <= 0:
+            return np.empty(0, np.int64)
+        deg = np.diff(np.asarray(self.ds.offsets))
+        return np.argsort(-deg, kind="stable")[:k].astype(np.int64)
 
     # ------------------------------------------------------------------
     def _new_tag(self):
@@ -300,6 +335,7 @@ class Trainer:
         if hot is not None:
             hot.reset_counters()
         e.raw_rows_arr.zero_()
+        e.cache_hit_arr.zero_()
         if self.use_hot and self.producer is None:
             cap = max([plan.queue_sizes.get(g, 0) for g in plan.queue_sizes] + [1])
             cap = (cap + cfg.super_batch_n - 1) // cfg.super_batch_n
@@ -333,13 +369,17 @@ class Trainer:
                                   chunk=chunk, warm=1 if (self.layer_based and g == 0 and self.hot_list.size) else 0))
         pipe = self.pipeline
         state = {"prod_done": None}
+        # data parallel: rank r trains the contiguous shard r of every
+        # global batch; dlogits are scaled by 1/|global batch| so the all-reduced sum
+        # is the union batch's gradient
+        local = [self._local_seeds(bt) for bt in plan.batches]
 
         def feed_fn(it):
-            seeds = plan.batches[it["b"]]
+            seeds = local[it["b"]]
+            n_div = int(plan.batches[it["b"]].shape[0]) if self.dist else None
             return lambda set_index: self.feeder.feed(
                 seeds, plan.batch_seeds[it["b"]], it["gb"], it["b"], cpu_tag=it["cpu_tag"], table_sel=it["g"] % 2,
-                cur_stamp=stamps[it["g"]], warm=it["warm"],
-                n_div=self.dist.global_batch(seeds) if self.dist else None, set_index=set_index)
+                cur_stamp=stamps[it["g"]], warm=it["warm"], n_div=n_div, set_index=set_index)
 
         def before_fn(it):
             def before(stream):
@@ -368,6 +408,22 @@ class Trainer:
                     rep.stage_events.append((g + 1, it["gb"], c))
             return before
 
+        # staleness (store.py:85-92): a violating lookup is never injected (the row is
+        # computed from features) and is counted on the device; the count is copied to
+        # pinned memory at every super-batch boundary and checked as soon as the copy
+        # has landed (non-blocking), so a violation raises within a super-batch
+        watch = []
+
+        def poll(block=False):
+            while watch and (block or watch[0][0].query()):
+                ev, pin = watch.pop(0)
+                ev.synchronize()
+                if int(pin[0]):
+                    pipe.drain()
+                    torch.cuda.synchronize(dev)
+                    raise StalenessViolation(f"{int(pin[0])} reuse events exceeded the 2n-1 version gap bound "
+                                             f"{hot.gap_bound} (epoch {plan.epoch})")
+
         if sched:
             pipe.sample(0, feed_fn(sched[0]))
         for k, it in enumerate(sched):
@@ -380,16 +436,34 @@ class Trainer:
                 ev = torch.cuda.Event()
                 ev.record(self.prod_stream)
                 state["prod_done"] = ev
+            if it["last"] and self.use_hot:
+                pin = torch.zeros(1, dtype=torch.int64).pin_memory()
+                with torch.cuda.stream(pipe.st):
+                    pin.copy_(hot.stats[1:2], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(pipe.st)
+                watch.append((ev, pin))
+                poll()
         pipe.drain()
         if state["prod_done"] is not None:
             main.wait_event(state["prod_done"])
         torch.cuda.synchronize(dev)
+        poll(block=True)
         e.check_numerics()
         rep.losses = e.loss_arr[:nb].double().cpu().tolist()
+        if self.dist is not None:  # the union batch's mean loss from the per-shard means
+            n_loc = torch.tensor([float(x.shape[0]) for x in local], dtype=torch.float64, device=dev)
+            tot = e.loss_arr[:nb].double() * n_loc
+            self.dist.allreduce(tot)
+            rep.losses = (tot / torch.tensor([float(b.shape[0]) for b in plan.batches], dtype=torch.float64,
+                                             device=dev)).cpu().tolist()
+        if not np.all(np.isfinite(rep.losses)):
+            raise FloatingPointError("non-finite training loss (forward aggregation or logits)")
         rep.max_weight_deltas = e.md_arr[:nb].double().cpu().tolist()
         hits = hot.batch_hits[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)
         miss = hot.batch_miss[:nb].cpu().numpy() if hot is not None else np.zeros(nb, np.int64)
         raw_rows = e.raw_rows_arr[:nb].cpu().numpy()
+        cache_rows = e.cache_hit_arr[:nb].cpu().numpy()
         feat_dim = self.dg.feat_dim
         # batch CSV transfer columns (orchestrator.py:505-543): raw features of the needed
         # rows; embeddings / aux move per super-batch, not per batch; the bottom weights'
@@ -400,7 +474,7 @@ class Trainer:
             for b in group:
                 rep.batch_rows.append({"epoch": plan.epoch, "batch": plan.first_global_batch + b, "super_batch": g,
                                        "loss": rep.losses[b], "reuse_hits": int(hits[b]), "fallbacks": int(miss[b]),
-                                       "raw_rows": int(raw_rows[b]), "cache_hit_rows": 0,
+                                       "raw_rows": int(raw_rows[b]), "cache_hit_rows": int(cache_rows[b]),
                                        "raw_elems": int(raw_rows[b]) * feat_dim, "emb_elems": 0, "aux_elems": 0,
                                        "grad_elems": int(grad_elems), "max_weight_delta": rep.max_weight_deltas[b]})
         rep.reuse_hits, rep.fallbacks = int(hits.sum()), int(miss.sum())
@@ -423,6 +497,13 @@ class Trainer:
 
     def weights(self):
         return self.engine.params.to_numpy()
+
+    def _local_seeds(self, batch: np.ndarray) -> np.ndarray:
+        """This rank's contiguous shard of a global batch (all of it single-process)."""
+        if self.dist is None:
+            return batch
+        from .parallel import shard
+        return shard(batch, self.dist.world, self.dist.rank)
 
     # ------------------------------------------------------------------
     def train_step(self, seeds: np.ndarray, batch_seed: int, batch_in_epoch: int = 0):
@@ -447,6 +528,7 @@ class Trainer:
 
         def handle():
             ev.synchronize()
+            self.engine.check_numerics()  # the reference's non-finite guard (gnnmath.py:100-102)
             return float(pin.item())
         return handle
 
@@ -481,12 +563,7 @@ class Trainer:
         pipe.drain()
         self.version += n
 
-        def handle(i):
-            def get():
-                done.synchronize()
-                return float(pin[i].item())
-            return get
-        return [handle(i) for i in range(n)]
+        return self._handles(done, pin, n)
 
     def _train_batches_native(self, batches):
         """train_batches through the native step driver (hg_pipeline_run): the
@@ -539,9 +616,19 @@ class Trainer:
         self.feeder.h2d_bytes = int(nbytes[0])
         self.version += n
 
+        return self._handles(done, pin, n)
+
+    def _handles(self, done, pin, n):
+        """One loss handle per batch; the first handle to complete also checks the
+        device numerics flags once for the whole call (gnnmath.py:100-102)."""
+        checked = []
+
         def handle(i):
             def get():
                 done.synchronize()
+                if not checked:
+                    checked.append(True)
+                    self.engine.check_numerics()
                 return float(pin[i].item())
             return get
         return [handle(i) for i in range(n)]

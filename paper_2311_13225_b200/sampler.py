@@ -292,8 +292,23 @@ def sample_khop_skip_hot(graph, seeds, fanouts, hot_set, rng_seed: int) -> Sampl
     stack = sample_khop(graph, seeds, fanouts, rng_seed)
     hot = np.asarray(list(hot_set) if isinstance(hot_set, set) else hot_set, dtype=np.int64)
     if hot.size:
-        stack.hot_flags = np.isin(stack.blocks[0].src_vertices, hot)
+        stack.hot_flags = hot_flags(as_device_graph(graph), stack.blocks[0].src_vertices, hot)
     return stack
+
+
+def hot_flags(dg: DeviceGraph, values: np.ndarray, hot: np.ndarray) -> np.ndarray:
+    """np.isin(values, hot) on the device (sampler.py:161-162): tag the hot ids in
+    a vertex-indexed table, then one flag per value (hg_member_flags)."""
+    dev = dg.device
+    hot = hot[(hot >= 0) & (hot < dg.num_vertices)]  # ids outside the graph match nothing (np.isin)
+    tag_of = torch.full((dg.num_vertices,), -1, dtype=torch.int32, device=dev)
+    h = torch.as_tensor(hot.astype(np.int32), device=dev)
+    v = torch.as_tensor(np.asarray(values).astype(np.int32), device=dev)
+    flags = torch.zeros(max(v.numel(), 1), dtype=torch.uint8, device=dev)
+    s = stream_ptr()
+    _lib.call("hg_tag_vertices", ptr(h), None, h.numel(), ptr(tag_of), 1, s)
+    _lib.call("hg_member_flags", ptr(v), None, v.numel(), ptr(tag_of), 1, ptr(flags), s)
+    return flags[:v.numel()].cpu().numpy().astype(bool)
 
 
 def sample_one_hop_hot(graph, hot_vertices, fanout: int, rng_seed: int, layer: int = 0) -> Block:
@@ -304,6 +319,5 @@ def sample_one_hop_hot(graph, hot_vertices, fanout: int, rng_seed: int, layer: i
         raise SamplerError("hot vertex list must not be empty")
     if np.unique(hot).shape[0] != hot.shape[0]:
         raise SamplerError("hot vertex list must be deduplicated")
-    if hot.min() < 0 or hot.max() >= dg.num_vertices:
-        raise SamplerError("hot vertex id out of range")
+    hot = hot[(hot >= 0) & (hot < dg.num_vertices)]  # ids outside the graph match nothing (np.isin)
     return _expand(dg, hot, fanout, derive_seed(rng_seed, SAMPLE_TAG, layer))

@@ -96,20 +96,29 @@ class EmbeddingStore:
         self.put_many(np.array([int(v)]), np.asarray(emb).reshape(1, -1), version, target_super_batch)
 
     def put_many(self, vs, embs, version: int, target_super_batch: int) -> None:
+        """``put`` for many vertices at one version (``puts`` counts every call's rows,
+        as that many reference ``put`` calls would)."""
+        n_calls = int(np.asarray(vs).reshape(-1).shape[0])
         with self._lock:
             if target_super_batch != self.current_super_batch + 1:
                 raise StoreContractError(f"put targets super-batch {target_super_batch} but only "
                                          f"{self.current_super_batch + 1} is stageable")
-            vs = np.asarray(vs, np.int64)
+            vs = np.asarray(vs, np.int64).reshape(-1)
+            embs = np.asarray(embs, np.float32).reshape(vs.shape[0], -1)
+            # a vertex put twice in one call: the last write wins (store.py:64, dict assignment)
+            last = vs.shape[0] - 1 - np.unique(vs[::-1], return_index=True)[1]
+            if last.shape[0] != vs.shape[0]:
+                last.sort()
+                vs, embs = vs[last], embs[last]
             slots = np.array([self._slot_of(int(v)) for v in vs], np.int64)
             stg = 1 - self._cur
             idx = torch.as_tensor(slots, device=self.device)
             newly = int((self._stamp[stg][idx] != self._stage_stamp).sum().item())
-            self._tab[stg][idx] = torch.as_tensor(np.asarray(embs, np.float32), device=self.device)
+            self._tab[stg][idx] = torch.as_tensor(embs, device=self.device)
             self._ver[stg][idx] = int(version)
             self._stamp[stg][idx] = self._stage_stamp
             self._staged += newly
-            self.puts += len(vs)
+            self.puts += n_calls
 
     def get(self, v: int, reading_batch: int):
         """store.py:67-98: the embedding staged for this super-batch, or None."""

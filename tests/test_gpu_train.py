@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 from conftest import golden_stack, has_cuda
+from _metrics import record
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_cuda(), reason="needs CUDA")]
 
@@ -60,13 +61,33 @@ def _run(ggraphs, name, meta, **over):
     return run_training(g.graph, g.data, cfg, return_trainer=True)
 
 
+# per-run bounds on the relative deviation from the reference's fp64 run (achieved
+# values are recorded in gpurun_out/parity_metrics.jsonl by every GPU run)
+LOSS_RTOL = {"sbm_gcn_hot": 2e-3, "sbm_sage_hot": 2e-3, "sbm_sage_plain": 2e-3, "pl_gcn_adam": 2e-3,
+             "sbm_sage_n1": 2e-3}
+MD_RTOL = {k: 2e-2 for k in LOSS_RTOL}
+
+
 @pytest.mark.parametrize("name", ["sbm_gcn_hot", "sbm_sage_hot", "sbm_sage_plain", "pl_gcn_adam", "sbm_sage_n1"])
 def test_training_matches_reference(golden, golden_meta, ggraphs, name):
     meta = golden_meta["runs"][name]
     reps, tr = _run(ggraphs, name, meta)
     assert np.array_equal(tr.hot_list, golden[f"run_{name}_hot"])
-    for rep, want in zip(reps, meta["epochs"]):
-        np.testing.assert_allclose(rep.losses, want["losses"], rtol=2e-3)
+    for k, (rep, want) in enumerate(zip(reps, meta["epochs"])):
+        r_loss = float(np.max(np.abs(np.array(rep.losses) - want["losses"]) / np.abs(want["losses"])))
+        r_md = float(np.max(np.abs(np.array(rep.max_weight_deltas) - want["max_weight_deltas"])
+                            / np.abs(want["max_weight_deltas"])))
+        r_eps = float(np.max(np.abs(np.array(rep.epsilon_trace) - want["epsilon_trace"])
+                             / np.abs(want["epsilon_trace"])))
+        record(f"{name}_e{k}.loss_rel", r_loss, LOSS_RTOL[name])
+        record(f"{name}_e{k}.max_dw_rel", r_md, MD_RTOL[name])
+        record(f"{name}_e{k}.epsilon_rel", r_eps, MD_RTOL[name])
+        assert r_loss <= LOSS_RTOL[name], r_loss
+        # the per-batch max |dw| (orchestrator.py:246-255) and the per-super-batch
+        # epsilon = max |dw| * 2n (orchestrator.py:547-551)
+        assert len(rep.epsilon_trace) == len(want["epsilon_trace"])
+        assert r_md <= MD_RTOL[name], r_md
+        assert r_eps <= MD_RTOL[name], r_eps
         assert [r["reuse_hits"] for r in rep.batch_rows] == want["reuse_hits"]
         assert [r["fallbacks"] for r in rep.batch_rows] == want["fallbacks"]
         for col in ("raw_rows", "cache_hit_rows", "raw_elems", "emb_elems", "aux_elems", "grad_elems"):
@@ -150,7 +171,7 @@ def test_bwd_scatter_flags_nonfinite():
     nself = torch.tensor([2, 2, 1], dtype=torch.int32, device="cuda")
     n_src = torch.tensor([6], dtype=torch.int32, device="cuda")
     outdeg = torch.tensor([1, 1, 0, 1, 1, 1], dtype=torch.int32, device="cuda")
-    acc = torch.zeros((6, F), dtype=torch.int64, device="cuda")
+    acc = torch.zeros((6, 2 * F), dtype=torch.int64, device="cuda")
     dx = torch.zeros((6, F), device="cuda")
     flags = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("hg_aggregate_bwd_scatter", 0, ptr(dagg), F, None, 0, F, ptr(frontier), None, n_dst, f, ptr(counts),
@@ -185,8 +206,7 @@ def test_training_edge_shapes_vs_oracle(model, fan, opt):
 @pytest.mark.parametrize("layers,hot", [(2, 0.3), (3, 0.2), (2, 0.0), (4, 0.2)])
 def test_top_fused_matches_unfused(monkeypatch, layers, hot):
     """The fused top SAGE layer kernel (aggregate -> transform -> softmax-CE -> dX ->
-    scatter in one launch, HG_TOP_FUSED) and the fused middle layers
-    (HG_MID_FUSED) reproduce the unfused kernel chain to
+    scatter in one launch, HG_TOP_FUSED) reproduces the unfused kernel chain to
     fp32 rounding over a whole run, incl. hot-embedding injection below a 2-layer
     top (the scatter then writes the injected-row-masked bottom gradient)."""
     from paper_2311_13225_b200.datagen import make_dataset
@@ -197,10 +217,8 @@ def test_top_fused_matches_unfused(monkeypatch, layers, hot):
               super_batch_n=2, hot_ratio=hot, presample_rounds=1,
               strategy="layer-based" if hot > 0 else "case1")
     monkeypatch.setenv("HG_TOP_FUSED", "0")
-    monkeypatch.setenv("HG_MID_FUSED", "0")
     a = run_training(ds, None, TrainConfig(**kw))
     monkeypatch.setenv("HG_TOP_FUSED", "1")
-    monkeypatch.setenv("HG_MID_FUSED", "1")
     b = run_training(ds, None, TrainConfig(**kw))
     for ra, rb in zip(a, b):
         np.testing.assert_allclose(ra.losses, rb.losses, rtol=1e-5)
