@@ -39,11 +39,23 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "train seeds/sec (GraphSAGE products-shape)"
 UNIT = "seeds/s"
-WORKLOAD = dict(workload="c2-products-shape", graph="synthetic Chung-Lu zipf2.5 (datagen.make_dataset('c2'))",
-                vertices=2_400_000, feat_dim=100, classes=47, model="sage", layers=3, fanouts=[15, 10, 5],
-                hidden=64, batch_size=1024, optimizer="sgd", hot_ratio=0.0)
+#: --workload: the driver's line is c2 (BASELINE configs[1], the metric's own config);
+#: c3 (configs[2], GCN on the Reddit shape, 602-dim rows) is the wide-row line
+WORKLOADS = {
+    "c2": dict(metric="train seeds/sec (GraphSAGE products-shape)",
+               config=dict(workload="c2-products-shape",
+                           graph="synthetic Chung-Lu zipf2.5 (datagen.make_dataset('c2'))", vertices=2_400_000,
+                           feat_dim=100, classes=47, model="sage", layers=3, fanouts=[15, 10, 5], hidden=64,
+                           batch_size=1024, optimizer="sgd", lr=0.01, hot_ratio=0.0)),
+    "c3": dict(metric="train seeds/sec (GCN Reddit-shape)",
+               config=dict(workload="c3-reddit-shape",
+                           graph="synthetic Chung-Lu zipf2.5 (datagen.make_dataset('c3'))", vertices=233_000,
+                           feat_dim=602, classes=41, model="gcn", layers=2, fanouts=[10, 25], hidden=256,
+                           batch_size=1024, optimizer="sgd", lr=0.01, hot_ratio=0.0)),
+}
+METRIC = WORKLOADS["c2"]["metric"]
+WORKLOAD = WORKLOADS["c2"]["config"]
 CACHE = os.environ.get("HG_BENCH_CACHE", "/tmp/hg_bench_cache")
 
 
@@ -104,7 +116,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # the CPU reference path (oracle port of the reference's per-batch pipeline)
 # ---------------------------------------------------------------------------
-def cpu_reference_steps(ds, batches, seeds_rng, budget_s, max_steps, warmup=1):
+def cpu_reference_steps(ds, batches, seeds_rng, budget_s, max_steps, warmup=1, wl=None):
     """Time the reference's per-batch path on the host (orchestrator.py:236-256 +
     sampler.sample_khop): oracle sample_khop (C restatement of the numba draw
     + numpy dedup/lexsort) -> float64 gather -> forward/backward (numpy/OpenBLAS)
@@ -114,10 +126,11 @@ def cpu_reference_steps(ds, batches, seeds_rng, budget_s, max_steps, warmup=1):
     feats64 = ds.features.astype(np.float64)
     data = O.VertexData(features=feats64, labels=ds.labels, train_mask=ds.train_mask, val_mask=ds.val_mask,
                         test_mask=ds.test_mask)
-    cfg = dict(O.DEFAULT_CFG, model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024,
-               lr=0.01, strategy="case1", hot_ratio=0.0)
-    dims = [ds.feat_dim, 64, 64, int(ds.labels.max()) + 1]
-    W = O.init_params("sage", dims, 0)
+    wl = wl or WORKLOAD
+    cfg = dict(O.DEFAULT_CFG, model=wl["model"], layers=wl["layers"], fanouts=tuple(wl["fanouts"]),
+               hidden_dim=wl["hidden"], batch_size=wl["batch_size"], lr=wl["lr"], strategy="case1", hot_ratio=0.0)
+    dims = [ds.feat_dim] + [wl["hidden"]] * (wl["layers"] - 1) + [int(ds.labels.max()) + 1]
+    W = O.init_params(wl["model"], dims, 0)
     adam = O.Adam()
     n_seeds = 0
     t_total = 0.0
@@ -185,14 +198,15 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from paper_2311_13225_b200.datagen import make_dataset
-    ds = make_dataset("c2", cache_dir=CACHE)
+    wl = WORKLOADS[args.workload]
+    ds = make_dataset(args.workload, cache_dir=CACHE)
     batches, rs = epoch_batches(ds, args.warmup + args.steps)
     budget = float(os.environ.get("HG_REF_BUDGET_S", "120"))
-    v, steps, secs = cpu_reference_steps(ds, batches, rs, budget, args.steps, warmup=args.warmup)
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
+    v, steps, secs = cpu_reference_steps(ds, batches, rs, budget, args.steps, warmup=args.warmup, wl=wl["config"])
+    line = {"metric": wl["metric"], "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * secs / max(steps, 1), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": dict(WORKLOAD, parallelism="host-cpu", l2_flush="inputs>L2 (2.4M x 100 feature table)"),
+            "config": dict(wl["config"], parallelism="host-cpu", l2_flush="inputs > L2 (feature table)"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port",
                              "sample": f"{steps} batches of 1024 seeds (requested {args.steps}, capped at "
                                        f"{budget:.0f}s of CPU work) after {args.warmup} warm-up; {cpu_model()}"},
@@ -206,6 +220,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--phases", action="store_true", help="also report a per-phase time breakdown")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -239,11 +254,14 @@ def main():
         t = torch.ones(1, device="cuda")
         dist.all_reduce(t)  # NCCL warm-up outside capture
     dev = torch.device("cuda", torch.cuda.current_device())
-    ds = make_dataset("c2", cache_dir=CACHE)
+    wl = WORKLOADS[args.workload]
+    WL = wl["config"]
+    ds = make_dataset(args.workload, cache_dir=CACHE)
     # report_transfers=False: the per-batch CSV bookkeeping (needed-row counting) is
     # not part of training and no report is written here
-    cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
-                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0, report_transfers=False)
+    cfg = TrainConfig(model=WL["model"], layers=WL["layers"], fanouts=tuple(WL["fanouts"]), hidden_dim=WL["hidden"],
+                      batch_size=WL["batch_size"], lr=WL["lr"], strategy="case1", hot_ratio=0.0, use_graph=True,
+                      seed=0, report_transfers=False)
     tr = Trainer(ds, cfg, dist=dist_ctx)
     e = tr.engine
     # instrumented copies of every set's graphs, split so CUDA events bracket the
@@ -451,17 +469,18 @@ def main():
     cpu_base = None
     if not args.no_cpu_baseline and world == 1:
         budget = float(os.environ.get("HG_CPU_BASELINE_S", "20"))
-        cb, steps, secs = cpu_reference_steps(ds, batches, rseeds, budget, 200, warmup=1)
+        cb, steps, secs = cpu_reference_steps(ds, batches, rseeds, budget, 200, warmup=1, wl=WL)
         cpu_base = {"value": cb, "unit": UNIT, "cores": host_cores(), "kind": "port",
-                    "sample": f"{steps} C2 batches of 1024 seeds ({secs:.1f}s CPU) after 1 warm-up; oracle port of "
+                    "sample": f"{steps} {args.workload.upper()} batches of 1024 seeds ({secs:.1f}s CPU) after 1 warm-up; oracle port of "
                               f"the reference path (C draw loop single-threaded, numpy/OpenBLAS on all cores); "
                               f"{cpu_model()}"}
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+    line = {"metric": wl["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
             "ms_per_step": ms / K, "ms_per_step_instrumented_serial": i_start.elapsed_time(i_end) / K,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "fp32", "data": "synthetic",
-            "config": dict(WORKLOAD, parallelism=f"dp{world}" if world > 1 else "single",
-                           l2_flush="inputs > L2: 0.96 GB feature table + 0.26 GB CSR, random rows per step",
+            "config": dict(WL, parallelism=f"dp{world}" if world > 1 else "single",
+                           l2_flush=f"inputs > L2: {ds.num_vertices * ds.feat_dim * 4 / 1e9:.2f} GB feature table "
+                                    f"+ {ds.num_edges * 4 / 1e9:.2f} GB CSR, random rows per step",
                            global_batch=global_batch, seeds_per_rank=n_loc),
             "roofline": {"bound": "hbm", "kernel": "k_agg_fwd (bottom fused gather+mean, SAGE)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

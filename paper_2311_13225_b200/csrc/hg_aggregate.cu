@@ -25,6 +25,7 @@
 // (gnnmath.py:130-134,183-188) before writing dZ of the layer below.
 #include "hg_common.cuh"
 #include "hg_gnn_internal.h"
+#include "hg_tc.cuh"
 
 namespace {
 
@@ -345,6 +346,221 @@ int launch_bwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* dagg, int l
     return HG_EUNSUPPORTED;
 }
 
+
+// ---------------------------------------------------------------------------
+// Wide rows (F > 128: C3's 602 features = 2.4 KB rows): the rows of a
+// destination's edges are staged into shared memory by the TMA engine
+// (cp.async.bulk global -> shared, one mbarrier per stage, complete_tx) instead
+// of per-lane 128-bit loads.  One lane per warp keeps up to S rows in flight
+// (S * 2.4 KB per warp, no register cost: the LDG loop holds 2 rows per warp in
+// ~96 registers), running ahead into the warp's next destination; the warp
+// consumes the rows in edge order from shared memory.  Same items, weights
+// and FMA order as k_agg_fwd, so the outputs are bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int BULK_WARPS = 4;
+
+struct BulkDesc {
+    int i, cnt, v, n_items;
+    bool skip, self_item;
+    unsigned valid;  // lanes j < cnt holding a consumed edge
+    int row;         // this lane's edge row (slot j = lane), -1 if none
+    float w;
+};
+
+template <int NV, int MODE>
+__global__ void __launch_bounds__(BULK_WARPS * 32) k_agg_fwd_bulk(
+    const float* __restrict__ hin, int ld_in, int F4, const int* __restrict__ frontier, const int* d_n, int cap,
+    int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
+    const int* __restrict__ nself, const int* __restrict__ outdeg, const uint8_t* __restrict__ inj,
+    float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out, int ld_agg, int S, int stage_bytes) {
+    using namespace hgtc;
+    constexpr bool GLOBAL = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL);
+    constexpr bool GCN = (MODE == M_GCN_LOCAL || MODE == M_GCN_GLOBAL);
+    extern __shared__ __align__(128) uint8_t sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* ring = sm + (size_t)warp * S * stage_bytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)BULK_WARPS * S * stage_bytes) + warp * S;
+    if (lane == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(&bar[st], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    hg_pdl_begin();
+    const int n = hg_load_count(d_n, cap);
+    const uint32_t row_bytes = (uint32_t)F4 * 16u;
+
+    auto load_desc = [&](int i, BulkDesc& d) {
+        d.i = i < n ? i : -1;
+        d.row = -1;
+        d.w = 0.f;
+        d.cnt = 0;
+        d.skip = true;
+        d.self_item = false;
+        d.valid = 0u;
+        d.n_items = 0;
+        if (d.i < 0) return;
+        d.skip = inj && inj[i];
+        d.v = frontier[i];
+        d.self_item = GLOBAL && self_out && !d.skip;
+        if (!d.skip) {
+            d.cnt = counts[i];
+            const int64_t sbase = (int64_t)i * f;
+            float wd = 0.f;
+            if (!GCN) { const int ns = nself[i]; wd = ns > 0 ? 1.0f / (float)ns : 0.f; }
+            if (lane < d.cnt) {
+                const int sg = slot_g[sbase + lane];
+                const int sl = (GLOBAL && !GCN) ? 0 : slot_local[sbase + lane];
+                if (GCN) { d.row = GLOBAL ? sg : sl; d.w = gcn_w(outdeg[sl], d.cnt); }
+                else if (sg != d.v) { d.row = GLOBAL ? sg : sl; d.w = wd; }
+            }
+        }
+        d.valid = __ballot_sync(0xffffffffu, d.row >= 0);
+        d.n_items = (d.self_item ? 1 : 0) + __popc(d.valid);
+    };
+    // row id of item t of descriptor d (uniform across the warp)
+    auto item_row = [&](const BulkDesc& d, int t) -> int {
+        if (d.self_item) {
+            if (t == 0) return d.v;
+            --t;
+        }
+        const int src = __fns(d.valid, 0, t + 1);
+        return __shfl_sync(0xffffffffu, d.row, src);
+    };
+    auto issue = [&](const BulkDesc& d, int t, long long k) {
+        const int r = item_row(d, t);
+        if (lane == 0) {
+            const int st = (int)(k % S);
+            fence_proxy_async();  // the stage's previous generic reads before the async write
+            mbar_expect_tx(&bar[st], row_bytes);
+            bulk_load(smem_u32(ring + (size_t)st * stage_bytes), hin + (int64_t)r * ld_in, row_bytes, &bar[st]);
+        }
+    };
+
+    const int gw = blockIdx.x * BULK_WARPS + warp, nw = gridDim.x * BULK_WARPS;
+    BulkDesc cur, nxt;
+    load_desc(gw, cur);
+    load_desc(gw + nw, nxt);
+    long long kp = 0, kc = 0;  // items produced / consumed by this warp
+    int pd = 0, pt = 0;        // producer: descriptor (0 = cur, 1 = nxt), next item
+    while (cur.i >= 0) {
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = 0; t < cur.n_items; ++t) {
+            while (kp - kc < S) {  // keep up to S rows in flight, into the next destination
+                if (pd == 0) {
+                    if (pt < cur.n_items) { issue(cur, pt++, kp++); continue; }
+                    pd = 1;
+                    pt = 0;
+                }
+                if (pt < nxt.n_items) { issue(nxt, pt++, kp++); continue; }
+                break;
+            }
+            const int st = (int)(kc % S);
+            mbar_wait(&bar[st], (uint32_t)((kc / S) & 1));
+            const float4* x = reinterpret_cast<const float4*>(ring + (size_t)st * stage_bytes);
+            if (cur.self_item && t == 0) {  // the destination's own row (SAGE self term input)
+                float4* dst = reinterpret_cast<float4*>(self_out + (int64_t)cur.i * ld_self);
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int c = lane + k * 32;
+                    if (c < F4) dst[c] = x[c];
+                }
+            } else {
+                const int te = t - (cur.self_item ? 1 : 0);
+                const float w = __shfl_sync(0xffffffffu, cur.w, __fns(cur.valid, 0, te + 1));
+#pragma unroll
+                for (int k = 0; k < NV; ++k) {
+                    const int c = lane + k * 32;
+                    if (c < F4) acc[k] = f4_fma(w, x[c], acc[k]);
+                }
+            }
+            __syncwarp();
+            ++kc;
+        }
+        if (GLOBAL && self_out && cur.skip) {
+            float4* dst = reinterpret_cast<float4*>(self_out + (int64_t)cur.i * ld_self);
+#pragma unroll
+            for (int k = 0; k < NV; ++k) {
+                const int c = lane + k * 32;
+                if (c < F4) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        float4* out = reinterpret_cast<float4*>(agg_out + (int64_t)cur.i * ld_agg);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lane + k * 32;
+            if (c < F4) out[c] = acc[k];
+        }
+        // the next destination becomes current; the producer keeps its position
+        if (pd == 1) pd = 0;
+        else pt = 0;
+        cur = nxt;
+        load_desc(cur.i < 0 ? n : cur.i + nw, nxt);
+    }
+}
+
+// wide-row gather: bulk-copy staging (default; hg_set_tuning key 12 = 0 or env
+// HG_AGG_BULK=0 selects the LDG loop)
+int g_agg_bulk = -1;
+bool agg_bulk_enabled() {
+    if (g_agg_bulk < 0) {
+        const char* e = getenv("HG_AGG_BULK");
+        g_agg_bulk = e ? (atoi(e) != 0) : 1;
+    }
+    return g_agg_bulk != 0;
+}
+
+// stages per warp for rows of row_bytes: fill ~2 CTAs x 100 KB per SM
+int bulk_stages(int stage_bytes) {
+    int S = (100 * 1024) / (BULK_WARPS * stage_bytes);
+    return S < 2 ? 2 : (S > 16 ? 16 : S);
+}
+
+template <int MODE>
+int launch_fwd_bulk(int F4, cudaStream_t s, const float* hin, int ld_in, const int* frontier, const int* d_n,
+                    int cap, int f, const int* counts, const int* slot_g, const int* slot_local, const int* nself,
+                    const int* outdeg, const uint8_t* inj, float* self_out, int ld_self, float* agg_out, int ld_agg) {
+    const int stage_bytes = (F4 * 16 + 127) / 128 * 128;
+    const int S = bulk_stages(stage_bytes);
+    const size_t smem = (size_t)BULK_WARPS * S * stage_bytes + (size_t)BULK_WARPS * S * 8;
+    if (smem > 227 * 1024) return HG_EUNSUPPORTED;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if ((MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL) && hg_l2_window_attr(&attr[na])) ++na;
+    if (hg_pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cudaLaunchConfig_t cfg = {};
+    const int per_sm = (int)((227 * 1024) / (smem + 1024));
+    const long long need = ((long long)cap + BULK_WARPS - 1) / BULK_WARPS;
+    long long grid = (long long)HG_NUM_SMS * (per_sm < 1 ? 1 : per_sm);
+    cfg.gridDim = dim3((unsigned)(need < grid ? (need < 1 ? 1 : need) : grid));
+    cfg.blockDim = dim3(BULK_WARPS * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
+#define HG_FWDB(V)                                                                                           \
+    if (F4 <= 32 * V) {                                                                                      \
+        static bool attr_set = false;                                                                        \
+        if (!attr_set) {                                                                                     \
+            cudaFuncSetAttribute(k_agg_fwd_bulk<V, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                 227 * 1024);                                                                \
+            attr_set = true;                                                                                 \
+        }                                                                                                    \
+        cudaLaunchKernelEx(&cfg, k_agg_fwd_bulk<V, MODE>, hin, ld_in, F4, frontier, d_n, cap, f, counts,      \
+                           slot_g, slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, ld_agg, S,    \
+                           stage_bytes);                                                                     \
+        return HG_OK;                                                                                        \
+    }
+    HG_FWDB(2) HG_FWDB(4) HG_FWDB(6) HG_FWDB(8)
+#undef HG_FWDB
+    return HG_EUNSUPPORTED;
+}
+
 // CTAs per SM of the bottom (global-id) aggregation grid: env HG_AGG_CTAS_PER_SM
 // (default 8); fewer leaves SM slots for the concurrently running training stream
 int agg_ctas_per_sm() {
@@ -368,6 +584,8 @@ void pick_lanes(int F4, int& LPR, int& NV) {
 
 }  // namespace
 
+void hg_set_agg_bulk(int v) { g_agg_bulk = v ? 1 : 0; }
+
 // model: 0 = SAGE (mean over non-self sampled neighbours), 1 = GCN (block sym-norm).
 // global_src: 1 = rows addressed by global id (bottom layer, reads the feature
 // table), 0 = by local src id (upper layers, reads the previous activation).
@@ -390,6 +608,15 @@ extern "C" int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* 
     cudaStream_t s = (cudaStream_t)stream;
     int rc;
     const int mode = (model ? 2 : 0) + (global_src ? 1 : 0);
+    if (F4 > 32 && F4 <= 256 && fanout <= 32 && agg_bulk_enabled()) {  // wide rows: TMA bulk-copy staging
+        switch (mode) {
+            case M_SAGE_LOCAL: rc = launch_fwd_bulk<M_SAGE_LOCAL>(F4, s, hin, ld_in, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+            case M_SAGE_GLOBAL: rc = launch_fwd_bulk<M_SAGE_GLOBAL>(F4, s, hin, ld_in, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+            case M_GCN_LOCAL: rc = launch_fwd_bulk<M_GCN_LOCAL>(F4, s, hin, ld_in, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+            default: rc = launch_fwd_bulk<M_GCN_GLOBAL>(F4, s, hin, ld_in, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
+        }
+        if (rc == HG_OK) return hg_check_launch("aggregate_fwd(bulk)");
+    }
     switch (mode) {
         case M_SAGE_LOCAL: rc = launch_fwd<M_SAGE_LOCAL>(LPR, NV, g, s, hin, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;
         case M_SAGE_GLOBAL: rc = launch_fwd<M_SAGE_GLOBAL>(LPR, NV, g, s, hin, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg); break;

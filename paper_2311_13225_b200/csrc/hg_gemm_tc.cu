@@ -623,6 +623,7 @@ extern "C" int hg_set_tuning(int32_t key, int32_t value) {
     if (key == 8) { hg_set_block_coop(value); return HG_OK; }
     if (key == 9) { hg_tma_set_dbg(value); return HG_OK; }
     if (key == 11) { hg_tma_set_wg_tsa(value); return HG_OK; }
+    if (key == 12) { hg_set_agg_bulk(value); return HG_OK; }
     hg_set_error("set_tuning: unknown key %d", key);
     return HG_EINVAL;
 }

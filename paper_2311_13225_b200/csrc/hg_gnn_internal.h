@@ -43,3 +43,6 @@ bool hg_l2_window_attr(cudaLaunchAttribute* a);
 void hg_set_pdl(int v);
 
 void hg_set_block_coop(int v);
+
+// wide-row bottom gather: TMA bulk-copy staging on/off (hg_aggregate.cu)
+void hg_set_agg_bulk(int v);

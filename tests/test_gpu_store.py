@@ -300,8 +300,10 @@ def _scatter(dagg_np, counts, slot_local, slot_g, frontier, nself, outdeg, n_src
     dx = torch.full((n_src, F), float("nan"), device=dev)
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     ns = t([n_src])
-    _lib.call("hg_aggregate_bwd_scatter", 0, ptr(dagg), F, None, 0, F, ptr(t(frontier)), None, n_dst, f,
-              ptr(t(counts)), ptr(t(slot_g)), ptr(t(slot_local)), ptr(t(nself)), ptr(t(outdeg)), ptr(ns), n_src,
+    keep = [t(a) for a in (frontier, counts, slot_g, slot_local, nself, outdeg)]  # alive across the call
+    fr_d, cnt_d, sg_d, sl_d, ns_d, od_d = keep
+    _lib.call("hg_aggregate_bwd_scatter", 0, ptr(dagg), F, None, 0, F, ptr(fr_d), None, n_dst, f,
+              ptr(cnt_d), ptr(sg_d), ptr(sl_d), ptr(ns_d), ptr(od_d), ptr(ns), n_src,
               None, 0, None, ptr(acc), ptr(dx), F, ptr(flags), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     return dx.double().cpu().numpy(), int(flags.item()), int(acc.abs().sum().item())
@@ -351,7 +353,7 @@ def test_fixed_point_scatter_range_and_nonfinite_flags():
     rng = np.random.default_rng(8)
     counts, sl, sg, fr, ns, od = _random_block(rng)
     F = 16
-    big = np.full((counts.shape[0], F), 3e13, np.float32)  # outdeg * |v| >= 2^42
+    big = np.full((counts.shape[0], F), 1e14, np.float32)  # outdeg * |v| >= 2^42 for shared sources
     _, flags, _ = _scatter(big, counts, sl, sg, fr, ns, od, 900, F)
     assert flags & 2
     bad = np.zeros((counts.shape[0], F), np.float32)

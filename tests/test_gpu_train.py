@@ -3,7 +3,8 @@ reference's golden runs.
 
 Tolerances (fp32 device arithmetic vs the reference's fp64):
 * logits / gradients of one batch: |d| <= 2e-4 * max(1, |ref|)
-* per-batch losses over a run: relative 2e-3 (SGD/Adam trajectories drift in fp32)
+* per-batch losses over a run: relative 1e-4; max |dw| per batch and the epsilon
+  trace: relative 1e-3 (achieved <= 1e-5; recorded in gpurun_out/parity_metrics.jsonl)
 * integer bookkeeping (reuse hits, fallbacks, staged counts/versions, max gap,
   warm-up rows, hot list, queues): exact
 * test/val accuracy: within 0.01 (1000-vertex fixture: 1 vertex = 0.004)
@@ -63,9 +64,9 @@ def _run(ggraphs, name, meta, **over):
 
 # per-run bounds on the relative deviation from the reference's fp64 run (achieved
 # values are recorded in gpurun_out/parity_metrics.jsonl by every GPU run)
-LOSS_RTOL = {"sbm_gcn_hot": 2e-3, "sbm_sage_hot": 2e-3, "sbm_sage_plain": 2e-3, "pl_gcn_adam": 2e-3,
-             "sbm_sage_n1": 2e-3}
-MD_RTOL = {k: 2e-2 for k in LOSS_RTOL}
+# (round 2 GPU run: losses <= 8.9e-6, max |dw| <= 9.5e-6, epsilon <= 5.0e-6)
+LOSS_RTOL = {k: 1e-4 for k in ("sbm_gcn_hot", "sbm_sage_hot", "sbm_sage_plain", "pl_gcn_adam", "sbm_sage_n1")}
+MD_RTOL = {k: 1e-3 for k in LOSS_RTOL}
 
 
 @pytest.mark.parametrize("name", ["sbm_gcn_hot", "sbm_sage_hot", "sbm_sage_plain", "pl_gcn_adam", "sbm_sage_n1"])
@@ -188,7 +189,7 @@ def test_training_edge_shapes_vs_oracle(model, fan, opt):
     """Engine paths the golden runs do not reach — fanout > 32 (sequential draw
     kernel) at the bottom and at the top, fanout 1, a one-layer model (no hidden
     ReLU, logits straight from the bottom layer), a partial last batch — against
-    the CPU oracle on the same graph bytes (fp64), per-batch losses rtol 2e-3."""
+    the CPU oracle on the same graph bytes (fp64), per-batch losses rtol 1e-4."""
     from oracle import oracle as O
     from paper_2311_13225_b200.datagen import make_dataset
     from paper_2311_13225_b200.orchestrator import TrainConfig, run_training
@@ -200,7 +201,9 @@ def test_training_edge_shapes_vs_oracle(model, fan, opt):
     od = O.VertexData(features=ds.features.astype(np.float64), labels=ds.labels, train_mask=ds.train_mask,
                       val_mask=ds.val_mask, test_mask=ds.test_mask)
     ref, _, _ = O.run_training(og, od, kw, evaluate_each_epoch=False)
-    np.testing.assert_allclose(reps[0].losses, ref[0]["losses"], rtol=2e-3)
+    r = float(np.max(np.abs(np.array(reps[0].losses) - ref[0]["losses"]) / np.abs(ref[0]["losses"])))
+    record(f"edge_{model}_{'x'.join(map(str, fan))}_{opt}.loss_rel", r, 1e-4)
+    assert r <= 1e-4, r
 
 
 @pytest.mark.parametrize("layers,hot", [(2, 0.3), (3, 0.2), (2, 0.0), (4, 0.2)])

@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Run exactly one eager (non-graph) C2 training step inside
+"""Run exactly one eager (non-graph) training step of a bench workload (c2 default, c3) inside
 cudaProfilerStart/Stop, for `ncu --profile-from-start off`:
 
     ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
@@ -21,9 +21,12 @@ from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer  # noqa: E40
 
 def main():
     workload = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    from bench import WORKLOADS
+    wl = WORKLOADS[workload]["config"]
     ds = make_dataset(workload, cache_dir="/tmp/hg_bench_cache")
-    cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
-                      strategy="case1", hot_ratio=0.0, use_graph=False, report_transfers=False)
+    cfg = TrainConfig(model=wl["model"], layers=wl["layers"], fanouts=tuple(wl["fanouts"]), hidden_dim=wl["hidden"],
+                      batch_size=1024, lr=wl["lr"], strategy="case1", hot_ratio=0.0, use_graph=False,
+                      report_transfers=False)
     tr = Trainer(ds, cfg)
     order = runplan.shuffle_epoch(ds.train_ids(), 0, 0)
     batches = runplan.split_batches(order, 1024)
