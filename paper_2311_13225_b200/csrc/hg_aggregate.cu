@@ -500,21 +500,23 @@ __global__ void __launch_bounds__(BULK_WARPS * 32) k_agg_fwd_bulk(
     }
 }
 
-// wide-row gather: bulk-copy staging (default; hg_set_tuning key 12 = 0 or env
-// HG_AGG_BULK=0 selects the LDG loop)
+// wide-row gather: bulk-copy staging on (hg_set_tuning key 12 = 1 or env
+// HG_AGG_BULK=1) / the per-lane LDG loop (default: measured 2.4x faster at C3,
+// profiles/r02_c3_wide_rows.md)
 int g_agg_bulk = -1;
 bool agg_bulk_enabled() {
     if (g_agg_bulk < 0) {
         const char* e = getenv("HG_AGG_BULK");
-        g_agg_bulk = e ? (atoi(e) != 0) : 1;
+        g_agg_bulk = e ? (atoi(e) != 0) : 0;
     }
     return g_agg_bulk != 0;
 }
 
-// stages per warp for rows of row_bytes: fill ~2 CTAs x 100 KB per SM
+// stages per warp for rows of row_bytes: fill ~2 CTAs x 100 KB per SM (env HG_BULK_STAGES)
 int bulk_stages(int stage_bytes) {
     int S = (100 * 1024) / (BULK_WARPS * stage_bytes);
-    return S < 2 ? 2 : (S > 16 ? 16 : S);
+    if (const char* e = getenv("HG_BULK_STAGES")) S = atoi(e);
+    return S < 2 ? 2 : (S > 32 ? 32 : S);
 }
 
 template <int MODE>

@@ -11,8 +11,9 @@ bound with the achieved value recorded (tests/_metrics.py):
   proposal; fp32 rounding of features and weights alone moves them ~1e-6);
 * max |dw| per batch and the epsilon trace: relative 1e-3 (a max over 27K-165K
   weight steps, each an fp32 gradient x lr);
-* the learnable dataset (lr 1.0 for 60 batches): the first 10 losses relative
-  1e-4, all losses 2e-2 (lr 1.0 amplifies fp32 rounding along the trajectory),
+* the learnable dataset (SGD lr 0.5, 3 epochs x 30 batches): the first 10
+  losses relative 1e-4, all losses 2e-2 (a large step amplifies fp32 rounding
+  along the trajectory),
   test and val accuracy within 0.005 (0.5 points, north_star) on 24,000 test
   vertices.
 """
@@ -192,15 +193,14 @@ def test_c1_two_epochs_match_reference(cmeta):
 @pytest.mark.parametrize("name", ["learn_sgd", "learn_hot"])
 def test_learnable_accuracy_within_half_point(cmeta, name):
     """north_star: test accuracy within 0.5 points of the reference on a
-    non-saturating task (reference: 38.1% / 19.7% test accuracy after 2 epochs,
-    24,000 test vertices), plus the losses of all 60 batches."""
+    non-saturating task (24,000 test vertices), plus the losses of all 90 batches."""
     from paper_2311_13225_b200.orchestrator import run_training
     meta = cmeta[name]
     ds = limited(meta)
     assert int(np.asarray(ds.test_mask).sum()) >= 20_000
     reps = run_training(ds, None, run_cfg(meta, execution="pipelined"))
     for k, (rep, want) in enumerate(zip(reps, meta["epochs"])):
-        # SGD at lr 1.0 amplifies fp32 rounding along the trajectory: the first 10
+        # a large SGD step amplifies fp32 rounding along the trajectory: the first 10
         # batches agree to 1e-4, the rest of the run drifts (recorded) within 2e-2
         r_first = rel(rep.losses[:10], want["losses"][:10])
         r_loss = rel(rep.losses, want["losses"])
