@@ -1,0 +1,10 @@
+#!/bin/bash
+# round-2 pass d: whole GPU suite, smoke, default bench (with CPU baseline), reference arm, c3 bench line
+TAG=${1:-r02}
+mkdir -p gpurun_out; rm -f gpurun_out/parity_metrics.jsonl
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 2400 python -m pytest tests -m gpu -q -rf --timeout 900 -p no:cacheprovider --durations=15 > gpurun_out/pytest_$TAG.log 2>&1; echo "tests rc=$?"; tail -30 gpurun_out/pytest_$TAG.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_$TAG.log
+timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"; cat gpurun_out/bench_$TAG.json
+timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"; cut -c1-400 gpurun_out/bench_ref_$TAG.json
+timeout 900 python bench.py --workload c3 --steps 50 --warmup 5 > gpurun_out/bench_c3_$TAG.json 2> gpurun_out/bench_c3_$TAG.err; echo "c3 rc=$?"; cut -c1-600 gpurun_out/bench_c3_$TAG.json
