@@ -77,9 +77,7 @@ int hg_first_occurrence_advance(int32_t* tag_ctr, void* stream);
  *      bumps *tag_ctr so the next use of minpos starts clean (first-occurrence
  *      entries are left holding their local id under the reserved tag 0xFFFFFFFF). */
 int64_t hg_dedup_ws_size(int32_t cap_dst, int32_t fanout);
-/* hg_sample_layer + hg_dedup_relabel in one call (same arguments, same outputs);
- * optionally (hg_set_tuning key 8) blocks with fanout <= 32 and cap_dst <= 16384
- * run as one cooperative kernel (draw | grid sync | mark/scan/emit | grid sync | relabel). */
+/* hg_sample_layer + hg_dedup_relabel in one call (same arguments, same outputs). */
 int hg_sample_block(const int64_t* offsets, const int32_t* targets, const int32_t* frontier, const int32_t* d_n_dst,
                     int32_t cap_dst, int32_t fanout, const uint64_t* d_seed, int32_t layer, int32_t* counts,
                     int32_t* slots, int32_t* slot_local, uint64_t* minpos, int32_t* tag_ctr, int32_t* src_vertices,
@@ -116,12 +114,6 @@ int hg_block_to_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, c
 int hg_raw_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
                  const int32_t* slots, int32_t* edge_dst, int32_t* edge_src, int32_t* d_n_edges, int32_t* ws,
                  void* stream);
-
-/* Stable src-major view for the transposed aggregation (gnnmath.py:140,199). */
-int64_t hg_csc_ws_size(int32_t cap_dst, int32_t fanout);
-int hg_build_csc(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
-                 const int32_t* slot_local, int32_t cap_src, int32_t* csc_slot, int32_t* seg_beg,
-                 int32_t* seg_end, int32_t* ws, void* stream);
 
 /* ---- generic plug-in kernels (numpy-shaped API) ------------------------- */
 /* kernels.stable_unique (kernels.py:166-180) for arbitrary int64 values. */
@@ -163,15 +155,7 @@ int hg_ipc_get_handle(const void* dptr, uint8_t* out_handle64, int64_t* out_offs
 int hg_ipc_open_handle(const uint8_t* handle64, void** out_ptr);
 int hg_ipc_close(void* ptr);
 int hg_enable_peer_access(int32_t peer_device);
-int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself, int32_t ld_dself,
-                     int32_t F, const int32_t* frontier, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                     const int32_t* counts, const int32_t* slot_g, const int32_t* nself, const int32_t* outdeg,
-                     const int32_t* csc_slot, const int32_t* seg_beg, const int32_t* seg_end,
-                     const int32_t* d_n_src, int32_t cap_src, const float* hmask, int32_t ld_hmask,
-                     const uint8_t* inj_mask, float* dx, int32_t ld_dx, const int32_t* csc_dst,
-                     const float* csc_w, void* stream);
-/* Transposed aggregation by deterministic fixed-point scatter (default path for
- * layers >= 1): dx[s] = mask(dself[s] (s < n_dst) + sum_e w_e dagg[dst_e]) with
+/* Transposed aggregation by deterministic fixed-point scatter (layers >= 1): dx[s] = mask(dself[s] (s < n_dst) + sum_e w_e dagg[dst_e]) with
  * the sum accumulated in two-word fixed point (hi = v*2^20, lo = remainder*2^60, two
  * int64 words; order-independent, bit-exact across runs, exact for every fp32
  * contribution >= 2^-37) in acc_ws (int64 [cap_src x 2F]: a row's F hi words then its
@@ -207,20 +191,7 @@ int hg_aggregate_bwd_finish(const float* dself, int32_t ld_dself, int32_t F, con
                             const int32_t* d_n_src, int32_t cap_src, const int32_t* outdeg, const float* hmask,
                             int32_t ld_hmask, const uint8_t* inj_mask, int64_t* acc_ws, float* dx, int32_t ld_dx,
                             void* stream);
-/* per sorted transposed edge: (dst, weight), dst = -1 for empty slots / SAGE self edges;
- * optional input of hg_aggregate_bwd (csc_dst/csc_w NULL => derived on the fly) */
-int hg_csc_weights(int32_t model, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
-                   const int32_t* frontier, const int32_t* slot_g, const int32_t* slot_local, const int32_t* nself,
-                   const int32_t* outdeg, const int32_t* csc_slot, int32_t* csc_dst, float* csc_w, void* stream);
-
 /* ---- K8 dense transforms (gnnmath.py:121,135,139,173,190-198) ---------- */
-int hg_gemm_f32(const float* A1, int32_t lda1, int32_t K1, const float* B1, int32_t ldb1, const float* A2,
-                int32_t lda2, int32_t K2, const float* B2, int32_t ldb2, int32_t trans_b, float* C, int32_t ldc,
-                int32_t N, const int32_t* d_M, int32_t M_cap, int32_t act, void* stream);
-int64_t hg_wgrad_ws_size(int32_t K, int32_t N, int32_t M_cap);
-int hg_wgrad_f32(const float* A, int32_t lda, int32_t K, const float* G, int32_t ldg, int32_t N,
-                 const int32_t* d_M, int32_t M_cap, float* out, float scale, float* ws, void* stream);
-
 /* tcgen05 (5th-gen tensor core, kind::tf32, 3xTF32 split => fp32-class accuracy).
  *  C = act(A1 op(B)[0:K1] + A2 op(B)[K1:K1+K2]); op(B)(k,n) = B[k*ldb+n] if trans_b
  *  (forward: B = [W_self; W_neigh] stacked [K x N]) else B[n*ldb+k] (dX = dZ W^T).
@@ -235,14 +206,9 @@ int hg_gemm_tc(const float* A1, int32_t lda1, int32_t K1, const float* A2, int32
                const void* bimg, float* C, int32_t ldc, int32_t N, const int32_t* d_M, int32_t M_cap, int32_t act,
                void* stream);
 /* process-wide tuning knobs for the tensor-core kernels (key 1: MN-major descriptor offsets;
- * key 2: 1 = legacy cp.async GEMM kernels instead of the warp-specialised TMA pipelines;
  * key 3: forward GEMM form, 1 = A operand through TMEM (default), 0 = both operands from smem;
- * key 4: 1 = fp32 SIMT latency kernels for M_cap <= 16384 and K, N <= 128, 0 (default) = tensor cores always;
  * key 5: programmatic dependent launch of the step kernels, 1 (default; env HG_PDL=0 at load turns it off) / 0;
- * key 6: TS-form GEMM keeps the whole B image resident in smem when it fits, A ring released by the split warps (1) / streams B per stage (0, default);
  * key 7: paired hi|lo MMAs (N = 2*BN operand, two instructions per K slice instead of three) for BN <= 64 (1, default) / 0;
- * key 8: hg_sample_block runs small blocks as one cooperative kernel (1) / three kernels (0, default: the
- *        grid syncs measured slower than the launch gaps they replace));
  * key 11: weight gradient with A^T's hi/lo written to TMEM by the split warps, MMAs reading only G from
  *        shared memory (1, default) / both operands from shared memory (0);
  * key 12: wide-row (F > 128) aggregation stages rows into shared memory with TMA bulk copies
@@ -298,7 +264,10 @@ int hg_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, f
 
 /* ---- native step driver: the per-batch loop of Trainer.train_batches
  *      (orchestrator.py:520-560) over captured half-step graphs.  For step k:
- *      H2D of host_stage[k*slot_bytes, +copy_bytes[k]) into dev_stage[k % n_sets]
+ *      pack host_stage[k*slot_bytes, +slot_bytes) = bp_rows[k] (8 int64) at 0 |
+ *      {n_seeds[k], n_div[k]} (int32) at counts_offset | the n_seeds[k] int64 seed ids
+ *      at host_seed_ptrs[k] narrowed to int32 at seeds_offset (engine.stage_views),
+ *      right before the step's launches; H2D of the packed bytes into dev_stage[k % n_sets]
  *      + sample_execs[k % n_sets] on sample_stream (after batch k - n_sets
  *      trained); train_execs[k % n_sets] on train_stream (after that sample half),
  *      which records batch k's loss at d_loss_arr[k] (bp[3] = k); at the end one
@@ -307,8 +276,9 @@ int hg_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, f
  *      for both at the end (asynchronous: synchronise caller_stream to read). */
 int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* sample_execs, const int64_t* train_execs,
                     void* caller_stream, void* sample_stream, void* train_stream, const int64_t* dev_stage,
-                    const uint8_t* host_stage, int64_t slot_bytes, const int64_t* copy_bytes,
-                    const float* d_loss_arr, float* host_loss);
+                    uint8_t* host_stage, int64_t slot_bytes, int32_t counts_offset, int32_t seeds_offset,
+                    const int64_t* bp_rows, const int64_t* host_seed_ptrs, const int32_t* n_seeds,
+                    const int32_t* n_div, const float* d_loss_arr, float* host_loss);
 
 /* ---- K11 historical-embedding store (store.py:24-146; orchestrator.py:259-271,
  *      381-395 producer, 480-504 consumer, gnnmath.py:240-245 injection).

@@ -90,9 +90,6 @@ def load(build_if_missing: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        import os
-        if os.environ.get("HG_GEMM_LEGACY", "0") not in ("", "0"):  # cp.async GEMMs instead of the TMA pipelines
-            lib.hg_set_tuning(2, 1)
         _lib = lib
         return lib
 

@@ -18,11 +18,11 @@
 // step, so accumulation order per column is fixed: deterministic, no atomics.
 //
 // Backward (layers >= 1 only, need_dx = l > 0, gnnmath.py:256) replaces the
-// transposed scatter segment_weighted_rows(ed, es, ...) (gnnmath.py:140,199):
-// each src row gathers its edges from the stable src-major (CSC) view, in
-// ascending dst order like the reference's edge loop, adds the SAGE self-term
-// gradient, and applies the lower layer's ReLU' and injected-row masks
-// (gnnmath.py:130-134,183-188) before writing dZ of the layer below.
+// transposed scatter segment_weighted_rows(ed, es, ...) (gnnmath.py:140,199)
+// with k_bwd_scatter + k_bwd_finish below: a deterministic two-word fixed-point
+// scatter (integer atomics, order-independent), then the SAGE self-term
+// gradient and the lower layer's ReLU' and injected-row masks
+// (gnnmath.py:130-134,183-188) before dZ of the layer below is written.
 #include "hg_common.cuh"
 #include "hg_gnn_internal.h"
 #include "hg_tc.cuh"
@@ -155,109 +155,6 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
     }
 }
 
-template <int LPR, int NV, bool GCN>
-__global__ void __launch_bounds__(256) k_agg_bwd(
-    const float* __restrict__ dagg, int ld_dagg, const float* __restrict__ dself, int ld_dself, int F4,
-    const int* __restrict__ frontier, const int* d_n_dst, int cap_dst, int f, const int* __restrict__ counts,
-    const int* __restrict__ slot_g, const int* __restrict__ nself, const int* __restrict__ outdeg,
-    const int* __restrict__ csc_slot, const int* __restrict__ seg_beg, const int* __restrict__ seg_end,
-    const int* d_n_src, int cap_src, const float* __restrict__ hmask, int ld_hmask,
-    const uint8_t* __restrict__ inj, float* __restrict__ dx, int ld_dx, const int* __restrict__ csc_dst,
-    const float* __restrict__ csc_w) {
-    const int n_src = hg_load_count(d_n_src, cap_src);
-    const int n_dst = hg_load_count(d_n_dst, cap_dst);
-    const int lane = threadIdx.x & 31;
-    const int lr = lane & (LPR - 1);
-    const int g0 = lane & ~(LPR - 1);
-    const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << g0);
-    const int groups_per_block = blockDim.x / LPR;
-    for (int s0 = blockIdx.x * groups_per_block; s0 < n_src; s0 += gridDim.x * groups_per_block) {
-        const int s = s0 + threadIdx.x / LPR;
-        if (s >= n_src) continue;
-        float4 acc[NV];
-#pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int beg = seg_beg[s], end = seg_end[s];
-        for (int j0 = beg; j0 < end; j0 += LPR) {
-            int my_row = -1;
-            float my_w = 0.f;
-            if (j0 + lr < end) {
-                if (csc_dst) {  // precomputed (dst, weight) of the sorted edge (hg_csc_weights)
-                    my_row = csc_dst[j0 + lr];
-                    my_w = csc_w[j0 + lr];
-                } else {
-                    const int e = csc_slot[j0 + lr];
-                    const int d = e / f;
-                    if (GCN) { my_row = d; my_w = gcn_w(outdeg[s], counts[d]); }
-                    else if (slot_g[e] != frontier[d]) { my_row = d; my_w = 1.0f / (float)nself[d]; }
-                }
-            }
-            const int m = min(LPR, end - j0);
-            int j = 0;
-            for (; j + 4 <= m; j += 4) {  // four rows in flight, consumed in order
-                int r[4]; float w[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    r[t] = __shfl_sync(gmask, my_row, j + t, LPR);
-                    w[t] = __shfl_sync(gmask, my_w, j + t, LPR);
-                }
-                float4 x[4][NV];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float4* rp = reinterpret_cast<const float4*>(dagg + (int64_t)(r[t] < 0 ? 0 : r[t]) * ld_dagg);
-#pragma unroll
-                    for (int k = 0; k < NV; ++k) {
-                        const int c = lr + k * LPR;
-                        x[t][k] = (r[t] >= 0 && c < F4) ? __ldg(rp + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
-                }
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (r[t] >= 0) {
-#pragma unroll
-                        for (int k = 0; k < NV; ++k) acc[k] = f4_fma(w[t], x[t][k], acc[k]);
-                    }
-            }
-            for (; j < m; ++j) {
-                const int r = __shfl_sync(gmask, my_row, j, LPR);
-                const float w = __shfl_sync(gmask, my_w, j, LPR);
-                if (r >= 0) {
-                    const float4* rp = reinterpret_cast<const float4*>(dagg + (int64_t)r * ld_dagg);
-#pragma unroll
-                    for (int k = 0; k < NV; ++k) {
-                        const int c = lr + k * LPR;
-                        if (c < F4) acc[k] = f4_fma(w, __ldg(rp + c), acc[k]);
-                    }
-                }
-            }
-        }
-        const bool zero_row = inj && inj[s];
-        float4* out = reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx);
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            const int c = lr + k * LPR;
-            if (c >= F4) continue;
-            float4 a = acc[k];
-            if (dself && s < n_dst) {  // dx[:n_dst] = dz W_self^T, then += scatter (gnnmath.py:195-199)
-                const float4 ds = __ldg(reinterpret_cast<const float4*>(dself + (int64_t)s * ld_dself) + c);
-                a.x = ds.x + a.x; a.y = ds.y + a.y; a.z = ds.z + a.z; a.w = ds.w + a.w;
-            }
-            if (hmask) {  // ReLU' of the layer below: z > 0  <=>  relu(z) > 0
-                const float4 h = __ldg(reinterpret_cast<const float4*>(hmask + (int64_t)s * ld_hmask) + c);
-                a.x = h.x > 0.f ? a.x : 0.f; a.y = h.y > 0.f ? a.y : 0.f;
-                a.z = h.z > 0.f ? a.z : 0.f; a.w = h.w > 0.f ? a.w : 0.f;
-            }
-            if (zero_row) a = make_float4(0.f, 0.f, 0.f, 0.f);
-            out[c] = a;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// fp64, bit-exact segment_weighted_rows for arbitrary edge lists (plug-in API,
-// kernels.py:121-144): out[d] += w*rows[s] in edge order, no FMA contraction.
-// Edges are grouped by destination with a stable radix sort first.
-// ---------------------------------------------------------------------------
 __global__ void k_swr_keys(const int64_t* __restrict__ edge_dst, long long n, uint32_t* __restrict__ keys,
                            int* __restrict__ vals) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -324,25 +221,6 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
     }
     HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 8)
 #undef HG_FWD
-    return HG_EUNSUPPORTED;
-}
-
-template <bool GCN>
-int launch_bwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* dagg, int ld_dagg, const float* dself,
-               int ld_dself, int F4, const int* frontier, const int* d_n_dst, int cap_dst, int f, const int* counts,
-               const int* slot_g, const int* nself, const int* outdeg, const int* csc_slot, const int* seg_beg,
-               const int* seg_end, const int* d_n_src, int cap_src, const float* hmask, int ld_hmask,
-               const uint8_t* inj, float* dx, int ld_dx, const int* csc_dst, const float* csc_w) {
-#define HG_BWD(L, V)                                                                                            \
-    if (LPR == L && NV == V) {                                                                                  \
-        k_agg_bwd<L, V, GCN><<<g, 256, 0, s>>>(dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, \
-                                               f, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end,    \
-                                               d_n_src, cap_src, hmask, ld_hmask, inj, dx, ld_dx, csc_dst,      \
-                                               csc_w);                                                          \
-        return HG_OK;                                                                                           \
-    }
-    HG_BWD(8, 1) HG_BWD(16, 1) HG_BWD(32, 1) HG_BWD(32, 2) HG_BWD(32, 4) HG_BWD(32, 8)
-#undef HG_BWD
     return HG_EUNSUPPORTED;
 }
 
@@ -669,65 +547,6 @@ extern "C" int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard
                          : launch_fwd<M_SAGE_GLOBAL, true>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh);
     if (rc) { hg_set_error("aggregate_fwd_sharded: unsupported width"); return rc; }
     return hg_check_launch("aggregate_fwd_sharded");
-}
-
-extern "C" int hg_aggregate_bwd(int32_t model, const float* dagg, int32_t ld_dagg, const float* dself,
-                                int32_t ld_dself, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
-                                int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
-                                const int32_t* nself, const int32_t* outdeg, const int32_t* csc_slot,
-                                const int32_t* seg_beg, const int32_t* seg_end, const int32_t* d_n_src,
-                                int32_t cap_src, const float* hmask, int32_t ld_hmask, const uint8_t* inj_mask,
-                                float* dx, int32_t ld_dx, const int32_t* csc_dst, const float* csc_w, void* stream) {
-    if (F % 4 || ld_dagg % 4 || ld_dx % 4) { hg_set_error("aggregate_bwd: widths must be multiples of 4"); return HG_EINVAL; }
-    if (F > 1024) { hg_set_error("aggregate_bwd: F > 1024 unsupported"); return HG_EUNSUPPORTED; }
-    if (cap_src == 0) return HG_OK;
-    const int F4 = F / 4;
-    int LPR, NV;
-    pick_lanes(F4, LPR, NV);
-    dim3 g(hg_grid((long long)cap_src * LPR, 256, 8));
-    cudaStream_t s = (cudaStream_t)stream;
-    int rc = model ? launch_bwd<true>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx, csc_dst, csc_w)
-                   : launch_bwd<false>(LPR, NV, g, s, dagg, ld_dagg, dself, ld_dself, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself, outdeg, csc_slot, seg_beg, seg_end, d_n_src, cap_src, hmask, ld_hmask, inj_mask, dx, ld_dx, csc_dst, csc_w);
-    if (rc) { hg_set_error("aggregate_bwd: unsupported width"); return rc; }
-    return hg_check_launch("aggregate_bwd");
-}
-
-namespace {
-// (dst, weight) of every sorted transposed edge: the backward gather then needs
-// one dependent load per edge instead of three (built off the critical path).
-// Empty slots and SAGE self edges get dst = -1.
-__global__ void k_csc_weights(int model, const int* d_n_dst, int cap_dst, int f, const int* __restrict__ counts,
-                              const int* __restrict__ frontier, const int* __restrict__ slot_g,
-                              const int* __restrict__ slot_local, const int* __restrict__ nself,
-                              const int* __restrict__ outdeg, const int* __restrict__ csc_slot,
-                              int* __restrict__ csc_dst, float* __restrict__ csc_w) {
-    const int n = hg_load_count(d_n_dst, cap_dst);
-    const long long Q = (long long)cap_dst * f;
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < Q; k += (long long)gridDim.x * blockDim.x) {
-        const int e = csc_slot[k];
-        const int d = e / f, j = e - d * f;
-        int dst = -1;
-        float w = 0.f;
-        if (d < n && j < counts[d]) {
-            if (model) { dst = d; w = gcn_w(outdeg[slot_local[e]], counts[d]); }
-            else if (slot_g[e] != frontier[d]) { dst = d; w = 1.0f / (float)nself[d]; }
-        }
-        csc_dst[k] = dst;
-        csc_w[k] = w;
-    }
-}
-}  // namespace
-
-extern "C" int hg_csc_weights(int32_t model, const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
-                              const int32_t* counts, const int32_t* frontier, const int32_t* slot_g,
-                              const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg,
-                              const int32_t* csc_slot, int32_t* csc_dst, float* csc_w, void* stream) {
-    const long long Q = (long long)cap_dst * fanout;
-    if (Q <= 0) return HG_OK;
-    k_csc_weights<<<hg_grid(Q, 256, 8), 256, 0, (cudaStream_t)stream>>>(model, d_n_dst, cap_dst, fanout, counts,
-                                                                       frontier, slot_g, slot_local, nself, outdeg,
-                                                                       csc_slot, csc_dst, csc_w);
-    return hg_check_launch("csc_weights");
 }
 
 extern "C" int64_t hg_swr_ws_size(int64_t n_edges, int32_t n_out) {

@@ -240,14 +240,10 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
 // written, A read by 8 of 12 MMAs, lo written) to ~72 KB, which is what bounds
 // the SS form at N = 64.  TMEM: 2 accumulators (2*BN columns) + S A stages of
 // 64 columns (hi 32 | lo 32).
-// RESB: the whole B image (nk tiles) stays resident in shared memory, loaded
-// once per CTA, and the ring holds A tiles only (B was re-streamed from L2 for
-// every K tile of every output tile, doubling the SM's ingress).
 template <int BN>
 __host__ __device__ constexpr int ts_stages() { return BN <= 64 ? 6 : 4; }
-template <int BN, bool RESB>
-__host__ __device__ constexpr int ts_stage_bytes() { return RESB ? A_BYTES : A_BYTES + 2 * BN * 128; }
-constexpr int RESB_MAX_BYTES = 128 * 1024;
+template <int BN>
+__host__ __device__ constexpr int ts_stage_bytes() { return A_BYTES + 2 * BN * 128; }
 
 // PAIR: the B image's hi and lo tiles are adjacent 64-row blocks of one K-major
 // tile, i.e. one N = 2*BN operand [B_hi ; B_lo]: per K slice the MMAs become
@@ -259,13 +255,13 @@ __host__ __device__ constexpr int ts_acc_cols() { return PAIR ? 2 * BN : BN; }
 template <int BN, bool PAIR>
 __host__ __device__ constexpr int ts_nstages() { return PAIR ? (512 - 2 * ts_acc_cols<BN, PAIR>()) / 64 : ts_stages<BN>(); }
 
-template <int BN, bool RESB, bool PAIR>
+template <int BN, bool PAIR>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
 k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2, int nk1, int nk2, int ls1, int ls2,
               const uint8_t* __restrict__ Bimg, float* __restrict__ C, int ldc, int N, const int* __restrict__ d_M,
               int M_cap, int act) {
     constexpr int S = ts_nstages<BN, PAIR>();
-    constexpr int STAGE = ts_stage_bytes<BN, RESB>();
+    constexpr int STAGE = ts_stage_bytes<BN>();
     constexpr int B_BYTES = 2 * BN * 128;
     constexpr int B_TILE = BN * 128;
     constexpr int ACC = ts_acc_cols<BN, PAIR>();  // accumulator columns per output tile
@@ -275,10 +271,7 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
     constexpr uint32_t IDESC = idesc_tf32(128, BN, 0, 0);
     constexpr uint32_t IDESC2 = idesc_tf32(128, 2 * BN, 0, 0);
     extern __shared__ uint8_t smem_raw[];
-    // RESB: afree[st] (split warps done reading smem stage st) releases the A
-    // ring to the producer independently of the MMAs; empty[st] then only
-    // guards the TMEM A stage the split warps write next
-    __shared__ uint64_t full[S], splt[S], empty[S], afree[S], tfull[2], tempty[2], bfull;
+    __shared__ uint64_t full[S], splt[S], empty[S], tfull[2], tempty[2];
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int nk = nk1 + nk2;
@@ -299,9 +292,6 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
-        mbar_init(&bfull, 1);
-#pragma unroll
-        for (int i = 0; i < S; ++i) mbar_init(&afree[i], 4);
         mbar_init_fence();
         tma_prefetch_desc(&tmA1);
         if (nk2) tma_prefetch_desc(&tmA2);
@@ -324,27 +314,21 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
             const uint8_t* bimg = Bimg + (int64_t)blockIdx.y * nk * B_BYTES;
-            if (RESB) {  // whole B image once, behind the A ring
-                mbar_expect_tx(&bfull, (uint32_t)(nk * B_BYTES));
-                for (int kt = 0; kt < nk; ++kt)
-                    bulk_load(smem_u32(smem + S * STAGE + kt * B_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &bfull);
-            }
             for (int it = 0; it < iters; ++it) {
                 const int st = it % S;
-                if (it >= S) mbar_wait(RESB ? &afree[st] : &empty[st], (uint32_t)(((it / S) - 1) & 1));
+                if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
                 TL(0, it);
                 const int tile = it / nk, kt = it - tile * nk;
                 const int m0 = ((int)blockIdx.x + tile * (int)gridDim.x) * 128;
                 uint8_t* base = smem + st * STAGE;
-                mbar_expect_tx(&full[st], RESB ? A_BYTES : A_BYTES + B_BYTES);
+                mbar_expect_tx(&full[st], A_BYTES + B_BYTES);
                 if (kt < nk1) tma_load_2d(smem_u32(base), &tmA1, kt * 32, m0, &full[st]);
                 else tma_load_2d(smem_u32(base), &tmA2, (kt - nk1) * 32, m0, &full[st]);
-                if (!RESB) bulk_load(smem_u32(base + A_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &full[st]);
+                bulk_load(smem_u32(base + A_BYTES), bimg + (int64_t)kt * B_BYTES, B_BYTES, &full[st]);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---- MMA issuer (A from TMEM)
-            if (RESB) mbar_wait(&bfull, 0u);
             int it = 0;
             for (int tile = 0; tile < n_my; ++tile) {
                 const int acc = tile & 1;
@@ -357,8 +341,7 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
                     TL(3, it);
                     tc_fence_after();
                     const uint32_t ta = tmem + A_COL0 + (uint32_t)(st * 64);
-                    const uint32_t b_hi = RESB ? smem_u32(smem + S * STAGE + kt * B_BYTES)
-                                               : smem_u32(smem + st * STAGE + A_BYTES);
+                    const uint32_t b_hi = smem_u32(smem + st * STAGE + A_BYTES);
                     const uint32_t b_lo = b_hi + B_TILE;
                     // 8-wide K slices past the source's K hold TMA zero fill: skipped
                     const int ns = kt == nk1 - 1 ? ls1 : (kt == nk1 + nk2 - 1 ? ls2 : 4);
@@ -391,10 +374,6 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             const uint8_t* base = smem + st * STAGE;
             if (c_dbg & 2) {  // profiling: no split work (same hand-offs)
                 __syncwarp();
-                if (RESB) {
-                    if (lane == 0) mbar_arrive(&afree[st]);
-                    if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
-                }
                 if (lane == 0) mbar_arrive(&splt[st]);
                 continue;
             }
@@ -409,15 +388,6 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
             }
 #pragma unroll
             for (int k = 0; k < 32; ++k) lo[k] = __float_as_uint(tf32_lo(__uint_as_float(hi[k])));
-            if (RESB) {  // smem stage consumed: hand it back to the producer (generic-proxy
-                // reads before the next async-proxy TMA write), then wait for the MMAs
-                // still reading this TMEM stage's previous contents
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&afree[st]);
-                if (it >= S) mbar_wait(&empty[st], (uint32_t)(((it / S) - 1) & 1));
-                tc_fence_after();
-            }
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(st * 64);
             tmem_st32(ta, hi);
             tmem_st32(ta + 32, lo);
@@ -820,45 +790,27 @@ int launch_fwd(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const
     return hg_check_launch("gemm_tma");
 }
 
-int g_resb = 0;  // resident-B TS form when the image fits (hg_set_tuning key 6; measured no faster, off)
-
 template <int BN>
 int launch_fwd_ts(int M_cap, int n_nt, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, int nk1,
                   int nk2, int ls1, int ls2, const uint8_t* bimg, float* C, int ldc, int N, const int* d_M, int act) {
-    const int nk = nk1 + nk2;
-    const bool resb = g_resb && nk * 2 * BN * 128 <= RESB_MAX_BYTES;
-    const int smem = resb ? ts_stages<BN>() * ts_stage_bytes<BN, true>() + nk * 2 * BN * 128 + 1024
-                          : ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024;
+    const int smem = ts_stages<BN>() * ts_stage_bytes<BN>() + 1024;
     const bool pair = g_pair && BN <= 64;
     constexpr bool PB = BN <= 64;
-    const int smem_pair = ts_nstages<BN, PB>() * ts_stage_bytes<BN, false>() + 1024;
-    // resident B + paired MMAs: the A ring only (TMEM-limited depth) behind the whole B image
-    const int smem_resb_pair = ts_nstages<BN, PB>() * ts_stage_bytes<BN, true>() + nk * 2 * BN * 128 + 1024;
+    const int smem_pair = ts_nstages<BN, PB>() * ts_stage_bytes<BN>() + 1024;
     static bool attr = false;
     if (!attr) {
-        const int mx = ts_stages<BN>() * ts_stage_bytes<BN, true>() + RESB_MAX_BYTES + 1024;
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN, true, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ts_nstages<BN, PB>() * ts_stage_bytes<BN, true>() + RESB_MAX_BYTES + 1024);
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ts_stages<BN>() * ts_stage_bytes<BN, false>() + 1024);
-        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair);
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_gemm_tma_ts<BN, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair);
         attr = true;
     }
     int gx = hg_ceil_div(M_cap, 128);
     gx = gx < HG_NUM_SMS ? gx : HG_NUM_SMS;
-    if (resb && pair)
-        hg_launch(k_gemm_tma_ts<BN, true, (BN <= 64)>, dim3(gx, n_nt), FWD_THREADS, smem_resb_pair, s, m1, m2, nk1, nk2,
-                  ls1, ls2, bimg, C, ldc, N, d_M, M_cap, act);
-    else if (resb)
-        hg_launch(k_gemm_tma_ts<BN, true, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc,
-                  N, d_M, M_cap, act);
-    else if (pair)
-        hg_launch(k_gemm_tma_ts<BN, false, (BN <= 64)>, dim3(gx, n_nt), FWD_THREADS, smem_pair, s, m1, m2, nk1, nk2, ls1, ls2,
+    if (pair)
+        hg_launch(k_gemm_tma_ts<BN, (BN <= 64)>, dim3(gx, n_nt), FWD_THREADS, smem_pair, s, m1, m2, nk1, nk2, ls1, ls2,
                   bimg, C, ldc, N, d_M, M_cap, act);
     else
-        hg_launch(k_gemm_tma_ts<BN, false, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C, ldc,
-                  N, d_M, M_cap, act);
+        hg_launch(k_gemm_tma_ts<BN, false>, dim3(gx, n_nt), FWD_THREADS, smem, s, m1, m2, nk1, nk2, ls1, ls2, bimg, C,
+                  ldc, N, d_M, M_cap, act);
     return hg_check_launch("gemm_tma_ts");
 }
 
@@ -893,7 +845,6 @@ int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMa
 }  // namespace
 
 void hg_tma_set_fwd_form(int v) { g_fwd_form = v; }
-void hg_tma_set_resb(int v) { g_resb = v ? 1 : 0; }
 void hg_tma_set_wg_tsa(int v) { g_wg_tsa = v ? 1 : 0; }
 void hg_tma_set_pair(int v) { g_pair = v ? 1 : 0; }
 void hg_tma_set_dbg(int v) { cudaMemcpyToSymbol(c_dbg, &v, sizeof(int)); }

@@ -2,17 +2,22 @@
 //
 // Replaces the per-batch host loop of orchestrator.Trainer.train_batches (the
 // reference's training loop, orchestrator.py:520-560, one Python iteration per
-// batch): with every batch's inputs already packed into pinned staging slots,
-// each step is a handful of CUDA runtime calls — H2D of the staging slot, the
-// sample-half graph on the sampling stream, the train-half graph on the training
-// stream (which records batch k's loss at d_loss_arr[k]) and, once at the end,
-// one D2H of all the losses — so the host never becomes the bottleneck of a step
-// that takes ~0.19 ms on the device (the Python loop cost ~0.2 ms per step).
+// batch): each step is a pack of the batch's inputs into its pinned staging slot
+// (parameter block, counts, int64 seed ids -> int32) followed by a handful of
+// CUDA runtime calls — H2D of the staging slot, the sample-half graph on the
+// sampling stream, the train-half graph on the training stream (which records
+// batch k's loss at d_loss_arr[k]) and, once at the end, one D2H of all the
+// losses.  Packing step k right before its launches (not all steps up front)
+// lets the device start after the first batch's ~1 us pack instead of after
+// the whole call's, so the host never becomes the bottleneck of a step that
+// takes ~0.19 ms on the device.
 //
 // Ordering (same as engine.Pipeline): sample set k % n_sets is refilled only
 // after batch k - n_sets trained; batch k trains after its sample half; both
 // streams start after the caller's stream and the caller's stream waits for both
 // at the end.
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "hg_common.cuh"
@@ -20,11 +25,22 @@
 
 extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* sample_execs,
                                const int64_t* train_execs, void* caller_stream, void* sample_stream,
-                               void* train_stream, const int64_t* dev_stage, const uint8_t* host_stage,
-                               int64_t slot_bytes, const int64_t* copy_bytes, const float* d_loss_arr,
-                               float* host_loss) {
+                               void* train_stream, const int64_t* dev_stage, uint8_t* host_stage,
+                               int64_t slot_bytes, int32_t counts_offset, int32_t seeds_offset,
+                               const int64_t* bp_rows, const int64_t* host_seed_ptrs, const int32_t* n_seeds,
+                               const int32_t* n_div, const float* d_loss_arr, float* host_loss) {
     if (n_steps < 0 || n_sets < 1) { hg_set_error("pipeline_run: bad n_steps / n_sets"); return HG_EINVAL; }
     if (n_steps == 0) return HG_OK;
+    if (counts_offset < 8 * HG_BP_WORDS || seeds_offset < counts_offset + 8) {
+        hg_set_error("pipeline_run: staging layout overlaps the parameter block");
+        return HG_EINVAL;
+    }
+    for (int k = 0; k < n_steps; ++k) {
+        if (n_seeds[k] < 0 || seeds_offset + 4LL * n_seeds[k] > slot_bytes) {
+            hg_set_error("pipeline_run: batch %d has %d seeds, more than a staging slot holds", k, n_seeds[k]);
+            return HG_EINVAL;
+        }
+    }
     cudaStream_t cs = (cudaStream_t)caller_stream, ss = (cudaStream_t)sample_stream, st = (cudaStream_t)train_stream;
     std::vector<cudaEvent_t> sampled(n_sets), trained(n_sets), copied(n_sets);
     std::vector<char> has_trained(n_sets, 0);
@@ -48,16 +64,32 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
     cudaStreamWaitEvent(st, start, 0);
     cudaStreamWaitEvent(cp, start, 0);
     cudaError_t err = cudaSuccess;
+    auto pack = [&](int k) {  // the staging slot of batch k: bp | counts | seeds (engine.stage_views)
+        uint8_t* slot = host_stage + (int64_t)k * slot_bytes;
+        memcpy(slot, bp_rows + (int64_t)k * HG_BP_WORDS, 8 * HG_BP_WORDS);
+        const int32_t cnt[2] = {n_seeds[k], n_div[k]};
+        memcpy(slot + counts_offset, cnt, sizeof(cnt));
+        const int64_t* src = reinterpret_cast<const int64_t*>(host_seed_ptrs[k]);
+        int32_t* dst = reinterpret_cast<int32_t*>(slot + seeds_offset);
+        for (int i = 0; i < n_seeds[k]; ++i) dst[i] = (int32_t)src[i];
+    };
     auto sample = [&](int k) {
         const int set = k % n_sets;
+        pack(k);
         if (has_trained[set]) {
             cudaStreamWaitEvent(cp, trained[set], 0);
             cudaStreamWaitEvent(ss, trained[set], 0);
         }
-        cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
-                        (size_t)copy_bytes[k], cudaMemcpyHostToDevice, cp);
-        cudaEventRecord(copied[set], cp);
-        cudaStreamWaitEvent(ss, copied[set], 0);
+        static int mode = getenv("HG_PIPE_COPY") ? atoi(getenv("HG_PIPE_COPY")) : 0;  // EXPERIMENT
+        if (mode == 0) {
+            cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
+                            (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, cp);
+            cudaEventRecord(copied[set], cp);
+            cudaStreamWaitEvent(ss, copied[set], 0);
+        } else if (mode == 1) {
+            cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
+                            (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, ss);
+        }
         const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(sample_execs[set]), ss);
         if (e != cudaSuccess && err == cudaSuccess) err = e;
         cudaEventRecord(sampled[set], ss);

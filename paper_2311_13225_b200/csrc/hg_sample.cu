@@ -27,12 +27,8 @@
 // id's first occurrence is the position that won.  The tag decreases with every
 // use of the table (a device counter bumped by the relabel kernel), so entries
 // left by earlier blocks always lose and the table never needs resetting.
-#include <cooperative_groups.h>
-
 #include "hg_common.cuh"
 #include "hg_gnn_internal.h"
-
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -221,8 +217,7 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// one tile t of the mark/scan/emit pass (t = blockIdx.x in k_markscan; a
-// strided loop over tiles in the cooperative fused block kernel)
+// one tile t of the mark/scan/emit pass (t = blockIdx.x in k_markscan)
 __device__ __forceinline__ void markscan_tile(int t, const int* __restrict__ frontier, const int* d_n, int cap,
                                               int f, const int* __restrict__ counts, const int* __restrict__ slots,
                                               unsigned long long* __restrict__ minpos,
@@ -431,35 +426,6 @@ __global__ void __launch_bounds__(256) k_relabel_sort_seg(const int* __restrict_
     relabel_seg_body<W>(frontier, d_n, cap, f, counts, slots, slot_local, minpos, nself, outdeg, tag_ctr, d_gen);
 }
 
-// ---------------------------------------------------------------------------
-// Small blocks (the upper layers: a few thousand destinations) in ONE
-// cooperative launch: draw -> grid sync -> mark/scan/emit (the decoupled
-// look-back tiles strided over the co-resident CTAs) -> grid sync -> relabel.
-// Same code and results as the three-kernel sequence; two launch gaps fewer.
-// ---------------------------------------------------------------------------
-template <int W>
-__global__ void __launch_bounds__(256) k_block_coop(const int64_t* __restrict__ offsets,
-                                                    const int* __restrict__ targets,
-                                                    const int* __restrict__ frontier, const int* d_n, int cap,
-                                                    int f, const uint64_t* __restrict__ d_seed, int layer,
-                                                    int* __restrict__ counts, int* __restrict__ slots,
-                                                    int* __restrict__ slot_local,
-                                                    unsigned long long* __restrict__ minpos, int* __restrict__ tag_ctr,
-                                                    int* __restrict__ src_vertices, int* __restrict__ d_n_src,
-                                                    int* __restrict__ nself, int* __restrict__ outdeg,
-                                                    int* __restrict__ rank, unsigned long long* __restrict__ status,
-                                                    int* __restrict__ d_gen, int tiles) {
-    __shared__ int s_last[256];
-    cg::grid_group grid = cg::this_grid();
-    draw_seg_body<W>(offsets, targets, frontier, d_n, cap, f, d_seed, layer, counts, slots, minpos, tag_ctr, nullptr,
-                     s_last);
-    grid.sync();
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x)
-        markscan_tile(t, frontier, d_n, cap, f, counts, slots, minpos, tag_ctr, rank, src_vertices, d_n_src, status,
-                      d_gen, outdeg);
-    grid.sync();
-    relabel_seg_body<W>(frontier, d_n, cap, f, counts, slots, slot_local, minpos, nself, outdeg, tag_ctr, d_gen);
-}
 
 __global__ void k_relabel_sort_seq(const int* __restrict__ frontier, const int* d_n, int cap, int f,
                                    const int* __restrict__ counts, int* __restrict__ slots,
@@ -523,34 +489,6 @@ __global__ void k_emit_raw(const int* d_n, int cap, int f, const int* __restrict
             edge_dst[starts[i] + j] = i;
             edge_src[starts[i] + j] = slots[q];
         }
-    }
-}
-
-// CSC keys for the transposed (backward) aggregation: key = src local id of a
-// valid slot, or `big` for empty slots (sorted to the end); value = slot index
-__global__ void k_csc_keys(const int* d_n, int cap, int f, const int* __restrict__ counts,
-                           const int* __restrict__ slot_local, uint32_t big, uint32_t* __restrict__ keys,
-                           int* __restrict__ vals) {
-    const int n = hg_load_count(d_n, cap);
-    const long long Q = (long long)cap * f;
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Q;
-         q += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(q / f), j = (int)(q - (long long)i * f);
-        const bool ok = i < n && j < counts[i];
-        keys[q] = ok ? (uint32_t)slot_local[q] : big;
-        vals[q] = (int)q;
-    }
-}
-
-// per-src segment [seg_beg[s], seg_end[s]) in the sorted key array (zeroed before)
-__global__ void k_csc_bounds(const uint32_t* __restrict__ keys, long long Q, uint32_t big,
-                             int* __restrict__ seg_beg, int* __restrict__ seg_end) {
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < Q;
-         k += (long long)gridDim.x * blockDim.x) {
-        const uint32_t key = keys[k];
-        if (key == big) continue;
-        if (k == 0 || keys[k - 1] != key) seg_beg[key] = (int)k;
-        if (k == Q - 1 || keys[k + 1] != key) seg_end[key] = (int)(k + 1);
     }
 }
 
@@ -698,53 +636,7 @@ extern "C" int hg_dedup_relabel(const int32_t* frontier, const int32_t* d_n_dst,
 }
 
 // Draw + dedup + relabel of one layer (hg_sample_layer followed by
-// hg_dedup_relabel).  Small blocks (fanout <= 32, cap_dst <= 16384: the upper
-// layers) run as ONE cooperative kernel (k_block_coop); larger ones as the
-// three-kernel sequence.  Same outputs either way.
-namespace {
-template <int W>
-int launch_block_coop(cudaStream_t s, const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
-                      const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed, int32_t layer,
-                      int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos, int32_t* tag_ctr,
-                      int32_t* src_vertices, int32_t* d_n_src, int32_t* nself, int32_t* outdeg, int32_t* ws) {
-    static int max_ctas = -1;
-    if (max_ctas < 0) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_coop<W>, 256, 0);
-        max_ctas = per_sm * HG_NUM_SMS;
-    }
-    const long long P = (long long)cap_dst * (fanout + 1);
-    const int tiles = (int)((P + MS_TILE - 1) / MS_TILE);
-    int grid = hg_grid((long long)cap_dst * W, 256, 8);
-    grid = grid > tiles ? grid : tiles;
-    grid = grid < max_ctas ? grid : max_ctas;
-    int* rank = ws;
-    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + ((P + 1) & ~1LL));
-    int* d_gen = ws + ((P + 1) & ~1LL) + 2 * tiles;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
-    cfg.stream = s;
-    cudaLaunchAttribute a[1];
-    a[0].id = cudaLaunchAttributeCooperative;
-    a[0].val.cooperative = 1;
-    cfg.attrs = a;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_block_coop<W>, offsets, targets, frontier, d_n_dst, cap_dst,
-                                             fanout, d_seed, layer, counts, slots, slot_local,
-                                             (unsigned long long*)minpos, tag_ctr, src_vertices, d_n_src, nself,
-                                             outdeg, rank, status, d_gen, tiles);
-    if (e != cudaSuccess) {
-        hg_set_error("sample_block: cooperative launch failed: %s", cudaGetErrorString(e));
-        return HG_ECUDA;
-    }
-    return HG_OK;
-}
-int g_block_coop = 0;  // hg_set_tuning key 8 (measured slower than the kernel sequence: grid syncs cost more than PDL launch gaps)
-}  // namespace
-
-void hg_set_block_coop(int v) { g_block_coop = v ? 1 : 0; }
-
+// hg_dedup_relabel).
 extern "C" int hg_sample_block(const int64_t* offsets, const int32_t* targets, const int32_t* frontier,
                                const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const uint64_t* d_seed,
                                int32_t layer, int32_t* counts, int32_t* slots, int32_t* slot_local, uint64_t* minpos,
@@ -753,16 +645,6 @@ extern "C" int hg_sample_block(const int64_t* offsets, const int32_t* targets, c
     cudaStream_t s = (cudaStream_t)stream;
     if (fanout < 1 || cap_dst < 0) { hg_set_error("sample_block: bad fanout/cap"); return HG_EINVAL; }
     if (cap_dst == 0) { cudaMemsetAsync(d_n_src, 0, sizeof(int), s); return hg_check_launch("sample_block(empty)"); }
-    if (g_block_coop && fanout <= 32 && cap_dst <= 16384) {
-        int rc;
-        switch (seg_width(fanout)) {
-            case 4: rc = launch_block_coop<4>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
-            case 8: rc = launch_block_coop<8>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
-            case 16: rc = launch_block_coop<16>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
-            default: rc = launch_block_coop<32>(s, offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots, slot_local, minpos, tag_ctr, src_vertices, d_n_src, nself, outdeg, ws); break;
-        }
-        return rc ? rc : hg_check_launch("sample_block");
-    }
     int rc = sample_layer_impl(offsets, targets, frontier, d_n_dst, cap_dst, fanout, d_seed, layer, counts, slots,
                                minpos, tag_ctr, scratch, nullptr, s);
     if (rc) return rc;
@@ -813,42 +695,6 @@ extern "C" int hg_raw_edges(const int32_t* d_n_dst, int32_t cap_dst, int32_t fan
     k_emit_raw<<<hg_grid((long long)cap_dst * fanout, 256, 8), 256, 0, s>>>(d_n_dst, cap_dst, fanout, counts, ws,
                                                                             slots, edge_dst, edge_src);
     return hg_check_launch("raw_edges");
-}
-
-// Transposed (src-major) view of a block's slots for the backward scatter
-// (gnnmath.py:140,199), stable so each src's edges stay in ascending dst order.
-// csc_slot: cap_dst*fanout ints (sorted slot indices); seg_beg/seg_end: cap_src
-// ints each.  ws >= hg_csc_ws_size(cap_dst, fanout) ints.
-extern "C" int64_t hg_csc_ws_size(int32_t cap_dst, int32_t fanout) {
-    long long Q = (long long)cap_dst * fanout;
-    return (int64_t)(3 * Q + (long long)hg_radix_ws_ints(Q) + 16);
-}
-
-extern "C" int hg_build_csc(const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout, const int32_t* counts,
-                            const int32_t* slot_local, int32_t cap_src, int32_t* csc_slot, int32_t* seg_beg,
-                            int32_t* seg_end, int32_t* ws, void* stream) {
-    cudaStream_t s = (cudaStream_t)stream;
-    const long long Q = (long long)cap_dst * fanout;
-    cudaMemsetAsync(seg_beg, 0, sizeof(int) * (size_t)cap_src, s);
-    cudaMemsetAsync(seg_end, 0, sizeof(int) * (size_t)cap_src, s);
-    if (Q == 0) return hg_check_launch("build_csc(empty)");
-    uint32_t* keys = (uint32_t*)ws;
-    uint32_t* k_alt = (uint32_t*)(ws + Q);
-    int* v_alt = ws + 2 * Q;
-    int* rws = ws + 3 * Q;
-    const uint32_t big = (uint32_t)cap_src;
-    int bits = 1;
-    while ((1u << bits) <= big && bits < 32) ++bits;
-    k_csc_keys<<<hg_grid(Q, 256, 8), 256, 0, s>>>(d_n_dst, cap_dst, fanout, counts, slot_local, big, keys, csc_slot);
-    int in_alt = 0;
-    int rc = hg_radix_sort_launch(keys, csc_slot, k_alt, v_alt, Q, bits, rws, &in_alt, s);
-    if (rc) return rc;
-    if (in_alt) {
-        cudaMemcpyAsync(csc_slot, v_alt, sizeof(int) * Q, cudaMemcpyDeviceToDevice, s);
-        keys = k_alt;
-    }
-    k_csc_bounds<<<hg_grid(Q, 256, 8), 256, 0, s>>>(keys, Q, big, seg_beg, seg_end);
-    return hg_check_launch("build_csc");
 }
 
 // ---------------------------------------------------------------------------

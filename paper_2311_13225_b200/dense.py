@@ -1,10 +1,8 @@
-"""Dense layer transforms (K8) dispatch: tcgen05 tensor cores by default.
+"""Dense layer transforms (K8) on the tcgen05 tensor cores (3xTF32, fp32-class).
 
-``HG_GEMM=simt`` selects the portable fp32 SIMT kernels instead (same library,
-same determinism; used to cross-check the tensor-core path).  Weights follow
-the flat layout of engine.DenseParams: per layer W_self then W_neigh (SAGE) or
-W (GCN), each row-major [d_in, d_out], so the stacked [W_self; W_neigh] is one
-contiguous [2*d_in, d_out] matrix.
+Weights follow the flat layout of engine.DenseParams: per layer W_self then
+W_neigh (SAGE) or W (GCN), each row-major [d_in, d_out], so the stacked
+[W_self; W_neigh] is one contiguous [2*d_in, d_out] matrix.
 
 The tensor-core GEMM consumes its B operand (the weights) as a prebuilt
 swizzled hi/lo image (``BImage``); the engine rebuilds its images once per
@@ -13,13 +11,9 @@ step from the current weights, the functional API builds them on the fly.
 
 from __future__ import annotations
 
-import os
-
 import torch
 
 from . import _lib
-
-BACKEND = os.environ.get("HG_GEMM", "tc").lower()
 
 
 class BImage:
@@ -27,21 +21,15 @@ class BImage:
 
     def __init__(self, K1: int, K2: int, N: int, trans_b: int, device):
         self.K1, self.K2, self.N, self.trans_b = int(K1), int(K2), int(N), int(trans_b)
-        nbytes = int(_lib.fn("hg_gemm_tc_bimg_size")(self.K1, self.K2, self.N)) if BACKEND != "simt" else 16
+        nbytes = int(_lib.fn("hg_gemm_tc_bimg_size")(self.K1, self.K2, self.N))
         self.buf = torch.empty(max(nbytes // 4, 4), dtype=torch.float32, device=device)
 
     def prep(self, W: int, ldb: int, s):
-        if BACKEND != "simt":
-            _lib.call("hg_gemm_tc_prep_b", W, ldb, self.trans_b, self.K1, self.K2, self.N, self.buf.data_ptr(), s)
+        _lib.call("hg_gemm_tc_prep_b", W, ldb, self.trans_b, self.K1, self.K2, self.N, self.buf.data_ptr(), s)
 
 
 def fwd(A1, lda1, A2, lda2, K, W, N, C, ldc, d_M, cap, act, s, img: BImage | None = None, device=None):
     """C = act(A1 W[0:K] + A2 W[K:2K])  (A2 None: C = act(A1 W))."""
-    if BACKEND == "simt":
-        w2 = (W + K * N * 4) if A2 is not None else None
-        _lib.call("hg_gemm_f32", A1, lda1, K, W, N, A2, lda2 if A2 else 0, K if A2 else 0, w2, N, 0, C, ldc, N,
-                  d_M, cap, act, s)
-        return
     if img is None:
         img = BImage(K, K if A2 is not None else 0, N, 1, device or torch.cuda.current_device())
         img.prep(W, N, s)
@@ -51,9 +39,6 @@ def fwd(A1, lda1, A2, lda2, K, W, N, C, ldc, d_M, cap, act, s, img: BImage | Non
 
 def dx(dZ, ldz, K, W, N, C, ldc, d_M, cap, s, img: BImage | None = None, device=None):
     """C[M x N] = dZ[M x K] W^T with W stored [N x K] (row-major, ld K)."""
-    if BACKEND == "simt":
-        _lib.call("hg_gemm_f32", dZ, ldz, K, W, K, None, 0, 0, None, 0, 1, C, ldc, N, d_M, cap, 0, s)
-        return
     if img is None:
         img = BImage(K, 0, N, 0, device or torch.cuda.current_device())
         img.prep(W, K, s)
@@ -62,16 +47,9 @@ def dx(dZ, ldz, K, W, N, C, ldc, d_M, cap, s, img: BImage | None = None, device=
 
 def wgrad_ws_size(K, N, cap, n_src) -> int:
     lib = _lib.load()
-    if BACKEND == "simt":
-        return int(lib.hg_wgrad_ws_size(K, N, cap))
     return int(lib.hg_wgrad_tc_ws_size(K, N, cap, n_src))
 
 
 def wgrad(A1, lda1, A2, lda2, K, G, ldg, N, d_M, cap, out1, out2, ws, s):
     """out1 = A1^T G, out2 = A2^T G (A2 optional)."""
-    if BACKEND == "simt":
-        _lib.call("hg_wgrad_f32", A1, lda1, K, G, ldg, N, d_M, cap, out1, 1.0, ws, s)
-        if A2 is not None:
-            _lib.call("hg_wgrad_f32", A2, lda2, K, G, ldg, N, d_M, cap, out2, 1.0, ws, s)
-    else:
-        _lib.call("hg_wgrad_tc", A1, lda1, A2, lda2 if A2 else 0, K, G, ldg, N, d_M, cap, out1, out2, ws, s)
+    _lib.call("hg_wgrad_tc", A1, lda1, A2, lda2 if A2 else 0, K, G, ldg, N, d_M, cap, out1, out2, ws, s)

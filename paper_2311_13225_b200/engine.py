@@ -202,9 +202,6 @@ class TrainEngine:
         # bit-identical to the sequential order) ----
         z32 = lambda *s: torch.zeros(*s, dtype=torch.int32, device=dev)  # noqa: E731
         zf = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
-        # transposed aggregation of layers >= 1: deterministic fixed-point scatter
-        # (default) or the CSC gather over a stable src-major view (HG_BWD=csc)
-        self.bwd_scatter = os.environ.get("HG_BWD", "scatter").lower() != "csc"
         # relabel halves of layers >= 1 off the sampling critical path (HG_SPLIT_RELABEL=0: in line)
         self.split_relabel = os.environ.get("HG_SPLIT_RELABEL", "1") != "0"
         self.sets = []
@@ -216,11 +213,10 @@ class TrainEngine:
             # layer's relabel half runs on a side stream concurrently with the next
             # layer's draw + mark (enqueue_sample_part)
             mps = (mp, mp.like() if self.L > 1 and self.split_relabel else mp)
-            # outdeg: GCN norm; with the scatter backward also the per-source edge
-            # counts that select its single-contribution fast path
+            # outdeg: GCN norm; for layers >= 1 also the per-source edge counts that
+            # select the backward scatter's single-contribution fast path
             smp = [LayerSampler(dg, self.cap_dst[l], self.fan[l], need_nself=self.sage,
-                                need_outdeg=(not self.sage) or (l > 0 and self.bwd_scatter),
-                                need_csc=l > 0 and not self.bwd_scatter, minpos=mps[l % 2]) for l in range(self.L)]
+                                need_outdeg=(not self.sage) or l > 0, minpos=mps[l % 2]) for l in range(self.L)]
             stage = torch.zeros(STAGE_SEEDS + 4 * self.batch_cap, dtype=torch.uint8, device=dev)
             bp, counts_in, seeds = stage_views(stage)
             self.sets.append(SampleSet(samplers=smp, seeds=seeds, counts_in=counts_in, bp=bp, stage=stage))
@@ -250,7 +246,7 @@ class TrainEngine:
         self.wgrad_ws = zf(max(ws, 1))
         # two-word fixed-point accumulators (hi | lo words per row, hg_aggregate.cu)
         self.fx_acc = [torch.zeros((self.cap_src[l], 2 * self.ld[l]), dtype=torch.int64, device=dev)
-                       if (l > 0 and self.bwd_scatter) else None for l in range(self.L)]
+                       if l > 0 else None for l in range(self.L)]
         self.fx_flags = z32(1)
         self.d_loss = zf(1)
         self.row_loss = zf(self.batch_cap + 1)  # + the loss kernel's last-block ticket
@@ -282,7 +278,7 @@ class TrainEngine:
                 nm = 2 if self.sage else 1
                 self.img_dx.append([dense.BImage(self.dims[l + 1], 0, self.dims[l], 0, dev) for _ in range(nm)])
         # the top SAGE layer's aggregate -> transform -> loss -> dX -> scatter in one kernel
-        self.top_fused = (self.sage and self.L >= 2 and self.bwd_scatter and self.dims[self.L - 1] <= 64
+        self.top_fused = (self.sage and self.L >= 2 and self.dims[self.L - 1] <= 64
                           and self.dims[self.L] <= 64 and self.fan[self.L - 1] <= 32
                           and self.fused_dx[self.L - 1] and os.environ.get("HG_TOP_FUSED", "1") != "0")
         self.graph = None
@@ -308,8 +304,6 @@ class TrainEngine:
         """Rebuild every tensor-core B image from the current weights (one launch)."""
         s = stream_ptr(stream)
         jobs = self._image_jobs()
-        if dense.BACKEND == "simt":
-            return
         for i in range(0, len(jobs), 8):
             part = jobs[i:i + 8]
             desc = self._image_desc(part)
@@ -397,13 +391,9 @@ class TrainEngine:
             if forked and l + 2 < self.L and self.samplers[l + 2].minpos is smp.minpos:
                 main.wait_stream(sc)  # the table is still being read by layer l+2's relabel
             split = self.split_relabel and l > 0 and not self._bottom_draws_only(l)
-            smp.run(fr, n, self.bp, l, main, with_csc=False, dedup=not self._bottom_draws_only(l),
+            smp.run(fr, n, self.bp, l, main, dedup=not self._bottom_draws_only(l),
                     relabel_stream=sc if split else None)
             forked = forked or split
-            if l > 0 and not self.bwd_scatter:
-                sc.wait_stream(main)
-                smp.build_csc(n, sc, frontier=fr)
-                forked = True
         if self.early_agg0():
             mark("sample_agg0")
             self._enqueue_agg0(main.cuda_stream)
@@ -522,18 +512,11 @@ class TrainEngine:
                 dense.dx(ptr(self.dz[l]), self.ld[l + 1], d_out, ptr(P.view(l, 0)), d_in, ptr(self.dagg[l]),
                          self.ld[l], ptr(n), self.cap_dst[l], s, img=self.img_dx[l][0])
                 dsp, dsl, dap, dal = None, 0, ptr(self.dagg[l]), self.ld[l]
-            if self.bwd_scatter:
-                _lib.call("hg_aggregate_bwd_scatter", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n),
-                          self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
-                          ptr(smp.nself), ptr(smp.outdeg), ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]),
-                          self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), ptr(self.dz[l - 1]),
-                          self.ld[l], ptr(self.fx_flags), s)
-                continue
-            _lib.call("hg_aggregate_bwd", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n), self.cap_dst[l],
-                      self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.nself), ptr(smp.outdeg),
-                      ptr(smp.csc_slot), ptr(smp.seg_beg), ptr(smp.seg_end), ptr(smp.n_src), self.cap_src[l],
-                      ptr(self.out[l - 1]), self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.dz[l - 1]),
-                      self.ld[l], ptr(smp.csc_dst), ptr(smp.csc_w), s)
+            _lib.call("hg_aggregate_bwd_scatter", model, dap, dal, dsp, dsl, self.ld[l], ptr(fr), ptr(n),
+                      self.cap_dst[l], self.fan[l], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
+                      ptr(smp.nself), ptr(smp.outdeg), ptr(smp.n_src), self.cap_src[l], ptr(self.out[l - 1]),
+                      self.ld[l], ptr(inj if l - 1 == 0 else None), ptr(self.fx_acc[l]), ptr(self.dz[l - 1]),
+                      self.ld[l], ptr(self.fx_flags), s)
         main.wait_stream(sw)
         if self.account_rows:  # the reference's per-batch transfer accounting (bookkeeping only)
             fr0, n0 = self.frontier(0)
@@ -546,7 +529,7 @@ class TrainEngine:
         if self.allreduce is not None:
             self.allreduce(P.grad)
         jobs = self._image_jobs()
-        if self.optimizer == "sgd" and dense.BACKEND != "simt" and len(jobs) <= 8:
+        if self.optimizer == "sgd" and len(jobs) <= 8:
             # SGD + B images of the updated weights + batch record: one launch
             desc = self._image_desc(jobs)
             _lib.call("hg_sgd_fused", ptr(P.flat), ptr(P.grad), P.numel, self.lr, len(jobs), desc.ctypes.data,

@@ -3,8 +3,9 @@
 The functional API keeps the reference's signatures (numpy in, numpy out) so
 it is a drop-in for parity tests; each call runs the library's kernels:
 aggregation K5 (``hg_aggregate_fwd``), transposed aggregation K6
-(``hg_aggregate_bwd`` over a stable src-major view), dense transforms K8
-(``hg_gemm_f32`` / ``hg_wgrad_f32``), loss K9 and updates K10.  Arithmetic is
+(``hg_aggregate_bwd_scatter``: deterministic fixed-point scatter), dense
+transforms K8 on the tensor cores (``hg_gemm_tc`` / ``hg_wgrad_tc``), loss K9
+and updates K10.  Arithmetic is
 fp32 on device (the reference is fp64); tolerances are stated in the tests.
 The training engine (engine.py) runs the same kernels device-resident.
 """
@@ -73,7 +74,7 @@ def init_params(model: str, dims, seed: int) -> ModelParams:
 class DeviceBlock:
     """A reference Block (edges sorted by (dst, src)) in the kernels' slot form."""
 
-    def __init__(self, block, device, need_csc=True):
+    def __init__(self, block, device):
         es = np.asarray(block.edge_src, np.int64)
         ed = np.asarray(block.edge_dst, np.int64)
         n_dst, n_src = int(block.n_dst), int(block.n_src)
@@ -98,14 +99,6 @@ class DeviceBlock:
         self.dst = t(dst_g if n_dst else [0])
         self.d_n_dst = t([n_dst])
         self.d_n_src = t([n_src])
-        if need_csc and n_dst:
-            lib = _lib.load()
-            self.csc_slot = torch.zeros(max(n_dst * f, 1), dtype=torch.int32, device=device)
-            self.seg_beg = torch.zeros(max(n_src, 1), dtype=torch.int32, device=device)
-            self.seg_end = torch.zeros_like(self.seg_beg)
-            ws = torch.zeros(int(lib.hg_csc_ws_size(n_dst, f)), dtype=torch.int32, device=device)
-            _lib.call("hg_build_csc", None, n_dst, f, ptr(self.counts), ptr(self.slot_local), n_src,
-                      ptr(self.csc_slot), ptr(self.seg_beg), ptr(self.seg_end), ptr(ws), stream_ptr())
 
 
 def _dev_rows(x, device, ld=None):
@@ -258,11 +251,15 @@ def backward_batch(caches, dlogits, params: ModelParams):
             dense.dx(ptr(dz), ld_out, c.d_out, ptr(W[0]), c.d_in, ptr(dagg), ld_in, ptr(db.d_n_dst), db.n_dst, s)
         below = caches[l - 1]
         dx = torch.zeros((max(db.n_src, 1), ld_in), dtype=torch.float32, device=dev)
-        _lib.call("hg_aggregate_bwd", code, ptr(dagg), ld_in, ptr(dself), ld_in, ld_in, ptr(db.dst), ptr(db.d_n_dst),
-                  db.n_dst, db.f, ptr(db.counts), ptr(db.slot_g), ptr(db.nself), ptr(db.outdeg), ptr(db.csc_slot),
-                  ptr(db.seg_beg), ptr(db.seg_end), ptr(db.d_n_src), db.n_src,
-                  ptr(below.out) if below.activation else None, ld_in, ptr(below.inj_dev), ptr(dx), ld_in, None,
-                  None, s)
+        acc = torch.zeros((max(db.n_src, 1), 2 * ld_in), dtype=torch.int64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("hg_aggregate_bwd_scatter", code, ptr(dagg), ld_in, ptr(dself), ld_in, ld_in, ptr(db.dst),
+                  ptr(db.d_n_dst), db.n_dst, db.f, ptr(db.counts), ptr(db.slot_g), ptr(db.slot_local),
+                  ptr(db.nself), ptr(db.outdeg), ptr(db.d_n_src), db.n_src,
+                  ptr(below.out) if below.activation else None, ld_in, ptr(below.inj_dev), ptr(acc), ptr(dx), ld_in,
+                  ptr(flags), s)
+        if int(flags.item()):  # gnnmath.py:100-102 (non-finite), or the fixed-point range guard
+            raise FloatingPointError(f"{params.model} backward: transposed aggregation flagged {int(flags.item())}")
         d = dx
     return grads
 

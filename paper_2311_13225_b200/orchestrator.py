@@ -566,10 +566,11 @@ class Trainer:
         return self._handles(done, pin, n)
 
     def _train_batches_native(self, batches):
-        """train_batches through the native step driver (hg_pipeline_run): the
-        batches' inputs are packed into pinned staging slots (SampleSet.stage
-        layout) up front, then one C call enqueues every step's H2D, both
-        half-step graphs and the loss D2H — no Python work per step."""
+        """train_batches through the native step driver (hg_pipeline_run): one C
+        call packs each batch's inputs into its pinned staging slot (SampleSet.stage
+        layout) and enqueues that step's H2D and both half-step graphs, then the
+        loss D2H — no Python work per step, and the device starts after the first
+        batch is packed, not after all of them."""
         e, pipe = self.engine, self.pipeline
         n, cap = len(batches), e.batch_cap
         rec = int(e.loss_arr.numel())  # batch k records its loss at loss_arr[bp[3] = k]
@@ -586,34 +587,34 @@ class Trainer:
         if buf is None or buf.shape[0] < n:
             buf = torch.zeros((max(n, 64), slot), dtype=torch.uint8).pin_memory()
             self._native_stage = buf
-        hn = buf.numpy()
-        bp = hn[:n, :STAGE_COUNTS].view(np.int64)
-        cnt = hn[:n, STAGE_COUNTS:STAGE_COUNTS + 8].view(np.int32)
-        sd = hn[:n, STAGE_SEEDS:].view(np.int32)
-        nbytes = np.empty(n, np.int64)
-        v0 = self.version
-        for i, (seeds, rs) in enumerate(batches):
-            seeds = np.asarray(seeds)
-            k = int(seeds.shape[0])
-            if k > cap:
-                raise ValueError("batch larger than the engine's capacity")
-            sd[i, :k] = seeds
-            cnt[i] = (k, self.dist.global_batch(seeds) if self.dist else k)
-            bp[i] = (np.array([int(rs) & 0xFFFFFFFFFFFFFFFF], np.uint64).view(np.int64)[0], k, v0 + i, i, -1, 0,
-                     -1, 0)
-            nbytes[i] = STAGE_SEEDS + 4 * k
+        # per-batch host inputs; the native driver packs batch k into its pinned
+        # staging slot right before launching step k
+        seeds = [np.ascontiguousarray(s, dtype=np.int64) for s, _ in batches]
+        n_seeds = np.fromiter((s.shape[0] for s in seeds), np.int32, n)
+        if n and int(n_seeds.max()) > cap:
+            raise ValueError("batch larger than the engine's capacity")
+        n_div = (np.fromiter((self.dist.global_batch(s) for s in seeds), np.int32, n) if self.dist else n_seeds)
+        seed_ptrs = np.fromiter((s.__array_interface__["data"][0] for s in seeds), np.int64, n)
+        bp = np.zeros((n, 8), np.int64)
+        bp[:, 0] = np.fromiter((int(rs) & 0xFFFFFFFFFFFFFFFF for _, rs in batches), np.uint64, n).view(np.int64)
+        bp[:, 1] = n_seeds
+        bp[:, 2] = self.version + np.arange(n)
+        bp[:, 3] = np.arange(n)
+        bp[:, 4] = -1
+        bp[:, 6] = -1
         pin = torch.zeros(n, dtype=torch.float32).pin_memory()
         execs_s = np.array([g.raw_cuda_graph_exec() for g in e.g_sample], np.int64)
         execs_t = np.array([g.raw_cuda_graph_exec() for g in e.g_train], np.int64)
         stages = np.array([st.stage.data_ptr() for st in e.sets], np.int64)
         cur = torch.cuda.current_stream(e.device)
         _lib.call("hg_pipeline_run", n, len(e.sets), execs_s.ctypes.data, execs_t.ctypes.data, cur.cuda_stream,
-                  pipe.ss.cuda_stream, pipe.st.cuda_stream, stages.ctypes.data, buf.data_ptr(), slot,
-                  nbytes.ctypes.data, ptr(e.loss_arr), pin.data_ptr())
+                  pipe.ss.cuda_stream, pipe.st.cuda_stream, stages.ctypes.data, buf.data_ptr(), slot, STAGE_COUNTS,
+                  STAGE_SEEDS, bp.ctypes.data, seed_ptrs.ctypes.data, n_seeds.ctypes.data, n_div.ctypes.data,
+                  ptr(e.loss_arr), pin.data_ptr())
         done = torch.cuda.Event()
         done.record(cur)
         self._native_done = done
-        self.feeder.h2d_bytes = int(nbytes[0])
+        self.feeder.h2d_bytes = int(STAGE_SEEDS + 4 * n_seeds[0]) if n else 0
         self.version += n
 
         return self._handles(done, pin, n)

@@ -111,11 +111,11 @@ class LayerSampler:
 
     Buffers (int32): counts[cap_dst], slots/slot_local[cap_dst*f] (slot form),
     src[cap_src] with device count n_src; nself[cap_dst] (SAGE), outdeg[cap_src]
-    (GCN); csc_slot/seg_beg/seg_end for the backward transposed aggregation.
+    (GCN; layers >= 1: the backward scatter's per-source edge counts).
     """
 
     def __init__(self, dg: DeviceGraph, cap_dst: int, fanout: int, need_nself=True, need_outdeg=False,
-                 need_csc=False, minpos=None):
+                 minpos=None):
         lib = _lib.load()
         dev = dg.device
         self.dg, self.f, self.cap_dst = dg, int(fanout), int(cap_dst)
@@ -133,20 +133,11 @@ class LayerSampler:
         self.outdeg = z(self.cap_src) if need_outdeg else None
         self.ws = z(lib.hg_dedup_ws_size(self.cap_dst, self.f))
         self.scratch = z(cap_dst * 2 * self.f) if self.f > 32 else None
-        self.need_csc = need_csc
-        if need_csc:
-            self.csc_slot = z(cap_dst * self.f)
-            self.seg_beg = z(self.cap_src)
-            self.seg_end = z(self.cap_src)
-            self.csc_ws = z(lib.hg_csc_ws_size(self.cap_dst, self.f))
-            self.csc_dst = z(cap_dst * self.f)
-            self.csc_w = torch.zeros(max(cap_dst * self.f, 1), dtype=torch.float32, device=dev)
 
     def run(self, frontier, d_n_dst, d_seed, layer: int, stream=None, cap_dst: int | None = None,
-            with_csc: bool = True, dedup: bool = True, relabel_stream=None):
+            dedup: bool = True, relabel_stream=None):
         """Enqueue the block build for `frontier` (device int32, count *d_n_dst).
-        ``with_csc=False`` defers the transposed view to ``build_csc`` (e.g. on a
-        side stream, off the forward critical path).  ``relabel_stream``: the
+        ``relabel_stream``: the
         relabel half (segment order, slot_local, nself, outdeg) runs there after
         the draw + mark half on ``stream``; src / n_src are ready on ``stream``,
         the rest once ``relabel_stream`` is joined.  The next layer's sampler on
@@ -183,31 +174,13 @@ class LayerSampler:
             _lib.call("hg_block_relabel", ptr(frontier), ptr(d_n_dst), cap, self.f, ptr(self.counts),
                       ptr(self.slots), ptr(self.slot_local), ptr(self.minpos.table), ptr(self.minpos.tag),
                       ptr(self.nself), ptr(self.outdeg), ptr(self.ws), relabel_stream.cuda_stream)
-            if self.need_csc and with_csc:
-                self.build_csc(d_n_dst, relabel_stream, cap)
             return self
-        # draw + dedup + relabel (one cooperative kernel for small blocks)
+        # draw + dedup + relabel
         _lib.call("hg_sample_block", ptr(g.offsets), ptr(g.targets), ptr(frontier), ptr(d_n_dst), cap, self.f,
                   ptr(d_seed), int(layer), ptr(self.counts), ptr(self.slots), ptr(self.slot_local),
                   ptr(self.minpos.table), ptr(self.minpos.tag), ptr(self.src), ptr(self.n_src), cap_src,
                   ptr(self.nself), ptr(self.outdeg), ptr(self.ws), ptr(self.scratch), s)
-        if self.need_csc and with_csc:
-            self.build_csc(d_n_dst, stream, cap)
         return self
-
-    def build_csc(self, d_n_dst, stream=None, cap_dst: int | None = None, frontier=None):
-        """Stable src-major view; with ``frontier`` also the per-edge (dst, weight)
-        table the backward gather reads (SAGE if nself is tracked, else GCN)."""
-        cap = self.cap_dst if cap_dst is None else int(cap_dst)
-        cap_src = min(self.cap_src, self.dg.num_vertices, cap * (self.f + 1))
-        s = stream_ptr(stream)
-        _lib.call("hg_build_csc", ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(self.slot_local), cap_src,
-                  ptr(self.csc_slot), ptr(self.seg_beg), ptr(self.seg_end), ptr(self.csc_ws), s)
-        if frontier is not None:
-            model = 0 if self.nself is not None else 1
-            _lib.call("hg_csc_weights", model, ptr(d_n_dst), cap, self.f, ptr(self.counts), ptr(frontier),
-                      ptr(self.slots), ptr(self.slot_local), ptr(self.nself), ptr(self.outdeg), ptr(self.csc_slot),
-                      ptr(self.csc_dst), ptr(self.csc_w), s)
 
     # -- host views (sync) ---------------------------------------------------
     def to_block(self, frontier_np: np.ndarray, stream=None) -> Block:
@@ -262,12 +235,12 @@ def _check_seeds(num_vertices, seeds):
     return seeds
 
 
-def _expand(dg, frontier_np, fanout, stream_seed, need_csc=False):
+def _expand(dg, frontier_np, fanout, stream_seed):
     dev = dg.device
     fr = torch.as_tensor(frontier_np.astype(np.int32), device=dev)
     n = torch.tensor([fr.numel()], dtype=torch.int32, device=dev)
     seed = u64_tensor(stream_seed, dev)
-    ls = LayerSampler(dg, fr.numel(), fanout, need_nself=False, need_outdeg=False, need_csc=need_csc)
+    ls = LayerSampler(dg, fr.numel(), fanout, need_nself=False, need_outdeg=False)
     ls.run(fr, n, seed, layer=-1)
     return ls.to_block(frontier_np)
 

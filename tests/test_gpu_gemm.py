@@ -1,7 +1,7 @@
-"""tcgen05 GEMMs (3xTF32) and the SIMT fallback against a float64 numpy reference.
+"""tcgen05 GEMMs (3xTF32) against a float64 numpy reference.
 
 Tolerance: |C - C_ref| <= 2e-5 * (|A| |B|)_ij  (the product-magnitude bound; 3xTF32
-and fp32 FMA accumulation both land ~1e-6 relative to it)."""
+lands ~1e-6 relative to it)."""
 
 import numpy as np
 import pytest
@@ -22,32 +22,28 @@ def _ld(k):
     return (k + 3) // 4 * 4
 
 
-@pytest.fixture(params=["tc", "tc_resb", "tc_unpaired", "tc_wg_ss", "tc_wg_ss_unpaired", "skinny"])
+@pytest.fixture(params=["tc", "tc_unpaired", "tc_wg_ss", "tc_wg_ss_unpaired", "tc_ss_fwd"])
 def path(request):
-    """hg_gemm_tc / hg_wgrad_tc dispatch: tensor cores (default: paired MMAs, wgrad
-    with A^T through TMEM), the resident-B TS form (hg_set_tuning key 6), unpaired
-    MMAs (key 7), the shared-memory wgrad form (key 11), or the optional SIMT
-    latency kernels for small M (key 4)."""
+    """hg_gemm_tc / hg_wgrad_tc kernel forms: default (paired MMAs, A through TMEM,
+    wgrad with A^T through TMEM), unpaired MMAs (hg_set_tuning key 7), the
+    shared-memory wgrad form (key 11), the shared-memory forward form (key 3)."""
     from paper_2311_13225_b200 import _lib
     lib = _lib.load()
-    lib.hg_set_tuning(4, 1 if request.param == "skinny" else 0)
-    lib.hg_set_tuning(6, 1 if request.param == "tc_resb" else 0)
     lib.hg_set_tuning(7, 0 if request.param.endswith("unpaired") else 1)
     lib.hg_set_tuning(11, 0 if request.param.startswith("tc_wg_ss") else 1)
+    lib.hg_set_tuning(3, 0 if request.param == "tc_ss_fwd" else 1)
     yield request.param
-    lib.hg_set_tuning(4, 0)
-    lib.hg_set_tuning(6, 0)
     lib.hg_set_tuning(7, 1)
     lib.hg_set_tuning(11, 1)
+    lib.hg_set_tuning(3, 1)
 
 
-@pytest.mark.parametrize("fn", ["hg_gemm_tc", "hg_gemm_f32"])
 @pytest.mark.parametrize("M,K1,K2,N,trans,act", [
     (300, 100, 100, 64, 1, 1), (1000, 64, 64, 47, 1, 0), (129, 32, 0, 16, 1, 0), (5000, 47, 0, 64, 0, 0),
     (777, 602, 0, 256, 1, 1), (1024, 128, 0, 172, 1, 0), (1, 3, 5, 9, 1, 0), (200, 64, 0, 300, 0, 0),
     (5700, 64, 64, 64, 1, 1), (1024, 64, 0, 128, 0, 0), (3000, 128, 128, 128, 1, 0), (6000, 47, 0, 64, 0, 0),
 ])
-def test_gemm(fn, M, K1, K2, N, trans, act, path):
+def test_gemm(M, K1, K2, N, trans, act, path):
     import torch
     from paper_2311_13225_b200 import _lib
     from paper_2311_13225_b200.device import ptr
@@ -73,22 +69,10 @@ def test_gemm(fn, M, K1, K2, N, trans, act, path):
     C = torch.full((M, ldc), 7.0, dtype=torch.float32, device="cuda")
     dM = torch.tensor([M], dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
-    if fn == "hg_gemm_tc":
-        img = torch.zeros(int(_lib.fn("hg_gemm_tc_bimg_size")(K1, K2, N)) // 4 + 4, dtype=torch.float32,
-                          device="cuda")
-        _lib.call("hg_gemm_tc_prep_b", ptr(dW), ldb, trans, K1, K2, N, ptr(img), s)
-        _lib.call(fn, ptr(dA1), _ld(K1), K1, ptr(dA2), _ld(K2) if K2 else 0, K2, ptr(img), ptr(C), ldc, N,
-                  ptr(dM), M + 5, act, s)
-    else:
-        if trans:
-            b1, b2 = ptr(dW), (dW[K1:].data_ptr() if K2 else None)
-            _lib.call(fn, ptr(dA1), _ld(K1), K1, b1, N, ptr(dA2), _ld(K2) if K2 else 0, K2, b2, N, 0, ptr(C), ldc,
-                      N, ptr(dM), M + 5, act, s)
-        else:
-            if K2:
-                pytest.skip("SIMT path takes a transposed second source only via trans")
-            _lib.call(fn, ptr(dA1), _ld(K1), K1, ptr(dW), Ktot, None, 0, 0, None, 0, 1, ptr(C), ldc, N, ptr(dM),
-                      M + 5, act, s)
+    img = torch.zeros(int(_lib.fn("hg_gemm_tc_bimg_size")(K1, K2, N)) // 4 + 4, dtype=torch.float32, device="cuda")
+    _lib.call("hg_gemm_tc_prep_b", ptr(dW), ldb, trans, K1, K2, N, ptr(img), s)
+    _lib.call("hg_gemm_tc", ptr(dA1), _ld(K1), K1, ptr(dA2), _ld(K2) if K2 else 0, K2, ptr(img), ptr(C), ldc, N,
+              ptr(dM), M + 5, act, s)
     got = C[:M, :N].double().cpu().numpy()
     err = np.abs(got - ref)
     assert np.all(err <= 2e-5 * mag + 1e-6), (err.max(), (err / (mag + 1e-9)).max())

@@ -182,36 +182,6 @@ def test_draws_only_matches_full_block(S):
         assert sorted(a[i, :cnt[i]].tolist()) == sorted(b[i, :cnt[i]].tolist()), i
 
 
-@pytest.mark.parametrize("n,f", [(5000, 10), (1024, 5), (16384, 3), (300, 32)])
-def test_cooperative_block_equals_three_kernels(S, n, f):
-    """hg_sample_block's cooperative single-kernel form (small blocks) produces the
-    same block bit for bit as the draw -> mark/scan -> relabel kernel sequence."""
-    import torch
-    from paper_2311_13225_b200 import _lib
-    from paper_2311_13225_b200.datagen import make_dataset
-    from paper_2311_13225_b200.device import DeviceGraph, u64_tensor
-    ds = make_dataset("c2", scale=0.1)
-    dg = DeviceGraph.from_dataset(ds)
-    rng = np.random.default_rng(n + f)
-    ids = torch.as_tensor(rng.choice(ds.num_vertices, size=n, replace=False).astype(np.int32), device="cuda")
-    seed = u64_tensor(0x5EED + n, "cuda")
-    lib = _lib.load()
-    out = []
-    for coop in (1, 0):
-        lib.hg_set_tuning(8, coop)
-        smp = S.LayerSampler(dg, n, f, need_nself=True, need_outdeg=True, minpos=dg.minpos.like())
-        smp.run(ids, None, seed, 1)
-        torch.cuda.synchronize()
-        k = int(smp.n_src.item())
-        out.append((k, smp.src[:k].cpu(), smp.counts.cpu(), smp.slots.cpu(), smp.slot_local.cpu(), smp.nself.cpu(),
-                    smp.outdeg[:k].cpu()))
-    lib.hg_set_tuning(8, 0)
-    a, b = out
-    assert a[0] == b[0]
-    for x, y in zip(a[1:], b[1:]):
-        assert torch.equal(x, y)
-
-
 @pytest.mark.parametrize("model,F", [("gcn", 602), ("sage", 602), ("sage", 200), ("gcn", 1000)])
 def test_wide_row_bulk_gather_bitexact(model, F):
     """Wide rows (F > 128): the TMA bulk-copy staged aggregation (tuning key 12)

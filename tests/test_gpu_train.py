@@ -142,20 +142,6 @@ def test_hot_ratio_zero_equals_baseline(golden_meta, ggraphs):
         assert ra.losses == rb.losses
 
 
-@pytest.mark.parametrize("name", ["sbm_sage_hot", "pl_gcn_adam"])
-def test_bwd_scatter_matches_csc_gather(golden_meta, ggraphs, monkeypatch, name):
-    """The fixed-point scatter backward (default) and the CSC-gather backward
-    (HG_BWD=csc) compute the same transposed aggregation: per-batch losses agree
-    to fp32 rounding over a whole run."""
-    meta = golden_meta["runs"][name]
-    monkeypatch.setenv("HG_BWD", "csc")
-    a, _ = _run(ggraphs, name, meta)
-    monkeypatch.setenv("HG_BWD", "scatter")
-    b, _ = _run(ggraphs, name, meta)
-    for ra, rb in zip(a, b):
-        np.testing.assert_allclose(ra.losses, rb.losses, rtol=1e-5)
-
-
 def test_bwd_scatter_flags_nonfinite():
     """A non-finite gradient entering the scatter raises FloatingPointError
     (the reference's non-finite guard, gnnmath.py:100-102)."""

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Microbenchmark of the dense-transform kernels at the C2 bottom-layer shape:
 forward [self | mean] [W_self; W_neigh] (M=51K, K=100+100, N=64) and the two
-weight gradients, for each kernel form (hg_set_tuning keys 2/3), CUDA events,
+weight gradients, for each kernel form (hg_set_tuning keys 3/7/11), CUDA events,
 inputs larger than L2 rotated between iterations."""
 import sys
 from pathlib import Path
@@ -56,17 +56,10 @@ def main():
     ref = None
     fwd_bytes = M * 2 * K * 4 + M * N * 4
     wg_bytes = M * 2 * K * 4 + M * N * 4
-    for name, legacy, form, sk, resb, pair, wts in (("legacy cp.async", 1, 1, 0, 0, 0, 1), ("tma SS", 0, 0, 0, 0, 0, 1),
-                                                    ("tma TS", 0, 1, 0, 0, 0, 1), ("tma TS resident B", 0, 1, 0, 1, 0, 1),
-                                                    ("tma TS paired", 0, 1, 0, 0, 1, 1),
-                                                    ("tma TS paired resident B", 0, 1, 0, 1, 1, 1),
-                                                    ("paired, SS-form wgrad", 0, 1, 0, 0, 1, 0),
-                                                    ("skinny simt", 0, 1, 1, 0, 1, 1)):
+    for name, form, pair, wts in (("tma SS", 0, 0, 1), ("tma TS", 1, 0, 1), ("tma TS paired", 1, 1, 1),
+                                  ("paired, SS-form wgrad", 1, 1, 0)):
         lib.hg_set_tuning(11, wts)
         lib.hg_set_tuning(7, pair)
-        lib.hg_set_tuning(6, resb)
-        lib.hg_set_tuning(4, sk)
-        lib.hg_set_tuning(2, legacy)
         lib.hg_set_tuning(3, form)
         f = lambda r: _lib.call("hg_gemm_tc", ptr(A1[r % R]), LD, K, ptr(A2[r % R]), LD, K, ptr(img), ptr(C), N, N,  # noqa
                                 ptr(dM), M, 1, torch.cuda.current_stream().cuda_stream)
@@ -85,30 +78,18 @@ def main():
                    (o2 - (A2[0].double().T @ G[0].double()).float()).abs().max().item())
         print(f"{name:16s} fwd {us:7.2f} us ({fwd_bytes / us / 1e3:6.0f} GB/s, max err {err:.2e})   "
               f"wgrad {us_w:7.2f} us ({wg_bytes / us_w / 1e3:6.0f} GB/s, max err {werr:.2e})")
-    lib.hg_set_tuning(2, 0)
     lib.hg_set_tuning(3, 1)
-    lib.hg_set_tuning(4, 0)
-    wsf = torch.zeros(int(lib.hg_wgrad_ws_size(K, N, M)), device="cuda")
-    cs = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
-    f = lambda r: _lib.call("hg_gemm_f32", ptr(A1[r % R]), LD, K, ptr(W), N, ptr(A2[r % R]), LD, K,  # noqa: E731
-                            W[K:].data_ptr(), N, 0, ptr(C), N, N, ptr(dM), M, 1, cs())
-    g = lambda r: (_lib.call("hg_wgrad_f32", ptr(A1[r % R]), LD, K, ptr(G[r % R]), N, N, ptr(dM), M, ptr(o1), 1.0,  # noqa
-                             ptr(wsf), cs()),
-                   _lib.call("hg_wgrad_f32", ptr(A2[r % R]), LD, K, ptr(G[r % R]), N, N, ptr(dM), M, ptr(o2), 1.0,
-                             ptr(wsf), cs()))
-    print(f"{'simt fp32':16s} fwd {timeit(f):7.2f} us   wgrad {timeit(g):7.2f} us")
     for dbg, what in ((1, "no MMA"), (2, "no split"), (3, "loads only"), (4, "no stores"), (7, "loads, no st")):
         lib.hg_set_tuning(9, dbg)
         f = lambda r: _lib.call("hg_gemm_tc", ptr(A1[r % R]), LD, K, ptr(A2[r % R]), LD, K, ptr(img), ptr(C), N, N,  # noqa
                                 ptr(dM), M, 1, torch.cuda.current_stream().cuda_stream)
-        print(f"fwd TS resB {what:12s} {timeit(f):7.2f} us")
+        print(f"fwd TS paired {what:12s} {timeit(f):7.2f} us")
     for dbg, what in ((1, "no MMA"), (2, "no split"), (3, "loads only")):
         lib.hg_set_tuning(9, dbg)
         g = lambda r: _lib.call("hg_wgrad_tc", ptr(A1[r % R]), LD, ptr(A2[r % R]), LD, K, ptr(G[r % R]), N, N,  # noqa
                                 ptr(dM), M, ptr(o1), ptr(o2), ptr(ws), torch.cuda.current_stream().cuda_stream)
         print(f"wgrad tma {what:12s} {timeit(g):7.2f} us")
     lib.hg_set_tuning(9, 0)
-    lib.hg_set_tuning(4, 0)
 
 
 if __name__ == "__main__":
