@@ -16,7 +16,6 @@
 // after batch k - n_sets trained; batch k trains after its sample half; both
 // streams start after the caller's stream and the caller's stream waits for both
 // at the end.
-#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -80,16 +79,10 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
             cudaStreamWaitEvent(cp, trained[set], 0);
             cudaStreamWaitEvent(ss, trained[set], 0);
         }
-        static int mode = getenv("HG_PIPE_COPY") ? atoi(getenv("HG_PIPE_COPY")) : 0;  // EXPERIMENT
-        if (mode == 0) {
-            cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
-                            (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, cp);
-            cudaEventRecord(copied[set], cp);
-            cudaStreamWaitEvent(ss, copied[set], 0);
-        } else if (mode == 1) {
-            cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
-                            (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, ss);
-        }
+        cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
+                        (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, cp);
+        cudaEventRecord(copied[set], cp);
+        cudaStreamWaitEvent(ss, copied[set], 0);
         const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(sample_execs[set]), ss);
         if (e != cudaSuccess && err == cudaSuccess) err = e;
         cudaEventRecord(sampled[set], ss);
