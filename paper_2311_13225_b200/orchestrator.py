@@ -583,6 +583,7 @@ class Trainer:
         prev = getattr(self, "_native_done", None)
         if prev is not None:
             prev.synchronize()  # the staging slots of the previous call may still be in flight
+            self._native_fill()  # its losses leave the shared pinned buffer before it is reused
         buf = getattr(self, "_native_stage", None)
         if buf is None or buf.shape[0] < n:  # sized once for the largest call (a pinned
             # allocation costs ~ms of host time in front of the call's first launch)
@@ -603,7 +604,10 @@ class Trainer:
         bp[:, 3] = np.arange(n)
         bp[:, 4] = -1
         bp[:, 6] = -1
-        pin = torch.zeros(n, dtype=torch.float32).pin_memory()
+        pin = getattr(self, "_native_loss", None)
+        if pin is None or pin.numel() < n:
+            pin = torch.zeros(max(n, rec), dtype=torch.float32).pin_memory()
+            self._native_loss = pin
         execs_s = np.array([g.raw_cuda_graph_exec() for g in e.g_sample], np.int64)
         execs_t = np.array([g.raw_cuda_graph_exec() for g in e.g_train], np.int64)
         stages = np.array([st.stage.data_ptr() for st in e.sets], np.int64)
@@ -618,22 +622,27 @@ class Trainer:
         self.feeder.h2d_bytes = int(STAGE_SEEDS + 4 * n_seeds[0]) if n else 0
         self.version += n
 
-        return self._handles(done, pin, n)
+        return self._handles(done, pin, n, native=True)
 
-    def _handles(self, done, pin, n):
+    def _handles(self, done, pin, n, native=False):
         """One loss handle per batch; the first handle to complete also checks the
         device numerics flags once for the whole call (gnnmath.py:100-102) and
         reads every loss of the call from the pinned buffer in one go."""
         vals = []
 
+        def fill():
+            if not vals:
+                done.synchronize()
+                self.engine.check_numerics()
+                vals.append(pin[:n].tolist())
+
         def handle(i):
             def get():
-                if not vals:
-                    done.synchronize()
-                    self.engine.check_numerics()
-                    vals.append(pin.tolist())
+                fill()
                 return float(vals[0][i])
             return get
+        if native:  # the next native call materialises these before reusing the pinned buffer
+            self._native_fill = fill
         return [handle(i) for i in range(n)]
 
     @property

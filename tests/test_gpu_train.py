@@ -219,7 +219,8 @@ def test_native_step_driver_equals_python_loop(monkeypatch, model):
     """Trainer.train_batches through the native step driver (hg_pipeline_run: one C
     call enqueues every step's staging H2D, both half-step graphs and the loss D2H)
     is bit-identical to the per-step Python pipeline loop, incl. a partial batch
-    and a second call that reuses the pinned staging slots."""
+    and a second call that reuses the pinned staging and loss slots before the
+    first call's handles were read."""
     from paper_2311_13225_b200.datagen import make_dataset
     from paper_2311_13225_b200.orchestrator import TrainConfig, Trainer
     ds = make_dataset("tiny")
@@ -232,8 +233,9 @@ def test_native_step_driver_equals_python_loop(monkeypatch, model):
     for native in ("0", "1"):
         monkeypatch.setenv("HG_NATIVE_LOOP", native)
         tr = Trainer(ds, cfg)
-        losses = [h() for h in tr.train_batches(batches)]
-        losses += [h() for h in tr.train_batches(batches[:3])]
+        h1 = tr.train_batches(batches)
+        h2 = tr.train_batches(batches[:3])  # reuses the pinned slots before h1 was read
+        losses = [h() for h in h1] + [h() for h in h2]
         out[native] = (np.array(losses), tr.engine.params.flat.cpu().numpy().copy(), tr.version)
     assert np.all(np.isfinite(out["1"][0]))
     assert np.array_equal(out["0"][0], out["1"][0])
