@@ -526,9 +526,12 @@ def run_epoch_mode(spec: str):
                       batch_size=int(opts.get("bs", 1024)), lr=float(opts.get("lr", 0.01)),
                       strategy="layer-based" if hot > 0 else "case1", hot_ratio=hot,
                       super_batch_n=int(opts.get("n", 4)), presample_rounds=int(opts.get("rounds", 2)),
-                      execution=opts.get("exec", "pipelined"), seed=0,
+                      execution=opts.get("exec", "pipelined"), seed=0, epochs=int(opts.get("epochs", 2)),
                       use_graph=bool(int(opts.get("graph", 1))))
     ds = make_dataset(name, cache_dir=CACHE)
+    if "limit" in opts:  # training mask cut to its first `limit` vertices (bounded epochs on the full graph)
+        from paper_2311_13225_b200.datagen import limit_train
+        ds = limit_train(ds, int(opts["limit"]))
     t0 = time.perf_counter()
     tr = Trainer(ds, cfg)
     setup_s = time.perf_counter() - t0
@@ -551,9 +554,27 @@ def run_epoch_mode(spec: str):
                     "last_loss": rep.losses[-1]})
         first += len(plan.batches)
     acc = evaluate(tr)
+    cpu = None
+    if int(opts.get("cpu", 0)):  # the reference path on the host cores beside it (the oracle port, fp64)
+        from oracle import oracle as O
+        og = O.Graph(offsets=ds.offsets, targets=ds.targets.astype(np.int64))
+        od = O.VertexData(features=ds.features.astype(np.float64), labels=ds.labels, train_mask=ds.train_mask,
+                          val_mask=ds.val_mask, test_mask=ds.test_mask)
+        kw = {k: v for k, v in cfg.to_dict().items() if k in O.DEFAULT_CFG}
+        w0 = time.perf_counter()
+        reps, weights, _ = O.run_training(og, od, kw, evaluate_each_epoch=False)
+        cpu_s = time.perf_counter() - w0
+        accs, _ = O.evaluate(og, od, cfg.model, weights)
+        n_all = sum(len(r["losses"]) for r in reps) * cfg.batch_size
+        cpu = {"seconds": cpu_s, "cores": host_cores(), "kind": "port",
+               "seeds_per_s_incl_presampling": n_all / cpu_s, "val_accuracy": accs["val"],
+               "test_accuracy": accs["test"], "max_gap": [r.get("max_gap", 0) for r in reps],
+               "reuse_hits": [sum(x["reuse_hits"] for x in r["rows"]) for r in reps],
+               "last_loss": reps[-1]["losses"][-1]}
     print(json.dumps({"mode": "epoch", "spec": spec, "config": cfg.to_dict(), "vertices": ds.num_vertices,
                       "edges": ds.num_edges, "hot_list": int(tr.hot_list.shape[0]), "setup_s": setup_s,
-                      "epochs": res, "val_accuracy": acc["val"], "test_accuracy": acc["test"]}), flush=True)
+                      "epochs": res, "val_accuracy": acc["val"], "test_accuracy": acc["test"],
+                      "cpu_reference": cpu}), flush=True)
 
 
 def phase_breakdown(e, d_seeds, d_bp, d_counts, i0, reps=20):
