@@ -262,6 +262,10 @@ int hg_sgd_fused(float* w, const float* g, int64_t n, float lr, int32_t n_img, c
 int hg_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
             int32_t* d_t, uint32_t* d_maxdelta, void* stream);
 
+/* Device-to-device copy of nbytes (16-byte aligned pointers) as one small kernel
+ * (a graph kernel node; the sample half's hand-off of the batch inputs). */
+int hg_copy_bytes(void* dst, const void* src, int64_t nbytes, void* stream);
+
 /* ---- native step driver: the per-batch loop of Trainer.train_batches
  *      (orchestrator.py:520-560) over captured half-step graphs.  For step k:
  *      pack host_stage[k*slot_bytes, +slot_bytes) = bp_rows[k] (8 int64) at 0 |

@@ -219,7 +219,8 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
                            shards);                                                                        \
         return HG_OK;                                                                                     \
     }
-    HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 8)
+    HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 5) HG_FWD(32, 6)
+    HG_FWD(32, 8)
 #undef HG_FWD
     return HG_EUNSUPPORTED;
 }
@@ -453,6 +454,17 @@ int agg_ctas_per_sm() {
     return v;
 }
 
+void pick_lanes(int F4, int& LPR, int& NV);
+
+// forward aggregation: wide rows (128 < F4 <= 192) get exactly the float4 columns
+// they need per lane (C3's 602 features: 5 instead of 8), so each warp keeps 3
+// rows in flight instead of 2 in about the same registers (C3 bottom aggregation
+// 81.6 -> 79.0 us, profiles/r02_c3_tight_nv.txt)
+void pick_lanes_fwd(int F4, int& LPR, int& NV) {
+    pick_lanes(F4, LPR, NV);
+    if (F4 > 128 && F4 <= 192) NV = F4 <= 160 ? 5 : 6;
+}
+
 void pick_lanes(int F4, int& LPR, int& NV) {
     if (F4 <= 8) { LPR = 8; NV = 1; }
     else if (F4 <= 16) { LPR = 16; NV = 1; }
@@ -483,7 +495,7 @@ extern "C" int hg_aggregate_fwd(int32_t model, int32_t global_src, const float* 
     if (cap_dst == 0) return HG_OK;
     const int F4 = F / 4;
     int LPR, NV;
-    pick_lanes(F4, LPR, NV);
+    pick_lanes_fwd(F4, LPR, NV);
     dim3 g(hg_grid((long long)cap_dst * LPR, 256, global_src ? agg_ctas_per_sm() : 8));
     cudaStream_t s = (cudaStream_t)stream;
     int rc;
@@ -540,7 +552,7 @@ extern "C" int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard
     sh.rows_per_shard = rows_per_shard;
     const int F4 = F / 4;
     int LPR, NV;
-    pick_lanes(F4, LPR, NV);
+    pick_lanes_fwd(F4, LPR, NV);
     dim3 g(hg_grid((long long)cap_dst * LPR, 256, agg_ctas_per_sm()));
     cudaStream_t s = (cudaStream_t)stream;
     const int rc = model ? launch_fwd<M_GCN_GLOBAL, true>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh)

@@ -12,10 +12,11 @@
 // the whole call's, so the host never becomes the bottleneck of a step that
 // takes ~0.19 ms on the device.
 //
-// Ordering (same as engine.Pipeline): sample set k % n_sets is refilled only
-// after batch k - n_sets trained; batch k trains after its sample half; both
-// streams start after the caller's stream and the caller's stream waits for both
-// at the end.
+// Ordering: the staging buffer of set k % n_sets is refilled (H2D) once batch
+// k - n_sets was SAMPLED (the train half reads a private copy the sample half
+// makes); the set's blocks are resampled once batch k - n_sets trained; batch k
+// trains after its sample half; all streams start after the caller's stream and
+// the caller's stream waits for them at the end.
 #include <cstring>
 #include <vector>
 
@@ -42,7 +43,7 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
     }
     cudaStream_t cs = (cudaStream_t)caller_stream, ss = (cudaStream_t)sample_stream, st = (cudaStream_t)train_stream;
     std::vector<cudaEvent_t> sampled(n_sets), trained(n_sets), copied(n_sets);
-    std::vector<char> has_trained(n_sets, 0);
+    std::vector<char> has_trained(n_sets, 0), has_sampled(n_sets, 0);
     cudaEvent_t start, end_s, end_t;
     const unsigned fl = cudaEventDisableTiming;
     cudaEventCreateWithFlags(&start, fl);
@@ -53,9 +54,10 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
         cudaEventCreateWithFlags(&trained[k], fl);
         cudaEventCreateWithFlags(&copied[k], fl);
     }
-    // staging H2D on its own stream: batch k's copy waits only for the set to be
-    // free (batch k - n_sets trained), so it lands while batch k-1 is still being
-    // sampled instead of in front of batch k's sample half
+    // staging H2D on its own stream: batch k's copy waits only for the set's
+    // staging buffer to be free (batch k - n_sets sampled), so it lands while
+    // earlier batches are still being sampled instead of in front of batch k's
+    // sample half
     cudaStream_t cp;
     cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
     cudaEventRecord(start, cs);
@@ -75,10 +77,12 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
     auto sample = [&](int k) {
         const int set = k % n_sets;
         pack(k);
-        if (has_trained[set]) {
-            cudaStreamWaitEvent(cp, trained[set], 0);
-            cudaStreamWaitEvent(ss, trained[set], 0);
-        }
+        // the set's staging buffer is free once its previous SAMPLE half ran (the
+        // train half reads the private copy that sample half made), so the H2D of
+        // batch k lands while earlier batches are still being sampled; the blocks
+        // of the set are free once its previous train half ran
+        if (has_sampled[set]) cudaStreamWaitEvent(cp, sampled[set], 0);
+        if (has_trained[set]) cudaStreamWaitEvent(ss, trained[set], 0);
         cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
                         (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, cp);
         cudaEventRecord(copied[set], cp);
@@ -86,6 +90,7 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
         const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(sample_execs[set]), ss);
         if (e != cudaSuccess && err == cudaSuccess) err = e;
         cudaEventRecord(sampled[set], ss);
+        has_sampled[set] = 1;
     };
     auto train = [&](int k) {
         const int set = k % n_sets;

@@ -410,3 +410,31 @@ extern "C" int hg_enable_peer_access(int32_t peer_device) {
     }
     return hg_check_launch("enable_peer_access");
 }
+
+// ---------------------------------------------------------------------------
+// Device-to-device copy of a small buffer as a kernel node (the per-batch input
+// block the sample half hands to the train half): inside a captured graph a
+// kernel node chains like its neighbours, a memcpy node does not.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_copy_words(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16,
+                             uint8_t* __restrict__ dtail, const uint8_t* __restrict__ stail, int tail) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x < tail) dtail[threadIdx.x] = stail[threadIdx.x];
+}
+}  // namespace
+
+extern "C" int hg_copy_bytes(void* dst, const void* src, int64_t nbytes, void* stream) {
+    if (nbytes <= 0) return HG_OK;
+    if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) {
+        hg_set_error("copy_bytes: dst and src must be 16-byte aligned");
+        return HG_EINVAL;
+    }
+    const int64_t n16 = nbytes / 16;
+    const int tail = (int)(nbytes - n16 * 16);
+    const int grid = (int)((n16 + 255) / 256) < 1 ? 1 : (int)((n16 + 255) / 256);
+    k_copy_words<<<grid < 64 ? grid : 64, 256, 0, (cudaStream_t)stream>>>(
+        (uint4*)dst, (const uint4*)src, n16, (uint8_t*)dst + n16 * 16, (const uint8_t*)src + n16 * 16, tail);
+    return hg_check_launch("copy_bytes");
+}

@@ -144,6 +144,11 @@ class SampleSet:
     counts_in: torch.Tensor  # int32 [2]: n_seeds, gradient divisor (global batch)
     bp: torch.Tensor         # int64 [BP_SIZE] parameter block
     stage: torch.Tensor      # uint8: bp | counts_in | seeds as ONE buffer (one H2D copy per batch)
+    # the train half's private copy of ``stage``, made by the sample half (a side
+    # branch of its graph): the next H2D into ``stage`` then only has to wait for
+    # this set's previous SAMPLE half, not its train half
+    tstage: torch.Tensor = None
+    tviews: tuple = None
 
 
 STAGE_COUNTS = BP_SIZE * 8       # byte offsets inside SampleSet.stage
@@ -161,9 +166,13 @@ class TrainEngine:
 
     # the current sample set's views (eager steps, capture and host planning use set `cur`)
     samplers = property(lambda self: self.sets[self.cur].samplers)
-    seeds = property(lambda self: self.sets[self.cur].seeds)
-    counts_in = property(lambda self: self.sets[self.cur].counts_in)
-    bp = property(lambda self: self.sets[self.cur].bp)
+    # per-batch inputs: the staging buffer while the sample half is enqueued, the
+    # train half's private copy of it while the train half is enqueued
+    seeds = property(lambda self: self.sets[self.cur].tviews[2] if self._train_view else self.sets[self.cur].seeds)
+    counts_in = property(lambda self: self.sets[self.cur].tviews[1] if self._train_view
+                         else self.sets[self.cur].counts_in)
+    bp = property(lambda self: self.sets[self.cur].tviews[0] if self._train_view else self.sets[self.cur].bp)
+    _train_view = False
 
     def __init__(self, dg: DeviceGraph, model: str, dims, fanouts, batch_cap: int, lr: float,
                  optimizer: str = "sgd", weights=None, hot: HotBuffers | None = None, max_batches: int = 1,
@@ -219,7 +228,9 @@ class TrainEngine:
                                 need_outdeg=(not self.sage) or l > 0, minpos=mps[l % 2]) for l in range(self.L)]
             stage = torch.zeros(STAGE_SEEDS + 4 * self.batch_cap, dtype=torch.uint8, device=dev)
             bp, counts_in, seeds = stage_views(stage)
-            self.sets.append(SampleSet(samplers=smp, seeds=seeds, counts_in=counts_in, bp=bp, stage=stage))
+            tstage = torch.zeros_like(stage)
+            self.sets.append(SampleSet(samplers=smp, seeds=seeds, counts_in=counts_in, bp=bp, stage=stage,
+                                       tstage=tstage, tviews=stage_views(tstage)))
         self.cur = 0
         # ---- parameters ----
         self.params = DenseParams(model, self.dims, weights, dev)
@@ -394,6 +405,12 @@ class TrainEngine:
             smp.run(fr, n, self.bp, l, main, dedup=not self._bottom_draws_only(l),
                     relabel_stream=sc if split else None)
             forked = forked or split
+            if l == self.L - 1:  # the train half's copy of the batch inputs, on the side branch
+                # (forked after the first kernels so the graph keeps a single root)
+                sc.wait_stream(main)
+                st_ = self.sets[self.cur]
+                _lib.call("hg_copy_bytes", ptr(st_.tstage), ptr(st_.stage), st_.stage.numel(), sc.cuda_stream)
+                forked = True
         if self.early_agg0():
             mark("sample_agg0")
             self._enqueue_agg0(main.cuda_stream)
@@ -401,6 +418,15 @@ class TrainEngine:
             main.wait_stream(sc)
 
     def enqueue_train_part(self, stream=None, mark=None):
+        """The train half of the current set; it reads the batch's inputs from the
+        private copy the sample half made (SampleSet.tstage)."""
+        self._train_view = True
+        try:
+            self._enqueue_train_part(stream, mark)
+        finally:
+            self._train_view = False
+
+    def _enqueue_train_part(self, stream=None, mark=None):
         main = stream if stream is not None else torch.cuda.current_stream(self.device)
         s = main.cuda_stream
         L, P = self.L, self.params
