@@ -22,6 +22,8 @@ def main():
     K = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seg = len(sys.argv) > 2 and sys.argv[2] == "seg"
     two = len(sys.argv) > 2 and sys.argv[2] == "2ss"  # alternate two sample streams (needs >= 3 sets)
+    native = len(sys.argv) > 2 and sys.argv[2] == "native"  # inputs by pinned H2D on a copy stream, as
+    # hg_pipeline_run does (gated by the set's previous sample half)
     ds = make_dataset("c2", cache_dir=bench.CACHE)
     cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
                       strategy="case1", hot_ratio=0.0, use_graph=True, seed=0, report_transfers=False)
@@ -40,6 +42,15 @@ def main():
     ss, st = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ss2 = torch.cuda.Stream(device=dev)
     ss_main = ss
+    cp = torch.cuda.Stream(device=dev)
+    from paper_2311_13225_b200.engine import STAGE_SEEDS
+    slot = STAGE_SEEDS + 4 * e.batch_cap
+    pinned = torch.zeros((K + 4, slot), dtype=torch.uint8).pin_memory()
+    for i in range(K + 4):  # the same inputs the device-resident loop copies, packed per step
+        row = pinned[i]
+        row[:64].view(torch.int64).copy_(d_bp[i].cpu())
+        row[64:72].view(torch.int32).copy_(d_counts.cpu())
+        row[STAGE_SEEDS:STAGE_SEEDS + 4096].view(torch.int32).copy_(d_seeds[i].cpu())
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     SPLIT = ("sample_l1", "sample_l0", "sample_agg0", "fwd0_gemm", "fwd_upper", "loss", "bwd", "update")
     parts = [e.capture_segments(split_at=SPLIT, set_index=k) for k in range(ns)] if seg else None
@@ -54,16 +65,26 @@ def main():
         ss2.wait_stream(cur)
         st.wait_stream(cur)
 
+        sampled_prev = [None] * ns
+
         def sample(i):
             k = i % ns
             ss = ss2 if (two and i % 2) else ss_main
+            if native:
+                if sampled_prev[k] is not None:
+                    cp.wait_event(sampled_prev[k])
+                with torch.cuda.stream(cp):
+                    e.sets[k].stage.copy_(pinned[i], non_blocking=True)
+                    cpd = torch.cuda.Event(); cpd.record(cp)
+                ss.wait_event(cpd)
             if trained[k] is not None:
                 ss.wait_event(trained[k])
             with torch.cuda.stream(ss):
                 s = e.sets[k]
-                s.seeds.copy_(d_seeds[i])
-                s.bp.copy_(d_bp[i])
-                s.counts_in.copy_(d_counts)
+                if not native:
+                    s.seeds.copy_(d_seeds[i])
+                    s.bp.copy_(d_bp[i])
+                    s.counts_in.copy_(d_counts)
                 if record:
                     a = ev(); a.record(ss); marks["s0"].append(a)
                 if seg:
@@ -77,6 +98,7 @@ def main():
                 if record:
                     b = ev(); b.record(ss); marks["s1"].append(b)
                 sampled[k].record(ss)
+                sp = torch.cuda.Event(); sp.record(ss); sampled_prev[k] = sp
 
         def train(i):
             k = i % ns
