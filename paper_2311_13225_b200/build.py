@@ -53,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     odir = PKG / "build"
     odir.mkdir(exist_ok=True)
     flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    flags += os.environ.get("HG_NVCC_EXTRA", "").split()  # experiment variants (-D knobs); empty in the product
 
     def compile_one(src):
         obj = odir / (src.stem + ".o")

@@ -63,6 +63,27 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 __device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
+// Epilogue store of 32 columns of this thread's output row (TMEM lane = row;
+// float4 stores when aligned).  A shared-memory staged form that turns the
+// row-per-thread stores into 128-byte row segments was measured slower in the
+// step (+18 KB of shared memory per CTA costs co-residency).
+__device__ __forceinline__ void epi_row32(const uint32_t (&r0)[16], const uint32_t (&r1)[16], int act,
+                                          float* __restrict__ crow, int lim, bool vec) {
+    auto val = [&](int j) {
+        const float v = __uint_as_float(j < 16 ? r0[j] : r1[j - 16]);
+        return act ? fmaxf(v, 0.f) : v;
+    };
+    if (vec && lim >= 32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(crow + j) = make_float4(val(j), val(j + 1), val(j + 2), val(j + 3));
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < lim) crow[j] = val(j);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // forward / dX: persistent CTAs over 128-row M tiles (blockIdx.y = BN-wide N tile)
 template <int BN>
@@ -192,33 +213,8 @@ k_gemm_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUt
                 tmem_ld16_nowait(ta, r0);
                 tmem_ld16_nowait(ta + 16, r1);
                 tmem_wait_ld();
-                if (gm < M && n0 + c0 < N && !(c_dbg & 4)) {
-                    float* crow = C + (int64_t)gm * ldc + n0 + c0;
-                    const int lim = N - (n0 + c0);
-                    if (vec && lim >= 32) {
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            float4 o = make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]),
-                                                   __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
-                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
-                            *reinterpret_cast<float4*>(crow + j) = o;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            float4 o = make_float4(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1]),
-                                                   __uint_as_float(r1[j + 2]), __uint_as_float(r1[j + 3]));
-                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
-                            *reinterpret_cast<float4*>(crow + 16 + j) = o;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            if (j < lim) crow[j] = act ? fmaxf(__uint_as_float(r0[j]), 0.f) : __uint_as_float(r0[j]);
-                            if (16 + j < lim)
-                                crow[16 + j] = act ? fmaxf(__uint_as_float(r1[j]), 0.f) : __uint_as_float(r1[j]);
-                        }
-                    }
-                }
+                if (gm < M && n0 + c0 < N && !(c_dbg & 4))
+                    epi_row32(r0, r1, act, C + (int64_t)gm * ldc + n0 + c0, N - (n0 + c0), vec);
             }
             tc_fence_before();
             __syncwarp();
@@ -424,33 +420,8 @@ k_gemm_tma_ts(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ 
                     }
                 }
                 tmem_wait_ld();
-                if (gm < M && n0 + c0 < N && !(c_dbg & 4)) {
-                    float* crow = C + (int64_t)gm * ldc + n0 + c0;
-                    const int lim = N - (n0 + c0);
-                    if (vec && lim >= 32) {
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            float4 o = make_float4(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1]),
-                                                   __uint_as_float(r0[j + 2]), __uint_as_float(r0[j + 3]));
-                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
-                            *reinterpret_cast<float4*>(crow + j) = o;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            float4 o = make_float4(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1]),
-                                                   __uint_as_float(r1[j + 2]), __uint_as_float(r1[j + 3]));
-                            if (act) { o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f); }
-                            *reinterpret_cast<float4*>(crow + 16 + j) = o;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            if (j < lim) crow[j] = act ? fmaxf(__uint_as_float(r0[j]), 0.f) : __uint_as_float(r0[j]);
-                            if (16 + j < lim)
-                                crow[16 + j] = act ? fmaxf(__uint_as_float(r1[j]), 0.f) : __uint_as_float(r1[j]);
-                        }
-                    }
-                }
+                if (gm < M && n0 + c0 < N && !(c_dbg & 4))
+                    epi_row32(r0, r1, act, C + (int64_t)gm * ldc + n0 + c0, N - (n0 + c0), vec);
             }
             tc_fence_before();
             __syncwarp();
@@ -684,12 +655,12 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 for (int jj = 0; jj < 16; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __uint_as_float(p[jj]));
             }
             tmem_wait_ld();
-            if (gk < K && c0 < N) {
-                float* prow = P + (int64_t)gk * N + c0;
+            if (gk < K && c0 < N) {  // partials are N-major: lanes (consecutive k) store one 128-byte line
+                float* pcol = P + (int64_t)c0 * K + gk;
                 const int lim = N - c0;
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj)
-                    if (jj < lim) prow[jj] = __uint_as_float(r[jj]);
+                    if (jj < lim) pcol[(int64_t)jj * K] = __uint_as_float(r[jj]);
             }
         }
         tc_fence_before();
@@ -703,10 +674,12 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
 }
 
 // Fixed-order reduction of the active chunks' partials (chunk order, then the
-// 8 warp sums in order): deterministic for a given M.
-__global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restrict__ partial, int KN, int n_chunks,
+// 8 warp sums in order): deterministic for a given M.  Partials are N-major
+// ([n][k], element e = n*K + k); the result is written row-major dW[k][n].
+__global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restrict__ partial, int K, int N, int n_chunks,
                                                           const int* __restrict__ d_M, int M_cap,
                                                           float* __restrict__ out1, float* __restrict__ out2) {
+    const int KN = K * N;
     hg_pdl_begin();
     __shared__ float s_part[8][33];
     const int M = hg_load_count(d_M, M_cap);
@@ -726,8 +699,9 @@ __global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restric
     if (w == 0 && e < KN) {
         float t = 0.f;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) t += s_part[k][lane];
-        (s ? out2 : out1)[e] = t;
+        for (int i = 0; i < 8; ++i) t += s_part[i][lane];
+        const int n = e / K, k = e - n * K;
+        (s ? out2 : out1)[(int64_t)k * N + n] = t;
     }
 }
 
@@ -920,7 +894,7 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
         else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
         if (rc) return rc;
     }
-    hg_launch(k_wgrad_tma_reduce, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K * N, n_chunks, d_M, M_cap,
-                                                                                out1, out2);
+    hg_launch(k_wgrad_tma_reduce, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K, N, n_chunks, d_M, M_cap,
+              out1, out2);
     return hg_check_launch("wgrad_tma_reduce");
 }
