@@ -37,15 +37,27 @@ constexpr int FWD_THREADS = 320;  // w0 TMA, w1 MMA, w2-5 split, w6-9 epilogue
 constexpr int WG_THREADS = 320;   // w0 TMA, w1 MMA, w2-9 split (w2-5 also the final epilogue)
 constexpr int WG_SPLIT = WG_THREADS - 64;
 constexpr int A_BYTES = 128 * 128;  // 128 rows x 32 fp32 (fwd) / 32 rows x 128 fp32 (wgrad)
+// pipeline depths (shared memory per CTA also decides what else fits on the SM
+// while these persistent kernels run)
+#ifndef HG_WG_STAGES64
+#define HG_WG_STAGES64 5
+#endif
+#ifndef HG_TS_PAIR_STAGES
+#define HG_TS_PAIR_STAGES 6
+#endif
 
 template <int BN>
 __host__ __device__ constexpr int fwd_stages() { return BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2; }
 template <int BN>
 __host__ __device__ constexpr int fwd_stage_bytes() { return 2 * A_BYTES + 2 * BN * 128; }
 template <int BN>
-__host__ __device__ constexpr int wg_stages() { return BN <= 64 ? 4 : BN <= 128 ? 3 : 2; }
-template <int BN>
-__host__ __device__ constexpr int wg_stage_bytes() { return 2 * A_BYTES + 2 * BN * 128; }
+__host__ __device__ constexpr int wg_stages() { return BN <= 64 ? HG_WG_STAGES64 : BN <= 128 ? 3 : 2; }
+// wgrad stage: [A | A lo (SS form only) | G hi | G lo]; the TS form (A^T through
+// TMEM) never writes A lo to shared memory, so its stages are 16 KB smaller
+template <int BN, bool TSA>
+__host__ __device__ constexpr int wg_goff() { return (TSA ? 1 : 2) * A_BYTES; }
+template <int BN, bool TSA>
+__host__ __device__ constexpr int wg_stage_bytes() { return wg_goff<BN, TSA>() + 2 * BN * 128; }
 template <int C>
 __host__ __device__ constexpr uint32_t tmem_cols() { return C <= 32 ? 32 : C <= 64 ? 64 : C <= 128 ? 128 : C <= 256 ? 256 : 512; }
 
@@ -249,7 +261,11 @@ __host__ __device__ constexpr int ts_stage_bytes() { return A_BYTES + 2 * BN * 1
 template <int BN, bool PAIR>
 __host__ __device__ constexpr int ts_acc_cols() { return PAIR ? 2 * BN : BN; }
 template <int BN, bool PAIR>
-__host__ __device__ constexpr int ts_nstages() { return PAIR ? (512 - 2 * ts_acc_cols<BN, PAIR>()) / 64 : ts_stages<BN>(); }
+__host__ __device__ constexpr int ts_nstages() {
+    return PAIR ? ((512 - 2 * ts_acc_cols<BN, PAIR>()) / 64 < HG_TS_PAIR_STAGES ? (512 - 2 * ts_acc_cols<BN, PAIR>()) / 64
+                                                                                : HG_TS_PAIR_STAGES)
+                : ts_stages<BN>();
+}
 
 template <int BN, bool PAIR>
 __global__ void __launch_bounds__(FWD_THREADS, 1)
@@ -459,7 +475,8 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
             int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
     constexpr int S = wg_stages<BN>();
-    constexpr int STAGE = wg_stage_bytes<BN>();
+    constexpr int STAGE = wg_stage_bytes<BN, TSA>();
+    constexpr int GOFF = wg_goff<BN, TSA>();
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
     constexpr int NG = BN / 32;       // G boxes (32 columns each) per stage
     constexpr uint32_t ACC = PAIR ? 2 * BN : BN;
@@ -523,7 +540,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 }
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
-                    tma_load_2d(smem_u32(base + 2 * A_BYTES + g * 4096), &tmG, g * 32, y, &full[st]);
+                    tma_load_2d(smem_u32(base + GOFF + g * 4096), &tmG, g * 32, y, &full[st]);
             }
         }
     } else if (warp == 1) {
@@ -534,7 +551,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 TL(3, j);
                 tc_fence_after();
                 const uint32_t a_hi = smem_u32(smem + st * STAGE), a_lo = a_hi + A_BYTES;
-                const uint32_t g_hi = a_hi + 2 * A_BYTES, g_lo = g_hi + G_TILE;
+                const uint32_t g_hi = a_hi + GOFF, g_lo = g_hi + G_TILE;
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {  // 8 reduction rows (two 4-row K atoms) per MMA
                     if (c_dbg & 1) break;
@@ -596,7 +613,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 float4 va[NA > 0 ? NA : 1], vg[NGC];
 #pragma unroll
                 for (int i = 0; i < NA; ++i) va[i] = *reinterpret_cast<const float4*>(base + (t + WG_SPLIT * i) * 16);
-                uint8_t* gb = base + 2 * A_BYTES;
+                uint8_t* gb = base + GOFF;
 #pragma unroll
                 for (int i = 0; i < NGC; ++i)
                     if (t + WG_SPLIT * i < G_TILE / 16) vg[i] = *reinterpret_cast<const float4*>(gb + (t + WG_SPLIT * i) * 16);
@@ -794,19 +811,20 @@ template <int BN>
 int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, const CUtensorMap& mg, int K,
               int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo,
               bool tsa) {
-    const int smem = wg_stages<BN>() * wg_stage_bytes<BN>() + 1024;
+    const int smem_ss = wg_stages<BN>() * wg_stage_bytes<BN, false>() + 1024;
+    const int smem_ts = wg_stages<BN>() * wg_stage_bytes<BN, true>() + 1024;
     constexpr bool PB = BN <= 64;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_wgrad_tma<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_wgrad_tma<BN, PB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_wgrad_tma<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_wgrad_tma<BN, PB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ss);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, PB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ss);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ts);
+        cudaFuncSetAttribute(k_wgrad_tma<BN, PB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ts);
         attr = true;
     }
 #define HG_WG(P, T)                                                                                                  \
-    hg_launch(k_wgrad_tma<BN, P, T>, grid, WG_THREADS, smem, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, partial, \
-              lbo, sbo)
+    hg_launch(k_wgrad_tma<BN, P, T>, grid, WG_THREADS, T ? smem_ts : smem_ss, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, \
+              n_chunks, partial, lbo, sbo)
     const bool pair = g_pair && PB;
     if (pair && tsa) HG_WG(PB, true);
     else if (pair) HG_WG(PB, false);
@@ -862,7 +880,12 @@ int hg_gemm_tma_launch(const float* A1, int lda1, int K1, const float* A2, int l
     }
 }
 
-int hg_wgrad_tma_chunks(int K, int n_src) {
+// Split-M chunk count: one CTA per (source, K tile, chunk), one wave.  (Capping
+// it by the layer's row count — >= 128/256/512 rows per chunk for the small
+// upper layers — measured slower in the pipelined step: 178.5/179.4/185.4 vs
+// 178.1 us; the side-stream weight gradients are latency-, not SM-time-bound.)
+int hg_wgrad_tma_chunks(int K, int n_src, int M_cap) {
+    (void)M_cap;
     const int units = hg_ceil_div(K > 0 ? K : 1, 128) * n_src;
     const int c = HG_NUM_SMS / units;
     return c < 1 ? 1 : c;
@@ -873,7 +896,7 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
                         cudaStream_t s) {
     const int n_src = A2 ? 2 : 1;
     const int ktiles = hg_ceil_div(K, 128);
-    const int n_chunks = hg_wgrad_tma_chunks(K, n_src);
+    const int n_chunks = hg_wgrad_tma_chunks(K, n_src, M_cap);
     if (M_cap > 0) {
         CUtensorMap m1, m2, mg;
         const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
