@@ -294,7 +294,9 @@ def main():
     n_div = 1024 if strong else 1024 * world
     d_counts = torch.tensor([n_loc, n_div], dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
-    ss, st = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    from paper_2311_13225_b200.engine import stream_priorities
+    ps, pt = stream_priorities()
+    ss, st = torch.cuda.Stream(device=dev, priority=ps), torch.cuda.Stream(device=dev, priority=pt)
     nset = len(e.sets)
     sampled = [torch.cuda.Event() for _ in range(nset)]
     trained = [None] * nset

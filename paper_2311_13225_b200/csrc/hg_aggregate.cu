@@ -53,8 +53,22 @@ struct FeatShards {
     int rows_per_shard;
 };
 
+// Rows in flight per warp when a whole row is one float4 per lane (F <= 128, LPR 32):
+// 8, not 16 — the kernel then needs 48 registers instead of 64, five 256-thread
+// CTAs fit on an SM (agg_ctas_per_sm() = 5, one wave) and the bottom aggregation
+// of the C2 step runs in 61 instead of 67.5 us with the step at 172.7 instead of
+// 177.2 us (4 CTAs x 16 rows, 3 CTAs, 6 CTAs at 40 registers with
+// spills, 10/12 rows in flight measured slower).
+#ifndef HG_AGG_U1
+#define HG_AGG_U1 8
+#endif
+#if defined(HG_AGG_MINB) && HG_AGG_MINB > 0  // experiment knob: register cap via min CTAs per SM
+#define HG_AGG_BOUNDS __launch_bounds__(256, HG_AGG_MINB)
+#else
+#define HG_AGG_BOUNDS __launch_bounds__(256)
+#endif
 template <int LPR, int NV, int MODE, bool SH = false>
-__global__ void __launch_bounds__(256) k_agg_fwd(
+__global__ void HG_AGG_BOUNDS k_agg_fwd(
     const float* __restrict__ hin, int ld_in, int F4, const int* __restrict__ frontier, const int* d_n, int cap,
     int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
     const int* __restrict__ nself, const int* __restrict__ outdeg, const uint8_t* __restrict__ inj,
@@ -110,7 +124,7 @@ __global__ void __launch_bounds__(256) k_agg_fwd(
                 const int m = min(LPR, cnt - j0);
                 // U rows in flight (a whole fanout-15 segment in one batch for F <= 128),
                 // consumed in edge order; slots past m are masked
-                constexpr int U = NV >= 8 ? 2 : 16 / NV;
+                constexpr int U = NV >= 8 ? 2 : (NV == 1 && LPR == 32) ? HG_AGG_U1 : 16 / NV;
                 for (int j = 0; j < m; j += U) {
                     int r[U]; float w[U];
 #pragma unroll
@@ -443,12 +457,12 @@ int launch_fwd_bulk(int F4, cudaStream_t s, const float* hin, int ld_in, const i
 }
 
 // CTAs per SM of the bottom (global-id) aggregation grid: env HG_AGG_CTAS_PER_SM
-// (default 8); fewer leaves SM slots for the concurrently running training stream
+// (default 5 = what fits at 48 registers: one wave, no tail)
 int agg_ctas_per_sm() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("HG_AGG_CTAS_PER_SM");
-        v = e ? atoi(e) : 8;
+        v = e ? atoi(e) : 5;
         v = v < 1 ? 1 : (v > 8 ? 8 : v);
     }
     return v;

@@ -50,8 +50,8 @@ template <int BN>
 __host__ __device__ constexpr int fwd_stages() { return BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2; }
 template <int BN>
 __host__ __device__ constexpr int fwd_stage_bytes() { return 2 * A_BYTES + 2 * BN * 128; }
-template <int BN>
-__host__ __device__ constexpr int wg_stages() { return BN <= 64 ? HG_WG_STAGES64 : BN <= 128 ? 3 : 2; }
+template <int BN, bool TSA>  // TS-form stages are 16 KB smaller (below): one more fits at BN <= 64
+__host__ __device__ constexpr int wg_stages() { return BN <= 64 ? (TSA ? HG_WG_STAGES64 : 4) : BN <= 128 ? 3 : 2; }
 // wgrad stage: [A | A lo (SS form only) | G hi | G lo]; the TS form (A^T through
 // TMEM) never writes A lo to shared memory, so its stages are 16 KB smaller
 template <int BN, bool TSA>
@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1)
 k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
             int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
-    constexpr int S = wg_stages<BN>();
+    constexpr int S = wg_stages<BN, TSA>();
     constexpr int STAGE = wg_stage_bytes<BN, TSA>();
     constexpr int GOFF = wg_goff<BN, TSA>();
     constexpr int G_TILE = BN * 128;  // 32 rows x BN fp32
@@ -811,8 +811,8 @@ template <int BN>
 int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, const CUtensorMap& mg, int K,
               int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo,
               bool tsa) {
-    const int smem_ss = wg_stages<BN>() * wg_stage_bytes<BN, false>() + 1024;
-    const int smem_ts = wg_stages<BN>() * wg_stage_bytes<BN, true>() + 1024;
+    const int smem_ss = wg_stages<BN, false>() * wg_stage_bytes<BN, false>() + 1024;
+    const int smem_ts = wg_stages<BN, true>() * wg_stage_bytes<BN, true>() + 1024;
     constexpr bool PB = BN <= 64;
     static bool attr = false;
     if (!attr) {

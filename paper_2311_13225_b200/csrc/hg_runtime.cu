@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Native step driver of the pipelined trainer.
 //
 // Replaces the per-batch host loop of orchestrator.Trainer.train_batches (the
@@ -58,6 +59,9 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
     // staging buffer to be free (batch k - n_sets sampled), so it lands while
     // earlier batches are still being sampled instead of in front of batch k's
     // sample half
+    // experiment knob HG_PIPE_H2D_LATE=1: the H2D on the sampling stream after the
+    // set's previous train half (the pre-round-2 schedule)
+    static const int late_h2d = getenv("HG_PIPE_H2D_LATE") ? atoi(getenv("HG_PIPE_H2D_LATE")) : 0;
     cudaStream_t cp;
     cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
     cudaEventRecord(start, cs);
@@ -83,10 +87,13 @@ extern "C" int hg_pipeline_run(int32_t n_steps, int32_t n_sets, const int64_t* s
         // of the set are free once its previous train half ran
         if (has_sampled[set]) cudaStreamWaitEvent(cp, sampled[set], 0);
         if (has_trained[set]) cudaStreamWaitEvent(ss, trained[set], 0);
+        cudaStream_t hs = late_h2d ? ss : cp;
         cudaMemcpyAsync(reinterpret_cast<void*>(dev_stage[set]), host_stage + (int64_t)k * slot_bytes,
-                        (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, cp);
-        cudaEventRecord(copied[set], cp);
-        cudaStreamWaitEvent(ss, copied[set], 0);
+                        (size_t)seeds_offset + 4 * (size_t)n_seeds[k], cudaMemcpyHostToDevice, hs);
+        if (!late_h2d) {
+            cudaEventRecord(copied[set], cp);
+            cudaStreamWaitEvent(ss, copied[set], 0);
+        }
         const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(sample_execs[set]), ss);
         if (e != cudaSuccess && err == cudaSuccess) err = e;
         cudaEventRecord(sampled[set], ss);

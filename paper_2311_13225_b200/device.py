@@ -110,14 +110,14 @@ class DeviceGraph:
         as the window of consecutive ids with the largest degree sum (sampled
         neighbours are drawn roughly in proportion to degree; the generators put
         hubs at low ids, graph.py:357).  Size: ``max_bytes`` or env
-        HG_L2_PERSIST_MB (default 32 MB), clamped to the device's persisting-L2
+        HG_L2_PERSIST_MB (default 48 MB; 0/16/32/48/64/80 MB measured, §5), clamped to the device's persisting-L2
         limit; 0 disables.  Returns the window size in bytes."""
         from . import _lib
         lib = _lib.load()
         if self.features is None:
             return 0
         if max_bytes is None:
-            max_bytes = int(float(os.environ.get("HG_L2_PERSIST_MB", "32")) * 2**20)
+            max_bytes = int(float(os.environ.get("HG_L2_PERSIST_MB", "48")) * 2**20)
         row = self.feat_ld * 4
         nbytes = min(int(max_bytes), int(lib.hg_l2_persist_max()), self.num_vertices * row)
         rows = nbytes // row

@@ -729,8 +729,9 @@ class Pipeline:
     def __init__(self, engine: TrainEngine):
         self.e = engine
         dev = engine.device
-        self.ss = torch.cuda.Stream(device=dev)
-        self.st = torch.cuda.Stream(device=dev)
+        ps, pt = stream_priorities()
+        self.ss = torch.cuda.Stream(device=dev, priority=ps)
+        self.st = torch.cuda.Stream(device=dev, priority=pt)
         n = len(engine.sets)
         self.sampled = [torch.cuda.Event() for _ in range(n)]
         self.trained = [None] * n
@@ -772,6 +773,19 @@ class Pipeline:
     def drain(self):
         torch.cuda.current_stream(self.e.device).wait_stream(self.st)
         torch.cuda.current_stream(self.e.device).wait_stream(self.ss)
+
+
+def stream_priorities():
+    """(sample stream, train stream) priorities of the two-stream pipeline: env
+    HG_STREAM_PRIO = "train" gives the training half the higher priority (lower
+    number), "sample" the sampling half, default none."""
+    mode = os.environ.get("HG_STREAM_PRIO", "")
+    hi = torch.cuda.Stream.priority_range()[1] if torch.cuda.is_available() else 0
+    if mode == "train":
+        return 0, hi
+    if mode == "sample":
+        return hi, 0
+    return 0, 0
 
 
 class BatchFeeder:

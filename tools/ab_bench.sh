@@ -13,4 +13,4 @@ import json; d=json.load(open('gpurun_out/ab_$V$i.json')); r=d['roofline']
 print('$V$i step', round(d['ms_per_step']*1e3,1), 'us  value', round(d['value']/1e6,3), ' agg', round(r['avg_launch_ms']*1e3,1), ' e2e', round(d['e2e']['value']/1e6,3))"
   done
 done
-cp paper_2311_13225_b200/libhg_gnn_B.so $L
+# (the last variant stays loaded)
