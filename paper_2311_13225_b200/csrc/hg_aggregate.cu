@@ -97,6 +97,7 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
         for (int k = 0; k < NV; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         const bool skip = inj && inj[i];
         const int v = frontier[i];
+        const int64_t sbase = (int64_t)i * f;
         if (!skip) {
             if (GLOBAL && self_out) {  // self row gather (the SAGE/GCN-free "gather" part)
                 const float4* src = rowp(v);
@@ -108,7 +109,6 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
                 }
             }
             const int cnt = counts[i];
-            const int64_t sbase = (int64_t)i * f;
             float wd = 0.f;
             if (!GCN) { const int ns = nself[i]; wd = ns > 0 ? 1.0f / (float)ns : 0.f; }
             for (int j0 = 0; j0 < cnt; j0 += LPR) {
@@ -700,18 +700,13 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
         const long long q = q0 + threadIdx.x / LPR;
         if (q >= Q) continue;
         const int d = (int)(q / f), j = (int)(q - (long long)d * f);
+        // round 1: everything that depends only on the slot (issued before any
+        // branch; slots past the destination's count hold stale ids, unused)
         const int cnt = counts[d];
-        if (j >= cnt) continue;
         const int s = slot_local[q];
-        float w;
-        if (GCN) {
-            w = gcn_w(outdeg[s], cnt);
-        } else {
-            if (slot_g[q] == frontier[d]) continue;  // SAGE drops self edges (gnnmath.py:148)
-            const int ns = nself[d];
-            w = ns > 0 ? 1.0f / (float)ns : 0.f;
-        }
-        const int od = outdeg[s];
+        const int sg = GCN ? 0 : slot_g[q];
+        const int fd = GCN ? 0 : frontier[d];
+        const int ns = GCN ? 0 : nself[d];
         float4 x[NV];
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -719,15 +714,30 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
             x[k] = c < F4 ? __ldg(reinterpret_cast<const float4*>(dagg + (int64_t)d * ld_dagg) + c)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        if (j >= cnt) continue;
+        if (!GCN && sg == fd) continue;  // SAGE drops self edges (gnnmath.py:148)
+        // round 2: the source's out-degree, ReLU' mask row and injected flag together
+        const int od = outdeg[s];
+        const bool zero_row = inj && inj[s];
+        float4 h[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            const int c = lr + k * LPR;
+            h[k] = (hmask && c < F4) ? __ldg(reinterpret_cast<const float4*>(hmask + (int64_t)s * ld_hmask) + c)
+                                     : make_float4(1.f, 1.f, 1.f, 1.f);
+        }
+        const float w = GCN ? gcn_w(od, cnt) : (ns > 0 ? 1.0f / (float)ns : 0.f);
         if (s >= n && od == 1) {  // single contribution: final row, no accumulator
-            const bool zero_row = inj && inj[s];
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 const int c = lr + k * LPR;
                 if (c < F4) {
                     float4 a = make_float4(w * x[k].x, w * x[k].y, w * x[k].z, w * x[k].w);
                     bad |= finite_flag(a);
-                    reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx)[c] = bwd_mask(a, hmask, ld_hmask, s, c, zero_row);
+                    a.x = h[k].x > 0.f ? a.x : 0.f; a.y = h[k].y > 0.f ? a.y : 0.f;
+                    a.z = h[k].z > 0.f ? a.z : 0.f; a.w = h[k].w > 0.f ? a.w : 0.f;
+                    if (zero_row) a = make_float4(0.f, 0.f, 0.f, 0.f);
+                    reinterpret_cast<float4*>(dx + (int64_t)s * ld_dx)[c] = a;
                 }
             }
             continue;
