@@ -10,6 +10,10 @@
 // and HBM-bound (K <= 2F, N <= 256), so the 3x MMA count is free.
 //
 #include "hg_common.cuh"
+#ifndef HG_GEMM_MAX_BN
+#define HG_GEMM_MAX_BN 128  // widest N tile of the forward / dX GEMMs: wider N runs as several 128-wide TS-form
+                            // N tiles (C3: 3.61 -> 3.82 M seeds/s vs one 256-wide SS-form tile, 2 stages)
+#endif
 #include "hg_gnn_internal.h"
 #include "hg_tc.cuh"
 
@@ -149,7 +153,7 @@ __global__ void k_prep_b(const float* __restrict__ B, int ldb, int trans_b, int 
 
 int gemm_bn(int N) {
     const int Nr = (N + 15) & ~15;
-    return Nr <= 32 ? 32 : Nr <= 64 ? 64 : Nr <= 128 ? 128 : 256;
+    return Nr <= 32 ? 32 : Nr <= 64 ? 64 : (Nr <= 128 || HG_GEMM_MAX_BN <= 128) ? 128 : 256;
 }
 
 
