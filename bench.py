@@ -467,6 +467,8 @@ def main():
     if args.phases and rank == 0:
         phases = phase_breakdown(e, d_seeds, d_bp, d_counts, W)
     if rank != 0:
+        if dist_ctx:
+            dist_ctx.close()
         return
     cpu_base = None
     if not args.no_cpu_baseline and world == 1:
@@ -510,6 +512,8 @@ def main():
     if phases:
         line["phases_ms"] = phases
     print(json.dumps(line), flush=True)
+    if dist_ctx:
+        dist_ctx.close()
 
 
 def run_epoch_mode(spec: str):

@@ -64,7 +64,15 @@ class DistContext:
         return float(t.item())
 
     def barrier(self):
-        dist.barrier()
+        if dist.get_backend() == "nccl" and torch.cuda.is_available():
+            dist.barrier(device_ids=[torch.cuda.current_device()])
+        else:
+            dist.barrier()
+
+    def close(self):
+        """Tear the process group down (end of a run)."""
+        if dist.is_initialized():
+            dist.destroy_process_group()
 
 
 class ShardedFeatures:
