@@ -153,9 +153,13 @@ __global__ void k_store_put(const int* __restrict__ ids, const int* d_n, int cap
                             int* __restrict__ ver, int* __restrict__ stamp, int version, int stamp_val,
                             int* __restrict__ d_puts) {
     hg_pdl_begin();
+    __shared__ int s_puts;
+    if (threadIdx.x == 0) s_puts = 0;
+    __syncthreads();
     const int n = hg_load_count(d_n, cap);
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
+    int puts = 0;
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
         const int slot = slot_of[ids[i]];
         if (slot < 0) continue;  // not a hot vertex: caller bug, ignored
@@ -163,9 +167,14 @@ __global__ void k_store_put(const int* __restrict__ ids, const int* d_n, int cap
         if (lane == 0) {
             ver[slot] = version;
             stamp[slot] = stamp_val;
-            if (d_puts) atomicAdd(d_puts, 1);
+            ++puts;
         }
     }
+    // one counter atomic per CTA (a per-row atomic on the single counter serialised
+    // ~23 K updates per producer chunk: 27 us of the 28 us kernel, ncu)
+    if (lane == 0 && puts) atomicAdd(&s_puts, puts);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_puts && d_puts) atomicAdd(d_puts, s_puts);
 }
 
 // lookup (store.py:67-98) for every bottom destination in the current cpu_set
