@@ -350,10 +350,16 @@ class TrainEngine:
         self.enqueue_train_part(main, mark)
 
     def early_agg0(self) -> bool:
-        """Bottom gather+aggregate in the sample half (no weights involved); kept
-        in the train half when hot embeddings are injected (its skip mask comes
-        from the store lookup) or with HG_EARLY_AGG=0."""
-        return self.hot is None and os.environ.get("HG_EARLY_AGG", "1") != "0"
+        """Bottom gather+aggregate in the sample half (no weights involved), also
+        with hot-embedding reuse: there the rows of destinations that the train
+        half's store lookup will inject are aggregated too (no skip mask yet) and
+        simply overwritten after the GEMM — their dz is masked to zero, so the
+        weight gradient is bit-identical — which keeps the aggregation overlapped
+        with the previous batch's training.  HG_EARLY_AGG=0: in the train half,
+        skipping the injected rows (HG_EARLY_AGG_HOT=0: that only with reuse)."""
+        if os.environ.get("HG_EARLY_AGG", "1") == "0":
+            return False
+        return self.hot is None or os.environ.get("HG_EARLY_AGG_HOT", "1") != "0"
 
     def _bottom_bufs(self):
         """(self rows, aggregate) buffers of the bottom layer for the current set."""
