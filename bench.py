@@ -495,9 +495,13 @@ def main():
                          "kernel_timing": "CUDA events on the kernel's stream over a second pass of the same steps "
                                           "with the sample and train halves back to back (the headline pass "
                                           "overlaps them)",
+                         "frac_vs_spec_8tbs": achieved / 8000.0,
                          "random_row_ceiling": {"gbs_of_row_data": 4000.0,
                                                 "source": "profiles/r01_gather_ceiling.txt (738K uniformly random "
-                                                          "400-byte rows, no compute: 72.6-75.8 us)"},
+                                                          "400-byte rows, no compute: 72.6-75.8 us); cost per 128-B "
+                                                          "line touched: profiles/r02s_gather_rowsize.txt; this "
+                                                          "block's own fetch list as a pure gather: 55-61 us, "
+                                                          "profiles/r02_order_probe.txt"},
                          "block0": {"n_dst": n_dst0, "n_src": n_src0, "edges": E0},
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
             "cpu_baseline": cpu_base,
