@@ -727,8 +727,7 @@ __global__ void __launch_bounds__(256) k_bwd_scatter(
                                      : make_float4(1.f, 1.f, 1.f, 1.f);
         }
         const float w = GCN ? gcn_w(od, cnt) : (ns > 0 ? 1.0f / (float)ns : 0.f);
-        if ((GCN || s >= n) && od == 1) {  // single contribution: final row, no accumulator
-            // (GCN: destinations too — no self term is added to them; SAGE adds dself in the finish)
+        if (s >= n && od == 1) {  // single contribution: final row, no accumulator
 #pragma unroll
             for (int k = 0; k < NV; ++k) {
                 const int c = lr + k * LPR;
@@ -773,8 +772,7 @@ __global__ void __launch_bounds__(256) k_bwd_finish(
     for (int s0 = blockIdx.x * groups_per_block; s0 < n_src; s0 += gridDim.x * groups_per_block) {
         const int s = s0 + threadIdx.x / LPR;
         if (s >= n_src) continue;
-        // written by the scatter's fast path (destinations only without a self term: GCN)
-        if ((s >= n_dst || !dself) && outdeg[s] == 1) continue;
+        if (s >= n_dst && outdeg[s] == 1) continue;  // written by the scatter's fast path
         const bool zero_row = inj && inj[s];
         ulonglong4* arow = reinterpret_cast<ulonglong4*>(acc + (int64_t)s * 2 * F);
         ulonglong4* lrow = arow + F4;
