@@ -246,7 +246,7 @@ extern "C" int hg_set_tuning(int32_t key, int32_t value) {
 }
 
 extern "C" int64_t hg_wgrad_tc_ws_size(int32_t K, int32_t N, int32_t M_cap, int32_t n_src) {
-    return (int64_t)n_src * hg_wgrad_tma_chunks(K, n_src, M_cap, N) * K * N;
+    return (int64_t)n_src * hg_wgrad_tma_chunks(K, n_src, M_cap) * K * N;
 }
 
 // out_s[K x N] = A_s[M x K]^T G[M x N] for s = 1 (A1) and, if A2, s = 2.

@@ -477,7 +477,7 @@ template <int BN, bool PAIR, bool TSA>
 __global__ void __launch_bounds__(WG_THREADS, 1)
 k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
             const __grid_constant__ CUtensorMap tmG, int K, int N, int ktiles, const int* __restrict__ d_M, int M_cap,
-            int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo, int n_nt) {
+            int n_chunks, float* __restrict__ partial, uint32_t lbo, uint32_t sbo) {
     constexpr int S = wg_stages<BN, TSA>();
     constexpr int STAGE = wg_stage_bytes<BN, TSA>();
     constexpr int GOFF = wg_goff<BN, TSA>();
@@ -493,11 +493,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
     __shared__ uint32_t s_tmem;
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int chunk = blockIdx.y;
-    // blockIdx.x = (src * ktiles + kt) * n_nt + nt: N wider than one tile runs as
-    // n_nt BN-wide column blocks of the same partial (more pipeline stages per CTA)
-    const int unit = blockIdx.x / n_nt, nt = blockIdx.x - unit * n_nt;
-    const int src = unit / ktiles, kt = unit - src * ktiles;
-    const int nb = nt * BN;  // first output column of this CTA
+    const int src = blockIdx.x / ktiles, kt = blockIdx.x - src * ktiles;
     const CUtensorMap* tmA = src ? &tmA2 : &tmA1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -548,7 +544,7 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 }
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
-                    tma_load_2d(smem_u32(base + GOFF + g * 4096), &tmG, nb + g * 32, y, &full[st]);
+                    tma_load_2d(smem_u32(base + GOFF + g * 4096), &tmG, g * 32, y, &full[st]);
             }
         }
     } else if (warp == 1) {
@@ -680,9 +676,9 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
                 for (int jj = 0; jj < 16; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __uint_as_float(p[jj]));
             }
             tmem_wait_ld();
-            if (gk < K && nb + c0 < N) {  // partials are N-major: lanes (consecutive k) store one 128-byte line
-                float* pcol = P + (int64_t)(nb + c0) * K + gk;
-                const int lim = N - (nb + c0);
+            if (gk < K && c0 < N) {  // partials are N-major: lanes (consecutive k) store one 128-byte line
+                float* pcol = P + (int64_t)c0 * K + gk;
+                const int lim = N - c0;
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj)
                     if (jj < lim) pcol[(int64_t)jj * K] = __uint_as_float(r[jj]);
@@ -818,7 +814,7 @@ int g_fwd_form = 1;  // 1: TS form for BN <= 128 (hg_set_tuning key 3), 0: SS fo
 template <int BN>
 int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMap& m2, const CUtensorMap& mg, int K,
               int N, int ktiles, const int* d_M, int M_cap, int n_chunks, float* partial, uint32_t lbo, uint32_t sbo,
-              bool tsa, int n_nt) {
+              bool tsa) {
     const int smem_ss = wg_stages<BN, false>() * wg_stage_bytes<BN, false>() + 1024;
     const int smem_ts = wg_stages<BN, true>() * wg_stage_bytes<BN, true>() + 1024;
     constexpr bool PB = BN <= 64;
@@ -832,7 +828,7 @@ int launch_wg(dim3 grid, cudaStream_t s, const CUtensorMap& m1, const CUtensorMa
     }
 #define HG_WG(P, T)                                                                                                  \
     hg_launch(k_wgrad_tma<BN, P, T>, grid, WG_THREADS, T ? smem_ts : smem_ss, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, \
-              n_chunks, partial, lbo, sbo, n_nt)
+              n_chunks, partial, lbo, sbo)
     const bool pair = g_pair && PB;
     if (pair && tsa) HG_WG(PB, true);
     else if (pair) HG_WG(PB, false);
@@ -892,17 +888,9 @@ int hg_gemm_tma_launch(const float* A1, int lda1, int K1, const float* A2, int l
 // it by the layer's row count — >= 128/256/512 rows per chunk for the small
 // upper layers — measured slower in the pipelined step: 178.5/179.4/185.4 vs
 // 178.1 us; the side-stream weight gradients are latency-, not SM-time-bound.)
-#ifndef HG_WG_MAX_BN
-#define HG_WG_MAX_BN 128  // widest weight-gradient N tile; wider N: several tiles per (source, K tile, chunk)
-#endif
-int hg_wgrad_tma_ntiles(int N) {
-    const int Nr = (N + 15) & ~15;
-    return Nr <= HG_WG_MAX_BN ? 1 : hg_ceil_div(Nr, HG_WG_MAX_BN);
-}
-
-int hg_wgrad_tma_chunks(int K, int n_src, int M_cap, int N) {
+int hg_wgrad_tma_chunks(int K, int n_src, int M_cap) {
     (void)M_cap;
-    const int units = hg_ceil_div(K > 0 ? K : 1, 128) * n_src * hg_wgrad_tma_ntiles(N);
+    const int units = hg_ceil_div(K > 0 ? K : 1, 128) * n_src;
     const int c = HG_NUM_SMS / units;
     return c < 1 ? 1 : c;
 }
@@ -912,8 +900,7 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
                         cudaStream_t s) {
     const int n_src = A2 ? 2 : 1;
     const int ktiles = hg_ceil_div(K, 128);
-    const int n_chunks = hg_wgrad_tma_chunks(K, n_src, M_cap, N);
-    const int n_nt = hg_wgrad_tma_ntiles(N);
+    const int n_chunks = hg_wgrad_tma_chunks(K, n_src, M_cap);
     if (M_cap > 0) {
         CUtensorMap m1, m2, mg;
         const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
@@ -926,12 +913,12 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
         if (!A2) m2 = m1;
         if (!rc) rc = make_map(&mg, G, N, M_cap, ldg, 32, 32, sw);
         if (rc) return rc;
-        const int Nr = n_nt > 1 ? HG_WG_MAX_BN : (N + 15) & ~15;  // the tile width
-        dim3 grid(ktiles * n_src * n_nt, n_chunks);
-        if (Nr <= 32) rc = launch_wg<32>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa, n_nt);
-        else if (Nr <= 64) rc = launch_wg<64>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa, n_nt);
-        else if (Nr <= 128) rc = launch_wg<128>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa, n_nt);
-        else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa, n_nt);
+        const int Nr = (N + 15) & ~15;
+        dim3 grid(ktiles * n_src, n_chunks);
+        if (Nr <= 32) rc = launch_wg<32>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
+        else if (Nr <= 64) rc = launch_wg<64>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
+        else if (Nr <= 128) rc = launch_wg<128>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
+        else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
         if (rc) return rc;
     }
     hg_launch(k_wgrad_tma_reduce, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K, N, n_chunks, d_M, M_cap,

@@ -24,7 +24,7 @@ void hg_tma_set_dbg(int v);
 void hg_tma_set_wg_tsa(int v);
 int hg_gemm_tma_launch(const float* A1, int lda1, int K1, const float* A2, int lda2, int K2, const uint8_t* bimg,
                        float* C, int ldc, int N, const int* d_M, int M_cap, int act, cudaStream_t s);
-int hg_wgrad_tma_chunks(int K, int n_src, int M_cap, int N);
+int hg_wgrad_tma_chunks(int K, int n_src, int M_cap);
 int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, int K, const float* G, int ldg, int N,
                         const int* d_M, int M_cap, float* out1, float* out2, float* ws, uint32_t lbo, uint32_t sbo,
                         cudaStream_t s);
