@@ -202,7 +202,15 @@ def run_reference(args, rank, world):
     ds = make_dataset(args.workload, cache_dir=CACHE)
     batches, rs = epoch_batches(ds, args.warmup + args.steps)
     budget = float(os.environ.get("HG_REF_BUDGET_S", "120"))
+    # every host core for the reference's BLAS (torchrun exports OMP_NUM_THREADS=1 to each rank)
+    try:
+        from threadpoolctl import threadpool_limits
+        limits = threadpool_limits(limits=host_cores())
+    except Exception:
+        limits = None
     v, steps, secs = cpu_reference_steps(ds, batches, rs, budget, args.steps, warmup=args.warmup, wl=wl["config"])
+    if limits is not None:
+        limits.restore_original_limits()
     line = {"metric": wl["metric"], "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * secs / max(steps, 1), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
