@@ -73,3 +73,35 @@ def test_sharded_step_equals_union_step_gloo(model):
         assert out["sage"] < 1e-12  # SAGE: sharded == union
     else:
         assert out["gcn"] > 1e-6   # GCN: block-local out-degree differs per shard (gnnmath.py:96)
+
+
+def _ctx_worker(rank, world, port, out):
+    """The product's DistContext host logic at world 2 on gloo: gradient all-reduce,
+    global-batch divisor, max over ranks, barrier, teardown."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    from paper_2311_13225_b200.parallel import DistContext
+    ctx = DistContext("gloo")
+    g = torch.full((4,), float(rank + 1), dtype=torch.float32)
+    ctx.allreduce(g)
+    local = shard(np.arange(1000), ctx.world, ctx.rank)
+    gb = ctx.global_batch(local)
+    ctx.set_global_batch(1000)
+    gb_strong = ctx.global_batch(local)
+    mx = ctx.max_over_ranks(float(rank) * 2.5)
+    ctx.barrier()
+    ctx.close()
+    out[rank] = (g.tolist(), int(local.shape[0]), gb, gb_strong, mx, torch.distributed.is_initialized())
+
+
+def test_dist_context_world2_gloo():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_ctx_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        g, n_local, gb, gb_strong, mx, still = out[r]
+        assert g == [3.0] * 4                 # sum over ranks
+        assert n_local == 500 and gb == 1000  # weak: world x local
+        assert gb_strong == 1000              # strong: the fixed global batch
+        assert mx == 2.5                      # max over ranks
+        assert not still                      # process group torn down
