@@ -62,6 +62,20 @@ struct FeatShards {
 #ifndef HG_AGG_U1
 #define HG_AGG_U1 8
 #endif
+// L2 prefetch of a destination's edge rows as soon as its edge list is known
+// (one prefetch.global.L2 per 128-byte line, no registers held): the rows past
+// the first U in flight are already on their way when the warp loads them.
+// Bottom aggregation 61.2 -> 60.3 us, C2 step -1 to -3 us (profiles/
+// r02s_occupancy_sweep.md); prefetching the next destination's rows or its
+// metadata, or before the self row copy, measured slower.
+#ifndef HG_AGG_PF
+#define HG_AGG_PF 1
+#endif
+__device__ __forceinline__ void prefetch_row_l2(const float4* p, int F4) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p), a1 = a0 + (uintptr_t)F4 * 16;
+    for (uintptr_t a = a0 & ~uintptr_t(127); a < a1; a += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+}
 #if defined(HG_AGG_MINB) && HG_AGG_MINB > 0  // experiment knob: register cap via min CTAs per SM
 #define HG_AGG_BOUNDS __launch_bounds__(256, HG_AGG_MINB)
 #else
@@ -121,6 +135,7 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
                     if (GCN) { my_row = GLOBAL ? sg : sl; my_w = gcn_w(outdeg[sl], cnt); }
                     else if (sg != v) { my_row = GLOBAL ? sg : sl; my_w = wd; }  // non-self edge
                 }
+                if (HG_AGG_PF && NV == 1 && !SH && my_row >= 0) prefetch_row_l2(rowp(my_row), F4);
                 const int m = min(LPR, cnt - j0);
                 // U rows in flight (a whole fanout-15 segment in one batch for F <= 128),
                 // consumed in edge order; slots past m are masked
