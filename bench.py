@@ -431,9 +431,11 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (agg_ms / 1000.0) / 1e9
-    traffic = None  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    # DRAM bytes per launch of the same kernel, this workload, from the committed ncu --set full capture
+    traffic, kernel_name = None, "k_agg_fwd (bottom fused gather + aggregation)"
     try:
-        traffic = float(json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["traffic_bytes_per_launch"])
+        rec = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())[args.workload]
+        traffic, kernel_name = float(rec["traffic_bytes_per_launch"]), rec["kernel"]
     except Exception:
         pass
     # kernels per step (graph kernel nodes) -> launches in the timed region
@@ -494,7 +496,7 @@ def main():
                            l2_flush=f"inputs > L2: {ds.num_vertices * ds.feat_dim * 4 / 1e9:.2f} GB feature table "
                                     f"+ {ds.num_edges * 4 / 1e9:.2f} GB CSR, random rows per step",
                            global_batch=global_batch, seeds_per_rank=n_loc),
-            "roofline": {"bound": "hbm", "kernel": "k_agg_fwd (bottom fused gather+mean, SAGE)",
+            "roofline": {"bound": "hbm", "kernel": kernel_name,
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": agg_ms,
@@ -504,12 +506,6 @@ def main():
                                           "with the sample and train halves back to back (the headline pass "
                                           "overlaps them)",
                          "frac_vs_spec_8tbs": achieved / 8000.0,
-                         "random_row_ceiling": {"gbs_of_row_data": 4000.0,
-                                                "source": "profiles/r01_gather_ceiling.txt (738K uniformly random "
-                                                          "400-byte rows, no compute: 72.6-75.8 us); cost per 128-B "
-                                                          "line touched: profiles/r02s_gather_rowsize.txt; this "
-                                                          "block's own fetch list as a pure gather: 55-61 us, "
-                                                          "profiles/r02_order_probe.txt"},
                          "block0": {"n_dst": n_dst0, "n_src": n_src0, "edges": E0},
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
             "cpu_baseline": cpu_base,
@@ -521,6 +517,12 @@ def main():
             "kernels_per_step": per_step,
             "clocks": clk,
             "final_loss": losses[-1]}
+    if args.workload == "c2":  # measured for C2's 400-byte rows
+        line["roofline"]["random_row_ceiling"] = {
+            "gbs_of_row_data": 4000.0,
+            "source": "profiles/r01_gather_ceiling.txt (738K uniformly random 400-byte rows, no compute: "
+                      "72.6-75.8 us); cost per 128-B line touched: profiles/r02s_gather_rowsize.txt; this "
+                      "block's own fetch list as a pure gather: 55-61 us, profiles/r02_order_probe.txt"}
     if phases:
         line["phases_ms"] = phases
     print(json.dumps(line), flush=True)

@@ -220,6 +220,25 @@ __global__ void k_swr_rows(const int64_t* __restrict__ edge_src, const double* _
     }
 }
 
+// The bottom (global-id) aggregation grid is sized as one wave of CTAs
+// (agg_ctas_per_sm() per SM); a wide-row instantiation whose registers allow
+// fewer resident CTAs (k_agg_fwd<32,5,..> for C3's 602-float rows: 113
+// registers, 2 per SM) is clamped to what fits, so it too runs as one wave:
+// C3 bottom aggregation 80.9 -> 75.1 us (profiles/r02s_occupancy_sweep.md).
+template <typename K>
+void clamp_to_resident(cudaLaunchConfig_t& cfg, K kernel, int& per_sm) {  // per_sm: per-instantiation cache
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (int)cfg.blockDim.x,
+                                                          cfg.dynamicSmemBytes) != cudaSuccess) {
+            (void)cudaGetLastError();
+            per_sm = -1;
+        }
+    }
+    if (per_sm < 1) return;
+    const unsigned cap = (unsigned)per_sm * HG_NUM_SMS;
+    if (cfg.gridDim.x > cap) cfg.gridDim.x = cap;
+}
+
 template <int MODE, bool SH = false>
 int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld_in, int F4, const int* frontier,
                const int* d_n, int cap, int f, const int* counts, const int* slot_g, const int* slot_local,
@@ -243,6 +262,9 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
     cfg.numAttrs = na;
 #define HG_FWD(L, V)                                                                                      \
     if (LPR == L && NV == V) {                                                                            \
+        static int per_sm = 0;                                                                            \
+        if (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL)                                                \
+            clamp_to_resident(cfg, k_agg_fwd<L, V, MODE, SH>, per_sm);                                    \
         cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE, SH>, hin, ld_in, F4, frontier, d_n, cap, f, counts, \
                            slot_g, slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, ld_agg,    \
                            shards);                                                                        \
