@@ -1,3 +1,4 @@
+#include <type_traits>
 // K8, warp-specialised TMA pipelines for the dense layer transforms.
 //
 // Same contracts as hg_gemm_tc.cu (fwd / dX: C = act(A1 op(B)[:K1] + A2 op(B)[K1:]);
@@ -694,34 +695,51 @@ k_wgrad_tma(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CU
     }
 }
 
-// Fixed-order reduction of the active chunks' partials (chunk order, then the
-// 8 warp sums in order): deterministic for a given M.  Partials are N-major
-// ([n][k], element e = n*K + k); the result is written row-major dW[k][n].
+// Fixed-order reduction of the active chunks' partials (chunk order within each
+// of the 8 warps, then the 8 warp sums in order): deterministic for a given M.
+// Partials are N-major ([n][k], element e = n*K + k); the result is written
+// row-major dW[k][n].  A block covers 32*VEC consecutive elements, VEC per lane
+// (VEC = 4: 16-byte loads, four chunk rows in flight per warp).
+template <int VEC>
 __global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restrict__ partial, int K, int N, int n_chunks,
                                                           const int* __restrict__ d_M, int M_cap,
                                                           float* __restrict__ out1, float* __restrict__ out2) {
+    constexpr int BE = 32 * VEC;  // elements per block
+    using VT = typename std::conditional<VEC == 4, float4, float>::type;
     const int KN = K * N;
     hg_pdl_begin();
-    __shared__ float s_part[8][33];
+    __shared__ float s_part[8][BE + 1];
     const int M = hg_load_count(d_M, M_cap);
     const int rpc = M > 0 ? wg_rows_per_chunk(M, n_chunks) : 1;
     const int chunks = M > 0 ? (M + rpc - 1) / rpc : 0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int per_src = (KN + 31) / 32;
+    const int per_src = (KN + BE - 1) / BE;
     const int s = blockIdx.x / per_src;
-    const int e = (blockIdx.x - s * per_src) * 32 + lane;
-    float acc = 0.f;
+    const int e0 = (blockIdx.x - s * per_src) * BE;
+    const int e = e0 + lane * VEC;  // KN % VEC == 0: a lane's VEC elements are all in range or all out
+    float acc[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
     if (e < KN) {
         const float* p = partial + (int64_t)s * n_chunks * KN + e;
-        for (int c = w; c < chunks; c += 8) acc += p[(int64_t)c * KN];
+#pragma unroll 4
+        for (int c = w; c < chunks; c += 8) {
+            const VT x = *reinterpret_cast<const VT*>(p + (int64_t)c * KN);
+            const float* xf = reinterpret_cast<const float*>(&x);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] += xf[v];
+        }
     }
-    s_part[w][lane] = acc;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) s_part[w][lane * VEC + v] = acc[v];
     __syncthreads();
-    if (w == 0 && e < KN) {
+    for (int i = threadIdx.x; i < BE; i += blockDim.x) {
+        const int ei = e0 + i;
+        if (ei >= KN) break;
         float t = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) t += s_part[i][lane];
-        const int n = e / K, k = e - n * K;
+        for (int r = 0; r < 8; ++r) t += s_part[r][i];
+        const int n = ei / K, k = ei - n * K;
         (s ? out2 : out1)[(int64_t)k * N + n] = t;
     }
 }
@@ -921,7 +939,11 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
         else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
         if (rc) return rc;
     }
-    hg_launch(k_wgrad_tma_reduce, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K, N, n_chunks, d_M, M_cap,
-              out1, out2);
+    if (((K * N) & 3) == 0 && !(reinterpret_cast<uintptr_t>(ws) & 15))
+        hg_launch(k_wgrad_tma_reduce<4>, n_src * hg_ceil_div((long long)K * N, 128), 256, 0, s, ws, K, N, n_chunks, d_M,
+                  M_cap, out1, out2);
+    else
+        hg_launch(k_wgrad_tma_reduce<1>, n_src * hg_ceil_div((long long)K * N, 32), 256, 0, s, ws, K, N, n_chunks, d_M,
+                  M_cap, out1, out2);
     return hg_check_launch("wgrad_tma_reduce");
 }

@@ -47,9 +47,12 @@ def main():
     if os.environ.get("HG_WHATIF_SKIP"):
         install_skips(os.environ["HG_WHATIF_SKIP"])
     K = 100
-    ds = make_dataset("c2", cache_dir=bench.CACHE)
-    cfg = TrainConfig(model="sage", layers=3, fanouts=(15, 10, 5), hidden_dim=64, batch_size=1024, lr=0.01,
-                      strategy="case1", hot_ratio=0.0, use_graph=True, seed=0, report_transfers=False)
+    workload = os.environ.get("HG_PROBE_WORKLOAD", "c2")
+    wl = bench.WORKLOADS[workload]["config"]
+    ds = make_dataset(workload, cache_dir=bench.CACHE)
+    cfg = TrainConfig(model=wl["model"], layers=wl["layers"], fanouts=tuple(wl["fanouts"]), hidden_dim=wl["hidden"],
+                      batch_size=1024, lr=wl["lr"], strategy="case1", hot_ratio=0.0, use_graph=True, seed=0,
+                      report_transfers=False)
     tr = Trainer(ds, cfg)
     e = tr.engine
     batches, rseeds = bench.epoch_batches(ds, K + 4)
