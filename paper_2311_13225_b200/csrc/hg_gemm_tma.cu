@@ -939,7 +939,10 @@ int hg_wgrad_tma_launch(const float* A1, int lda1, const float* A2, int lda2, in
         else rc = launch_wg<256>(grid, s, m1, m2, mg, K, N, ktiles, d_M, M_cap, n_chunks, ws, lbo, sbo, tsa);
         if (rc) return rc;
     }
-    if (((K * N) & 3) == 0 && !(reinterpret_cast<uintptr_t>(ws) & 15))
+    // 16-byte lanes only when that still leaves >= 2 blocks per SM (C3's bottom layer:
+    // 1,204 blocks); the small C2 layers keep one float per lane and 4x the blocks
+    const long long blocks4 = n_src * hg_ceil_div((long long)K * N, 128);
+    if (((K * N) & 3) == 0 && !(reinterpret_cast<uintptr_t>(ws) & 15) && blocks4 >= 2 * HG_NUM_SMS)
         hg_launch(k_wgrad_tma_reduce<4>, n_src * hg_ceil_div((long long)K * N, 128), 256, 0, s, ws, K, N, n_chunks, d_M,
                   M_cap, out1, out2);
     else
