@@ -1,5 +1,6 @@
 #!/bin/bash
-# A/B of two bench.py versions (tools/bench_prev_tmp.py vs bench.py) x HG_AGG_CTAS_PER_SM, interleaved
+# A/B of two bench.py versions x HG_AGG_CTAS_PER_SM, interleaved; make the old one with
+#   git show <rev>:bench.py > tools/bench_prev_tmp.py  (and ROOT = parents[1] in it)
 R=${R:-2}
 for i in $(seq 1 $R); do
   for c in ${CTAS:-5 4 3}; do
