@@ -722,12 +722,23 @@ __global__ void __launch_bounds__(256) k_wgrad_tma_reduce(const float* __restric
     for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
     if (e < KN) {
         const float* p = partial + (int64_t)s * n_chunks * KN + e;
-#pragma unroll 4
-        for (int c = w; c < chunks; c += 8) {
-            const VT x = *reinterpret_cast<const VT*>(p + (int64_t)c * KN);
-            const float* xf = reinterpret_cast<const float*>(&x);
+        // G chunk rows per batch, all loads issued before the in-order sums: one
+        // memory latency per batch instead of one per chunk
+        constexpr int G = 16 / VEC;
+        for (int c0 = w; c0 < chunks; c0 += 8 * G) {
+            VT x[G];
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] += xf[v];
+            for (int u = 0; u < G; ++u) {
+                const int c = c0 + 8 * u;
+                if (c < chunks) x[u] = *reinterpret_cast<const VT*>(p + (int64_t)c * KN);
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                if (c0 + 8 * u >= chunks) break;
+                const float* xf = reinterpret_cast<const float*>(&x[u]);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[v] += xf[v];
+            }
         }
     }
 #pragma unroll
