@@ -51,7 +51,14 @@ struct FeatShards {
     const float* base[HG_MAX_SHARDS];
     int n;
     int rows_per_shard;
+    // split rows (AD_SPLIT): columns [0, 4*body4) in the line-aligned body table
+    // (hin, stride ld_in), columns [4*body4, F) in the tail table (stride tail_ld)
+    const float* tail;
+    int tail_ld;
+    int body4;
 };
+// Row addressing of the feature gather: one table, row-sharded tables, or split rows.
+enum { AD_PLAIN = 0, AD_SHARDED = 1, AD_SPLIT = 2 };
 
 // Rows in flight per warp when a whole row is one float4 per lane (F <= 128, LPR 32):
 // 8, not 16 — the kernel then needs 48 registers instead of 64, five 256-thread
@@ -81,19 +88,32 @@ __device__ __forceinline__ void prefetch_row_l2(const float4* p, int F4) {
 #else
 #define HG_AGG_BOUNDS __launch_bounds__(256)
 #endif
-template <int LPR, int NV, int MODE, bool SH = false>
+template <int LPR, int NV, int MODE, int AD = AD_PLAIN>
 __global__ void HG_AGG_BOUNDS k_agg_fwd(
     const float* __restrict__ hin, int ld_in, int F4, const int* __restrict__ frontier, const int* d_n, int cap,
     int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ slot_local,
     const int* __restrict__ nself, const int* __restrict__ outdeg, const uint8_t* __restrict__ inj,
     float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out, int ld_agg, const FeatShards shards) {
     hg_pdl_begin();
+    constexpr bool SH = AD == AD_SHARDED, SPLIT = AD == AD_SPLIT;
     auto rowp = [&](int v) -> const float4* {
         if (SH) {
             const int k = v / shards.rows_per_shard;
             return reinterpret_cast<const float4*>(shards.base[k] + (int64_t)(v - k * shards.rows_per_shard) * ld_in);
         }
         return reinterpret_cast<const float4*>(hin + (int64_t)v * ld_in);
+    };
+    // float4 column c of row v.  Split rows (one float4 per lane, c == lane's column):
+    // the lane's column lives in the body's whole 128-byte lines or in the tail
+    // table, fixed per lane, so the address is one base + v * stride as for a plain row.
+    static_assert(!SPLIT || NV == 1, "split rows: one float4 column per lane");
+    const int lr0 = threadIdx.x & (LPR - 1);
+    const bool in_tail = SPLIT && lr0 >= shards.body4;
+    const float* lbase = in_tail ? shards.tail + (lr0 - shards.body4) * 4 : hin + lr0 * 4;
+    const int64_t lstride = in_tail ? shards.tail_ld : ld_in;
+    auto colp = [&](int v, int c) -> const float4* {
+        if (SPLIT) return reinterpret_cast<const float4*>(lbase + (int64_t)v * lstride);
+        return rowp(v) + c;
     };
     constexpr bool GLOBAL = (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL);
     constexpr bool GCN = (MODE == M_GCN_LOCAL || MODE == M_GCN_GLOBAL);
@@ -114,12 +134,11 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
         const int64_t sbase = (int64_t)i * f;
         if (!skip) {
             if (GLOBAL && self_out) {  // self row gather (the SAGE/GCN-free "gather" part)
-                const float4* src = rowp(v);
                 float4* dst = reinterpret_cast<float4*>(self_out + (int64_t)i * ld_self);
 #pragma unroll
                 for (int k = 0; k < NV; ++k) {
                     const int c = lr + k * LPR;
-                    if (c < F4) dst[c] = __ldg(src + c);
+                    if (c < F4) dst[c] = __ldg(colp(v, c));
                 }
             }
             const int cnt = counts[i];
@@ -135,7 +154,8 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
                     if (GCN) { my_row = GLOBAL ? sg : sl; my_w = gcn_w(outdeg[sl], cnt); }
                     else if (sg != v) { my_row = GLOBAL ? sg : sl; my_w = wd; }  // non-self edge
                 }
-                if (HG_AGG_PF && NV == 1 && !SH && my_row >= 0) prefetch_row_l2(rowp(my_row), F4);
+                if (HG_AGG_PF && NV == 1 && !SH && my_row >= 0)
+                    prefetch_row_l2(rowp(my_row), SPLIT ? shards.body4 : F4);  // split: tails are L2-persisting
                 const int m = min(LPR, cnt - j0);
                 // U rows in flight (a whole fanout-15 segment in one batch for F <= 128),
                 // consumed in edge order; slots past m are masked
@@ -152,11 +172,11 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
                     float4 x[U][NV];
 #pragma unroll
                     for (int t = 0; t < U; ++t) {
-                        const float4* rp = rowp(r[t] < 0 ? 0 : r[t]);
+                        const int rv = r[t] < 0 ? 0 : r[t];
 #pragma unroll
                         for (int k = 0; k < NV; ++k) {
                             const int c = lr + k * LPR;
-                            x[t][k] = (r[t] >= 0 && c < F4) ? __ldg(rp + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                            x[t][k] = (r[t] >= 0 && c < F4) ? __ldg(colp(rv, c)) : make_float4(0.f, 0.f, 0.f, 0.f);
                         }
                     }
 #pragma unroll
@@ -239,7 +259,7 @@ void clamp_to_resident(cudaLaunchConfig_t& cfg, K kernel, int& per_sm) {  // per
     if (cfg.gridDim.x > cap) cfg.gridDim.x = cap;
 }
 
-template <int MODE, bool SH = false>
+template <int MODE, int AD = AD_PLAIN>
 int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld_in, int F4, const int* frontier,
                const int* d_n, int cap, int f, const int* counts, const int* slot_g, const int* slot_local,
                const int* nself, const int* outdeg, const uint8_t* inj, float* self_out, int ld_self,
@@ -264,14 +284,18 @@ int launch_fwd(int LPR, int NV, dim3 g, cudaStream_t s, const float* hin, int ld
     if (LPR == L && NV == V) {                                                                            \
         static int per_sm = 0;                                                                            \
         if (MODE == M_SAGE_GLOBAL || MODE == M_GCN_GLOBAL)                                                \
-            clamp_to_resident(cfg, k_agg_fwd<L, V, MODE, SH>, per_sm);                                    \
-        cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE, SH>, hin, ld_in, F4, frontier, d_n, cap, f, counts, \
+            clamp_to_resident(cfg, k_agg_fwd<L, V, MODE, AD>, per_sm);                                    \
+        cudaLaunchKernelEx(&cfg, k_agg_fwd<L, V, MODE, AD>, hin, ld_in, F4, frontier, d_n, cap, f, counts, \
                            slot_g, slot_local, nself, outdeg, inj, self_out, ld_self, agg_out, ld_agg,    \
                            shards);                                                                        \
         return HG_OK;                                                                                     \
     }
-    HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 5) HG_FWD(32, 6)
-    HG_FWD(32, 8)
+    if constexpr (AD == AD_SPLIT) {  // split rows: one float4 per lane (F <= 128)
+        HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1)
+    } else {
+        HG_FWD(8, 1) HG_FWD(16, 1) HG_FWD(32, 1) HG_FWD(32, 2) HG_FWD(32, 4) HG_FWD(32, 5) HG_FWD(32, 6)
+        HG_FWD(32, 8)
+    }
 #undef HG_FWD
     return HG_EUNSUPPORTED;
 }
@@ -606,10 +630,53 @@ extern "C" int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard
     pick_lanes_fwd(F4, LPR, NV);
     dim3 g(hg_grid((long long)cap_dst * LPR, 256, agg_ctas_per_sm()));
     cudaStream_t s = (cudaStream_t)stream;
-    const int rc = model ? launch_fwd<M_GCN_GLOBAL, true>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh)
-                         : launch_fwd<M_SAGE_GLOBAL, true>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh);
+    const int rc = model ? launch_fwd<M_GCN_GLOBAL, AD_SHARDED>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh)
+                         : launch_fwd<M_SAGE_GLOBAL, AD_SHARDED>(LPR, NV, g, s, nullptr, ld_in, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh);
     if (rc) { hg_set_error("aggregate_fwd_sharded: unsupported width"); return rc; }
     return hg_check_launch("aggregate_fwd_sharded");
+}
+
+// hg_aggregate_fwd for the bottom layer over a split-row copy of the feature
+// table: columns [0, body_cols) of row v at body + v * ld_body (ld_body a
+// multiple of 32 floats and body 128-byte aligned, so a row's body is whole
+// 128-byte lines), columns [body_cols, F) at tail + v * ld_tail.  A 100-float
+// (400-byte) row otherwise always touches four 128-byte lines; split, it
+// touches three lines of the body plus a 16-byte tail whose table (V x 16 B)
+// is held in L2 by the persisting window (DeviceGraph.persist_hot_rows).  The
+// gather's DRAM cost is per line touched (profiles/r02s_gather_rowsize.txt).
+// Same items, weights and FMA order as hg_aggregate_fwd: bit-identical outputs.
+extern "C" int hg_aggregate_fwd_split(int32_t model, const float* body, int32_t ld_body, const float* tail,
+                                      int32_t ld_tail, int32_t body_cols, int32_t F, const int32_t* frontier,
+                                      const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
+                                      const int32_t* counts, const int32_t* slot_g, const int32_t* slot_local,
+                                      const int32_t* nself, const int32_t* outdeg, const uint8_t* inj_mask,
+                                      float* self_out, int32_t ld_self, float* agg_out, int32_t ld_agg,
+                                      void* stream) {
+    if (F % 4 || body_cols % 4 || ld_body % 4 || ld_tail % 4 || ld_agg % 4 || (self_out && ld_self % 4)) {
+        hg_set_error("aggregate_fwd_split: F, body_cols and row strides must be multiples of 4");
+        return HG_EINVAL;
+    }
+    if (body_cols <= 0 || body_cols >= F || ld_body < body_cols || ld_tail < F - body_cols || !body || !tail ||
+        (reinterpret_cast<uintptr_t>(body) & 15) || (reinterpret_cast<uintptr_t>(tail) & 15)) {
+        hg_set_error("aggregate_fwd_split: need 0 < body_cols < F, ld_body >= body_cols, ld_tail >= F - body_cols, "
+                     "16-byte aligned tables");
+        return HG_EINVAL;
+    }
+    if (F > 128) { hg_set_error("aggregate_fwd_split: F > 128 unsupported"); return HG_EUNSUPPORTED; }
+    if (cap_dst == 0) return HG_OK;
+    FeatShards sh{};
+    sh.tail = tail;
+    sh.tail_ld = ld_tail;
+    sh.body4 = body_cols / 4;
+    const int F4 = F / 4;
+    int LPR, NV;
+    pick_lanes_fwd(F4, LPR, NV);
+    dim3 g(hg_grid((long long)cap_dst * LPR, 256, agg_ctas_per_sm()));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int rc = model ? launch_fwd<M_GCN_GLOBAL, AD_SPLIT>(LPR, NV, g, s, body, ld_body, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh)
+                         : launch_fwd<M_SAGE_GLOBAL, AD_SPLIT>(LPR, NV, g, s, body, ld_body, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh);
+    if (rc) { hg_set_error("aggregate_fwd_split: unsupported width"); return rc; }
+    return hg_check_launch("aggregate_fwd_split");
 }
 
 extern "C" int64_t hg_swr_ws_size(int64_t n_edges, int32_t n_out) {

@@ -118,6 +118,16 @@ class DeviceGraph:
             return 0
         if max_bytes is None:
             max_bytes = int(float(os.environ.get("HG_L2_PERSIST_MB", "48")) * 2**20)
+        sp = self.split_rows()
+        if sp is not None:  # window over [tail table | first body rows] (hubs at low ids, graph.py:357)
+            nbytes = min(int(max_bytes), int(lib.hg_l2_persist_max()), sp["buf"].numel() * 4)
+            if nbytes <= 0:
+                _lib.call("hg_set_l2_persist", None, 0, 0.0)
+                return 0
+            hub_rows = max(0, nbytes - sp["tail_bytes"]) // (sp["body_cols"] * 4)
+            self.l2_window = (0, hub_rows)
+            _lib.call("hg_set_l2_persist", sp["buf"].data_ptr(), nbytes, float(hit_ratio))
+            return nbytes
         row = self.feat_ld * 4
         nbytes = min(int(max_bytes), int(lib.hg_l2_persist_max()), self.num_vertices * row)
         rows = nbytes // row
@@ -131,6 +141,39 @@ class DeviceGraph:
         _lib.call("hg_set_l2_persist", self.features[start].data_ptr(), rows * row, float(hit_ratio))
         return rows * row
 
+    def split_rows(self):
+        """Split-row copy of the feature table for the bottom gather
+        (``hg_aggregate_fwd_split``), or None when it does not apply.
+
+        A row of F_pad floats whose size is not a multiple of 128 bytes touches
+        ceil-plus-one 128-byte lines (400-byte C2 rows: always 4), and the random
+        gather's DRAM cost is per line touched (profiles/r02s_gather_rowsize.txt).
+        The copy keeps columns [0, 32*floor(F_pad/32)) as whole lines of a body
+        table and the last F_pad mod 32 (<= 8) columns in a tail table
+        (V x 16 B for C2: 38 MB) placed in front of the body in one allocation, so
+        the persisting L2 window covers the whole tail table plus the first (hub)
+        body rows.  Off with HG_SPLIT_ROWS=0; never used for row-sharded tables."""
+        if hasattr(self, "_split"):
+            return self._split
+        self._split = None
+        x = self.features
+        if x is None or os.environ.get("HG_SPLIT_ROWS", "1") == "0" or getattr(self, "shards", None) is not None:
+            return None
+        V, ld = x.shape
+        body_cols = ld // 32 * 32
+        tail_cols = ld - body_cols
+        if ld > 128 or body_cols == 0 or tail_cols == 0 or tail_cols > 8:
+            return None
+        tail_elems = (V * tail_cols + 31) // 32 * 32  # body starts 128-byte aligned
+        buf = torch.empty(tail_elems + V * body_cols, dtype=torch.float32, device=self.device)
+        tail = buf[:V * tail_cols].view(V, tail_cols)
+        body = buf[tail_elems:].view(V, body_cols)
+        tail.copy_(x[:, body_cols:])
+        body.copy_(x[:, :body_cols])
+        self._split = dict(buf=buf, body=body, tail=tail, body_cols=body_cols, tail_cols=tail_cols,
+                           tail_bytes=tail_elems * 4)
+        return self._split
+
     @classmethod
     def from_dataset(cls, ds, device=None):
         return cls(ds.offsets, ds.targets, ds.features, ds.labels, device=device)
@@ -139,6 +182,8 @@ class DeviceGraph:
         n = self.offsets.numel() * 8 + self.targets.numel() * 4 + self.minpos.nbytes()
         if self.features is not None:
             n += self.features.numel() * 4
+        if getattr(self, "_split", None) is not None:
+            n += self._split["buf"].numel() * 4
         if self.labels is not None:
             n += self.labels.numel() * 4
         return n
