@@ -152,20 +152,14 @@ int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard_ptrs, int3
 /* Bottom-layer hg_aggregate_fwd (orchestrator.py:239) over a split-row copy of the
  * feature table: columns [0, body_cols) of row v at body + v*ld_body (128-byte
  * aligned, ld_body a multiple of 32: whole 128-byte lines), columns [body_cols, F)
- * at tail + v*ld_tail (the small tail table is kept in L2).  F <= 128; n_rows = rows
- * of the table.  Outputs are bit-identical to hg_aggregate_fwd on the unsplit table,
- * except with HG_AGG_RANGES=K > 1 (SAGE): the gather then sweeps the source ids in
- * K range passes and each destination sums range by range (fp32 summation order). */
+ * at tail + v*ld_tail (the small tail table is kept in L2).  F <= 128.  Outputs are
+ * bit-identical to hg_aggregate_fwd on the unsplit table. */
 int hg_aggregate_fwd_split(int32_t model, const float* body, int32_t ld_body, const float* tail, int32_t ld_tail,
-                           int32_t body_cols, int32_t F, int32_t n_rows, const int32_t* frontier, const int32_t* d_n_dst,
+                           int32_t body_cols, int32_t F, const int32_t* frontier, const int32_t* d_n_dst,
                            int32_t cap_dst, int32_t fanout, const int32_t* counts, const int32_t* slot_g,
                            const int32_t* slot_local, const int32_t* nself, const int32_t* outdeg,
                            const uint8_t* inj_mask, float* self_out, int32_t ld_self, float* agg_out,
                            int32_t ld_agg, void* stream);
-/* Source-range passes of the split-row SAGE bottom gather (1 = off, the default;
- * env HG_AGG_RANGES sets the initial value).  Process-wide tuning knob. */
-int hg_set_agg_ranges(int32_t k);
-int hg_get_agg_ranges(void);
 /* CUDA IPC between the per-GPU processes (64-byte cudaIpcMemHandle_t blobs); the
  * handle names dptr's whole allocation and *out_offset locates dptr inside it */
 int hg_ipc_get_handle(const void* dptr, uint8_t* out_handle64, int64_t* out_offset);

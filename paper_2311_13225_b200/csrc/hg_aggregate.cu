@@ -204,209 +204,6 @@ __global__ void HG_AGG_BOUNDS k_agg_fwd(
     }
 }
 
-// ---------------------------------------------------------------------------
-// Source-range bucketed bottom gather (SAGE, rows by global id, F <= 128,
-// fanout <= 32).  The random row gather costs less when the rows fetched at
-// the same time come from a narrow id range (DRAM page locality, L2 reuse of
-// duplicates: profiles/r02_order_probe.txt, destination order 61.4 us vs 8
-// source ranges 55.3 us for the same fetch list).  Each warp owns up to
-// D destinations i = w + j*W (one wave of warps; D from the shared memory budget), keeps their
-// float4 accumulators in shared memory and sweeps the source ids in n_ranges
-// passes: in pass k it queues, destination by destination in slot order, the
-// non-self edges whose source lies in range k (ballot + shared-memory queue,
-// an L2 prefetch per queued row) and consumes the queue 8 rows in flight.  All
-// warps sweep the ranges at about the same pace, so at any moment the GPU
-// gathers from ~1/n_ranges of the table.  Per destination the sum runs range
-// by range, slot order within a range: deterministic, fp32 rounding differs
-// from the draw-order kernel only in summation order.  Destinations past W*D
-// (more than one wave can hold) run the plain per-destination loop.
-// ---------------------------------------------------------------------------
-int agg_ctas_per_sm();
-constexpr int RNG_THREADS = 256;
-constexpr int RNG_U = 8;
-// shared memory per CTA: 8 warps x (D destinations x F4 float4 accumulators + a 32-entry queue);
-// D is sized so five CTAs fit per SM (40 KB each: D = 11 for C2's 25 float4 columns)
-constexpr int RNG_SMEM_BUDGET = 40 * 1024;
-int rng_dests(int F4) {
-    int d = (RNG_SMEM_BUDGET / (RNG_THREADS / 32) - 32 * 12) / (F4 * 16);
-    return d < 1 ? 1 : (d > 32 ? 32 : d);
-}
-int rng_smem_bytes(int D, int F4) { return (RNG_THREADS / 32) * (D * F4 * 16 + 32 * 12); }
-
-template <int AD>
-__global__ void __launch_bounds__(RNG_THREADS, 5) k_agg_fwd_rng(
-    const float* __restrict__ hin, int ld_in, int F4, const int* __restrict__ frontier, const int* d_n, int cap,
-    int f, const int* __restrict__ counts, const int* __restrict__ slot_g, const int* __restrict__ nself,
-    const uint8_t* __restrict__ inj, float* __restrict__ self_out, int ld_self, float* __restrict__ agg_out,
-    int ld_agg, const FeatShards shards, int n_ranges, int range_rows, int D) {
-    hg_pdl_begin();
-    constexpr bool SPLIT = AD == AD_SPLIT;
-    extern __shared__ float4 rng_smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int W = gridDim.x * (RNG_THREADS / 32);
-    const int w = blockIdx.x * (RNG_THREADS / 32) + wib;
-    const int n = hg_load_count(d_n, cap);
-    float4* acc = rng_smem + wib * D * F4;
-    int* q_row = reinterpret_cast<int*>(rng_smem + (RNG_THREADS / 32) * D * F4) + wib * 96;
-    int* q_j = q_row + 32;
-    float* q_w = reinterpret_cast<float*>(q_row + 64);
-    const bool in_tail = SPLIT && lane >= shards.body4;
-    const float* lbase = in_tail ? shards.tail + (lane - shards.body4) * 4 : hin + lane * 4;
-    const int64_t lstride = in_tail ? shards.tail_ld : ld_in;
-    auto colp = [&](int v) { return reinterpret_cast<const float4*>(lbase + (int64_t)v * lstride); };
-    const int body4 = SPLIT ? shards.body4 : F4;
-    const bool col = lane < F4;
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    // destination j of this warp lives in lane j's registers: vertex, count (-1 skipped, -2 absent), 1/nself
-    int my_v = 0, my_cnt = -2;
-    float my_wd = 0.f;
-    {
-        const int i = w + lane * W;
-        if (lane < D && i < n) {
-            my_v = frontier[i];
-            my_cnt = (inj && inj[i]) ? -1 : counts[i];
-            const int ns = nself[i];
-            my_wd = ns > 0 ? 1.0f / (float)ns : 0.f;
-        }
-    }
-    int nd = 0;  // destinations this warp owns in the bucketed part
-    for (int j = 0; j < D; ++j) {
-        const int cj = __shfl_sync(0xffffffffu, my_cnt, j);
-        if (cj == -2) break;
-        nd = j + 1;
-        if (col) acc[j * F4 + lane] = z4;
-        const int vj = __shfl_sync(0xffffffffu, my_v, j);  // all lanes (full-mask shuffle)
-        if (self_out && col) {
-            reinterpret_cast<float4*>(self_out + (int64_t)(w + j * W) * ld_self)[lane] = cj >= 0 ? __ldg(colp(vj)) : z4;
-        }
-    }
-    int qn = 0;
-    auto flush = [&]() {
-        __syncwarp();
-        for (int t0 = 0; t0 < qn; t0 += RNG_U) {
-            float4 x[RNG_U];
-#pragma unroll
-            for (int u = 0; u < RNG_U; ++u) {
-                const int t = t0 + u;
-                x[u] = (t < qn && col) ? __ldg(colp(q_row[t])) : z4;
-            }
-#pragma unroll
-            for (int u = 0; u < RNG_U; ++u) {
-                const int t = t0 + u;
-                if (t < qn && col) {
-                    float4* a = acc + q_j[t] * F4 + lane;
-                    *a = f4_fma(q_w[t], x[u], *a);
-                }
-            }
-        }
-        __syncwarp();
-        qn = 0;
-    };
-    for (int k = 0; k < n_ranges; ++k) {
-        const int lo = k * range_rows, hi = (k == n_ranges - 1) ? 0x7fffffff : lo + range_rows;
-        for (int j = 0; j < nd; ++j) {
-            const int cj = __shfl_sync(0xffffffffu, my_cnt, j);
-            if (cj <= 0) continue;
-            const int vj = __shfl_sync(0xffffffffu, my_v, j);
-            const float wj = __shfl_sync(0xffffffffu, my_wd, j);
-            const int sg = lane < cj ? slot_g[(int64_t)(w + j * W) * f + lane] : -1;
-            const bool m = lane < cj && sg != vj && sg >= lo && sg < hi;
-            const unsigned bal = __ballot_sync(0xffffffffu, m);
-            if (!bal) continue;
-            const int nm = __popc(bal);
-            if (qn + nm > 32) flush();
-            if (m) {
-                const int pos = qn + __popc(bal & ((1u << lane) - 1u));
-                q_row[pos] = sg;
-                q_j[pos] = j;
-                q_w[pos] = wj;
-                if (HG_AGG_PF) prefetch_row_l2(reinterpret_cast<const float4*>(hin + (int64_t)sg * ld_in), body4);
-            }
-            qn += nm;
-        }
-        flush();
-    }
-    for (int j = 0; j < nd; ++j)
-        if (col) reinterpret_cast<float4*>(agg_out + (int64_t)(w + j * W) * ld_agg)[lane] = acc[j * F4 + lane];
-    // destinations beyond one wave's capacity: plain per-destination loop (slot order)
-    for (int i = w + D * W; i < n; i += W) {
-        const bool skip = inj && inj[i];
-        const int v = frontier[i];
-        float4 a = z4;
-        if (!skip) {
-            if (self_out && col) reinterpret_cast<float4*>(self_out + (int64_t)i * ld_self)[lane] = __ldg(colp(v));
-            const int cnt = counts[i], ns = nself[i];
-            const float wd = ns > 0 ? 1.0f / (float)ns : 0.f;
-            for (int j0 = 0; j0 < cnt; j0 += 4) {  // 4 rows in flight, slot order
-                float4 x[4];
-                bool use[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int sg = j0 + u < cnt ? slot_g[(int64_t)i * f + j0 + u] : v;
-                    use[u] = sg != v && col;
-                    x[u] = use[u] ? __ldg(colp(sg)) : z4;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (use[u]) a = f4_fma(wd, x[u], a);
-            }
-        } else if (self_out && col) {
-            reinterpret_cast<float4*>(self_out + (int64_t)i * ld_self)[lane] = z4;
-        }
-        if (col) reinterpret_cast<float4*>(agg_out + (int64_t)i * ld_agg)[lane] = a;
-    }
-}
-
-// bucketed passes over the source ids for the bottom gather (1 = off): env HG_AGG_RANGES,
-// or hg_set_agg_ranges()
-int g_agg_ranges = -1;
-int agg_ranges() {
-    if (g_agg_ranges < 0) {
-        const char* e = getenv("HG_AGG_RANGES");
-        const int v = e ? atoi(e) : 1;
-        g_agg_ranges = v < 1 ? 1 : (v > 64 ? 64 : v);
-    }
-    return g_agg_ranges;
-}
-
-template <int AD>
-int launch_fwd_rng(cudaStream_t s, const float* hin, int ld_in, int F4, const int* frontier, const int* d_n, int cap,
-                   int f, const int* counts, const int* slot_g, const int* nself, const uint8_t* inj,
-                   float* self_out, int ld_self, float* agg_out, int ld_agg, const FeatShards& shards, int n_rows,
-                   int n_ranges) {
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (hg_l2_window_attr(&attr[na])) ++na;
-    if (hg_pdl_enabled()) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    const int D = rng_dests(F4), smem = rng_smem_bytes(D, F4);
-    static int per_sm_f4[33] = {};
-    int& per_sm = per_sm_f4[F4 < 32 ? F4 : 32];
-    if (per_sm == 0) {
-        cudaFuncSetAttribute(k_agg_fwd_rng<AD>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_agg_fwd_rng<AD>, RNG_THREADS, smem) !=
-                cudaSuccess || per_sm < 1) {
-            (void)cudaGetLastError();
-            per_sm = 1;
-        }
-    }
-    const int want = agg_ctas_per_sm();
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)((want < per_sm ? want : per_sm) * HG_NUM_SMS));
-    cfg.blockDim = dim3(RNG_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cfg.attrs = na ? attr : nullptr;
-    cfg.numAttrs = na;
-    const int range_rows = (n_rows + n_ranges - 1) / n_ranges;
-    cudaLaunchKernelEx(&cfg, k_agg_fwd_rng<AD>, hin, ld_in, F4, frontier, d_n, cap, f, counts, slot_g, nself, inj,
-                       self_out, ld_self, agg_out, ld_agg, shards, n_ranges, range_rows, D);
-    return HG_OK;
-}
-
 __global__ void k_swr_keys(const int64_t* __restrict__ edge_dst, long long n, uint32_t* __restrict__ keys,
                            int* __restrict__ vals) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
@@ -756,13 +553,6 @@ void pick_lanes(int F4, int& LPR, int& NV) {
 
 void hg_set_agg_bulk(int v) { g_agg_bulk = v ? 1 : 0; }
 
-extern "C" int hg_set_agg_ranges(int32_t k) {
-    if (k < 1 || k > 64) { hg_set_error("set_agg_ranges: 1..64"); return HG_EINVAL; }
-    g_agg_ranges = k;
-    return HG_OK;
-}
-extern "C" int hg_get_agg_ranges(void) { return agg_ranges(); }
-
 // model: 0 = SAGE (mean over non-self sampled neighbours), 1 = GCN (block sym-norm).
 // global_src: 1 = rows addressed by global id (bottom layer, reads the feature
 // table), 0 = by local src id (upper layers, reads the previous activation).
@@ -856,8 +646,7 @@ extern "C" int hg_aggregate_fwd_sharded(int32_t model, const float* const* shard
 // gather's DRAM cost is per line touched (profiles/r02s_gather_rowsize.txt).
 // Same items, weights and FMA order as hg_aggregate_fwd: bit-identical outputs.
 extern "C" int hg_aggregate_fwd_split(int32_t model, const float* body, int32_t ld_body, const float* tail,
-                                      int32_t ld_tail, int32_t body_cols, int32_t F, int32_t n_rows,
-                                      const int32_t* frontier,
+                                      int32_t ld_tail, int32_t body_cols, int32_t F, const int32_t* frontier,
                                       const int32_t* d_n_dst, int32_t cap_dst, int32_t fanout,
                                       const int32_t* counts, const int32_t* slot_g, const int32_t* slot_local,
                                       const int32_t* nself, const int32_t* outdeg, const uint8_t* inj_mask,
@@ -882,14 +671,8 @@ extern "C" int hg_aggregate_fwd_split(int32_t model, const float* body, int32_t 
     const int F4 = F / 4;
     int LPR, NV;
     pick_lanes_fwd(F4, LPR, NV);
-    cudaStream_t s = (cudaStream_t)stream;
-    const int nr = agg_ranges();
-    if (nr > 1 && model == 0 && fanout <= 32 && n_rows > 0) {  // source-range bucketed passes (SAGE)
-        launch_fwd_rng<AD_SPLIT>(s, body, ld_body, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, nself,
-                                 inj_mask, self_out, ld_self, agg_out, ld_agg, sh, n_rows, nr);
-        return hg_check_launch("aggregate_fwd_split(ranges)");
-    }
     dim3 g(hg_grid((long long)cap_dst * LPR, 256, agg_ctas_per_sm()));
+    cudaStream_t s = (cudaStream_t)stream;
     const int rc = model ? launch_fwd<M_GCN_GLOBAL, AD_SPLIT>(LPR, NV, g, s, body, ld_body, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh)
                          : launch_fwd<M_SAGE_GLOBAL, AD_SPLIT>(LPR, NV, g, s, body, ld_body, F4, frontier, d_n_dst, cap_dst, fanout, counts, slot_g, slot_local, nself, outdeg, inj_mask, self_out, ld_self, agg_out, ld_agg, sh);
     if (rc) { hg_set_error("aggregate_fwd_split: unsupported width"); return rc; }

@@ -380,7 +380,7 @@ class TrainEngine:
         sp = self.dg.split_rows() if hasattr(self.dg, "split_rows") else None
         if sp is not None and sp["body_cols"] + sp["tail_cols"] == self.ld[0]:  # line-aligned body + L2-held tail
             _lib.call("hg_aggregate_fwd_split", 0 if self.sage else 1, ptr(sp["body"]), sp["body_cols"],
-                      ptr(sp["tail"]), sp["tail_cols"], sp["body_cols"], self.ld[0], self.dg.num_vertices, ptr(fr), ptr(n),
+                      ptr(sp["tail"]), sp["tail_cols"], sp["body_cols"], self.ld[0], ptr(fr), ptr(n),
                       self.cap_dst[0], self.fan[0], ptr(smp.counts), ptr(smp.slots), ptr(smp.slot_local),
                       ptr(smp.nself), ptr(smp.outdeg), ptr(inj), ptr(sb if self.sage else None), self.ld[0],
                       ptr(ag), self.ld[0], s)
