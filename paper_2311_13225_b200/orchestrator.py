@@ -188,9 +188,14 @@ class HotProducer:
         # SAGE reads the chunk's neighbour rows by global id: draws only, no dedup
         self.smp.run(ids, None, seed_dev, 0, stream, cap_dst=c, dedup=not e.sage)
         model = 0 if e.sage else 1
-        _lib.call("hg_aggregate_fwd", model, 1, ptr(e.dg.features), e.dg.feat_ld, e.ld[0], ptr(ids), None, c,
-                  e.fan[0], ptr(self.smp.counts), ptr(self.smp.slots), ptr(self.smp.slot_local), ptr(self.smp.nself),
-                  ptr(self.smp.outdeg), None, ptr(self.self_buf), e.ld[0], ptr(self.agg), e.ld[0], s)
+        sp = e.dg.split_rows() if hasattr(e.dg, "split_rows") else None
+        blk = (ptr(ids), None, c, e.fan[0], ptr(self.smp.counts), ptr(self.smp.slots), ptr(self.smp.slot_local),
+               ptr(self.smp.nself), ptr(self.smp.outdeg), None, ptr(self.self_buf), e.ld[0], ptr(self.agg), e.ld[0], s)
+        if sp is not None and sp["body_cols"] + sp["tail_cols"] == e.ld[0]:  # same split-row gather as the step
+            _lib.call("hg_aggregate_fwd_split", model, ptr(sp["body"]), sp["body_cols"], ptr(sp["tail"]),
+                      sp["tail_cols"], sp["body_cols"], e.ld[0], *blk)
+        else:
+            _lib.call("hg_aggregate_fwd", model, 1, ptr(e.dg.features), e.dg.feat_ld, e.ld[0], *blk)
         w = self.snaps[snap]
         act = 1 if e.L > 1 else 0
         self.img.prep(ptr(w), d1, s)
