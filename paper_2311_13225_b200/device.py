@@ -93,9 +93,13 @@ class DeviceGraph:
             feats = np.asarray(features)
             V, F = feats.shape
             self.feat_dim = F
-            # row stride: multiple of HG_FEAT_ALIGN floats (default 4 = 16-byte rows
-            # for float4 loads); 8 / 32 align rows to 32-byte sectors / 128-byte lines
-            align = max(4, int(os.environ.get("HG_FEAT_ALIGN", "4")))
+            # row stride: multiple of HG_FEAT_ALIGN floats.  Default: 4 (16-byte rows for
+            # float4 loads) up to 128 features — narrower rows get the split-row copy
+            # (split_rows) — and 32 (whole 128-byte lines) for wider rows: C3's 602
+            # features as 608 floats touch 19 lines per row instead of 19.75 on average,
+            # bottom aggregation 74.8 -> 73.4 us, step 259.5 -> 255.8 us
+            # (profiles/r02t_c3_align.txt); the GEMMs pad K to 32 anyway.
+            align = max(4, int(os.environ.get("HG_FEAT_ALIGN", "32" if F > 128 else "4")))
             self.feat_ld = (F + align - 1) // align * align
             x = torch.zeros((V, self.feat_ld), dtype=torch.float32, device=self.device)
             x[:, :F] = torch.as_tensor(np.ascontiguousarray(feats, dtype=np.float32), device=self.device)
