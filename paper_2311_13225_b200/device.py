@@ -108,7 +108,7 @@ class DeviceGraph:
         # first-occurrence table for the dedup kernel (shared by sequential users)
         self.minpos = FirstOccurrenceTable(self.num_vertices, self.device)
 
-    def persist_hot_rows(self, max_bytes: int | None = None, hit_ratio: float = 1.0) -> int:
+    def persist_hot_rows(self, max_bytes: int | None = None, hit_ratio: float | None = None) -> int:
         """Pin the hottest contiguous block of feature rows in L2 (persisting
         access-policy window on the feature-gathering kernels).  Rows are chosen
         as the window of consecutive ids with the largest degree sum (sampled
@@ -122,6 +122,8 @@ class DeviceGraph:
             return 0
         if max_bytes is None:
             max_bytes = int(float(os.environ.get("HG_L2_PERSIST_MB", "48")) * 2**20)
+        if hit_ratio is None:  # fraction of the window's lines given the persisting property
+            hit_ratio = float(os.environ.get("HG_L2_HIT", "1.0"))
         sp = self.split_rows()
         if sp is not None:  # window over [tail table | first body rows] (hubs at low ids, graph.py:357)
             nbytes = min(int(max_bytes), int(lib.hg_l2_persist_max()), sp["buf"].numel() * 4)
