@@ -158,7 +158,8 @@ class DeviceGraph:
         table and the last F_pad mod 32 (<= 8) columns in a tail table
         (V x 16 B for C2: 38 MB) placed in front of the body in one allocation, so
         the persisting L2 window covers the whole tail table plus the first (hub)
-        body rows.  Off with HG_SPLIT_ROWS=0; never used for row-sharded tables."""
+        body rows.  Off with HG_SPLIT_ROWS=0; never used for row-sharded tables, nor when
+        the copy would take more than half of the free HBM (the plain table is then read)."""
         if hasattr(self, "_split"):
             return self._split
         self._split = None
@@ -171,6 +172,10 @@ class DeviceGraph:
         if ld > 128 or body_cols == 0 or tail_cols == 0 or tail_cols > 8:
             return None
         tail_elems = (V * tail_cols + 31) // 32 * 32  # body starts 128-byte aligned
+        need = (tail_elems + V * body_cols) * 4
+        free, _ = torch.cuda.mem_get_info(self.device)
+        if need > free // 2:  # a second copy of the table only while it leaves HBM to spare
+            return None
         buf = torch.empty(tail_elems + V * body_cols, dtype=torch.float32, device=self.device)
         tail = buf[:V * tail_cols].view(V, tail_cols)
         body = buf[tail_elems:].view(V, body_cols)
